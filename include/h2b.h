@@ -1,0 +1,164 @@
+/*
+ * h2b.h — C ABI of the B200-native H² boundary-operator matvec (libh2b.so).
+ *
+ * This is the drop-in boundary for the reference's H² application path:
+ *
+ *   strayfield.hmatrix.h2.h2_matvec(op: H2Matrix, x) -> y
+ *       /root/reference/pkg/src/strayfield/hmatrix/h2.py:186-244
+ *   H2Matrix.matvec(self, x)                       h2.py:74-75
+ *   H2Matrix.storage_bytes(self)                   h2.py:77-83
+ *   BoundaryOperator.apply / apply_operator        bem.py:255-256, 277-284
+ *
+ * The reference is pure Python and has no FFI of its own; these entry points
+ * are what its ctypes layer binds.  Every argument is a
+ * plain pointer or integer — no torch, no numpy, no C++ types.
+ *
+ * Conventions
+ *  - All matrices are C-contiguous little-endian float64, exactly as the
+ *    reference stores them in H2Matrix (h2.py:35-42):
+ *      row_basis[c]     V_c  (|c| x k_row(c))   for leaf clusters
+ *      col_basis[c]     W_c  (|c| x k_col(c))   for leaf clusters
+ *      row_transfer[c]  E_c  (k_row(c) x k_row(parent(c)))   keyed by child c
+ *      col_transfer[c]  F_c  (k_col(c) x k_col(parent(c)))   keyed by child c
+ *      coupling b       S_b  (k_row(t) x k_col(s))
+ *      near b           N_b  (|t| x |s|)   (includes D = Psi/4pi - 1 on the
+ *                                          diagonal blocks, bem.py:232-234)
+ *  - Cluster ids are the reference's preorder ids (cluster.py:385-393).
+ *  - x / y are in ORIGINAL node order; perm maps tree position -> node
+ *    (cluster.py:42-59).  Multi-RHS vectors are node-major (n x nrhs).
+ *  - Return codes: 0 ok, H2B_EINVAL invalid argument (message in
+ *    h2b_last_error()), H2B_ECUDA CUDA error, H2B_ENCCL NCCL error,
+ *    H2B_ENOMEM host allocation failure, H2B_ENODEV no CUDA device.
+ *  - h2b_last_error() is thread-local.
+ */
+#ifndef H2B_H_
+#define H2B_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2B_ABI_VERSION 1
+
+#define H2B_OK 0
+#define H2B_EINVAL (-1)
+#define H2B_ECUDA (-2)
+#define H2B_ENCCL (-3)
+#define H2B_ENOMEM (-4)
+#define H2B_ENODEV (-5)
+
+/* One H2Matrix, as the reference holds it (h2.py:23-42, cluster.py:13-59).
+ * Host arrays; they are only read during h2b_create / h2b_plan_create and may
+ * be freed afterwards. */
+typedef struct h2b_desc {
+  int64_t n;                    /* H2Matrix.n == len(tree.perm)             */
+  int64_t nclusters;            /* len(tree.clusters), preorder             */
+  const int64_t* perm;          /* [n] tree.perm                            */
+  const int64_t* cl_start;      /* [nclusters] Cluster.start                */
+  const int64_t* cl_end;        /* [nclusters] Cluster.end                  */
+  const int64_t* cl_child;      /* [2*nclusters] children cids, -1 = none   */
+  const int64_t* k_row;         /* [nclusters] H2Matrix.row_rank(c)         */
+  const int64_t* k_col;         /* [nclusters] H2Matrix.col_rank(c)         */
+  const double* const* row_basis;    /* [nclusters] leaf V_c, NULL otherwise */
+  const double* const* col_basis;    /* [nclusters] leaf W_c, NULL otherwise */
+  const double* const* row_transfer; /* [nclusters] E_c for non-root c        */
+  const double* const* col_transfer; /* [nclusters] F_c for non-root c        */
+  int64_t ncoupling;            /* len(H2Matrix.coupling)                   */
+  const int64_t* cp_row;        /* [ncoupling] row cid                      */
+  const int64_t* cp_col;        /* [ncoupling] col cid                      */
+  const double* const* cp_data; /* [ncoupling] S_b                          */
+  int64_t nnear;                /* len(H2Matrix.near)                       */
+  const int64_t* nr_row;        /* [nnear] row cid                          */
+  const int64_t* nr_col;        /* [nnear] col cid                          */
+  const double* const* nr_data; /* [nnear] N_b                              */
+} h2b_desc;
+
+/* Execution-plan knobs.  Zero-initialise for defaults. */
+typedef struct h2b_options {
+  int64_t task_bytes;   /* max streamed bytes per work item (default 32768)  */
+  int32_t warps_per_cta;/* persistent CTA width in warps (default 8)         */
+  int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
+  int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
+  int32_t interleave;   /* 0 (default) = interleave near-field work items
+                           between far-field tree levels in the queue;
+                           -1 = far field first, near field after            */
+  /* Multi-GPU (one process per GPU).  world_size <= 1: whole operator. */
+  int32_t rank;
+  int32_t world_size;
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId shared by all ranks  */
+} h2b_options;
+
+typedef struct h2b_op h2b_op;      /* device-resident operator             */
+typedef struct h2b_plan h2b_plan;  /* host-only execution plan (no device) */
+
+typedef struct h2b_stats {
+  int64_t n;
+  int64_t stream_bytes;     /* == H2Matrix.storage_bytes() (h2.py:77-83)   */
+  int64_t pool_bytes;       /* matrix pool incl. alignment padding         */
+  int64_t coef_doubles;     /* coefficient workspace (x^, y^, partials)    */
+  int64_t ntasks;           /* work items in the persistent queue          */
+  int64_t nsegs;
+  int64_t ndeps;
+  int64_t tasks_by_kind[5]; /* up-leaf, up-node, down, near, final         */
+  int64_t bytes_by_kind[5];
+  int32_t grid;             /* persistent CTAs                             */
+  int32_t warps_per_cta;
+  int32_t rank, world_size;
+  int64_t local_bytes;      /* bytes this rank streams                     */
+} h2b_stats;
+
+/* Plan arrays for host-side inspection (tests execute them with a numpy
+ * interpreter to validate the layout without a GPU).  All pointers stay
+ * valid until h2b_plan_destroy.  Task/segment semantics: see DESIGN.md §4. */
+typedef struct h2b_plan_view {
+  int64_t ntasks, nsegs, ndeps, mat_len, coef_len;
+  const double* mat;        /* [mat_len] packed column-major matrix pool    */
+  const int64_t* t_data;    /* [ntasks] mat offset of (row0, col0)          */
+  const int64_t* t_out;     /* [ntasks] coef offset or tree position        */
+  const int64_t* t_bias;    /* [ntasks] coef offset of bias slot 0, or -1   */
+  const int32_t* t_m;       /* [ntasks] rows                                */
+  const int32_t* t_ld;      /* [ntasks] column stride                       */
+  const int32_t* t_ncols;   /* [ntasks]                                     */
+  const int32_t* t_kind;    /* [ntasks] 0 up-leaf 1 up-node 2 down 3 near 4 final */
+  const int32_t* t_seg0;    /* [ntasks+1] CSR into segments                 */
+  const int32_t* t_dep0;    /* [ntasks+1] CSR into deps                     */
+  const int32_t* t_bias_nslots;  /* [ntasks] */
+  const int32_t* t_bias_stride;  /* [ntasks] */
+  const int64_t* s_src;     /* [nsegs] tree position (x) or coef offset     */
+  const int32_t* s_ncols;   /* [nsegs]                                      */
+  const int32_t* s_kind;    /* [nsegs] 0 = x[perm[src+c]], 1 = coef slots   */
+  const int32_t* s_nslots;  /* [nsegs] slots summed (coef)                  */
+  const int32_t* s_stride;  /* [nsegs] slot stride (coef)                   */
+  const int32_t* deps;      /* [ndeps] task indices, all < dependent        */
+} h2b_plan_view;
+
+int h2b_abi_version(void);
+const char* h2b_last_error(void);
+
+/* Host-only planning (no CUDA calls; works on machines without a GPU). */
+int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out);
+int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* out);
+int h2b_plan_stats(const h2b_plan* p, h2b_stats* out);
+void h2b_plan_destroy(h2b_plan* p);
+
+/* Device operator on the current CUDA device (cudaSetDevice beforehand). */
+int h2b_create(const h2b_desc* d, const h2b_options* opt, h2b_op** out);
+/* y = M x with x, y device pointers (n x nrhs, node-major); asynchronous on
+ * `stream` (cudaStream_t, NULL = legacy default).  The timed path. */
+int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, void* stream);
+/* Synchronous host convenience (the drop-in path): copies x in, y out. */
+int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs);
+int64_t h2b_stream_bytes(const h2b_op* op);
+int h2b_stats_get(const h2b_op* op, h2b_stats* out);
+void h2b_destroy(h2b_op* op);
+
+/* Multi-GPU helper: fill a 128-byte NCCL unique id (rank 0 calls this and
+ * broadcasts the bytes to the other ranks, e.g. over torch.distributed). */
+int h2b_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2B_H_ */

@@ -1,0 +1,631 @@
+// h2b.cu — B200 (sm_100a) H² matvec: one persistent dataflow kernel + C ABI.
+//
+// The whole product y = M x (h2.py:186-244) is ONE kernel launch.  The host
+// planner (plan.cpp) turns every small GEMV of the reference's four loops into
+// a work item of the form
+//
+//     out[0:m] = bias[0:m] + A[0:m, 0:ncols] @ gather(segments)
+//
+// stored in a topologically ordered queue.  Persistent warps pull items with
+// an atomic ticket, wait (acquire) on the items they depend on, stream their
+// column-major slice of the matrix pool from HBM with 64-bit
+// ld.global.nc.L1::no_allocate loads, and publish (release) a per-item flag.
+// Near-field items (no dependencies, ~80% of the bytes) are interleaved
+// between the tree levels of the far field, so the level-by-level latency of
+// the upward/downward passes hides under the near-field stream.
+//
+// Lanes own rows (r = lane, lane + 32) so every column is a contiguous,
+// coalesced read and no cross-lane reduction is needed; small items
+// (m <= 16) pack several columns per warp instruction and reduce once.
+// Partial sums of split rows are written to separate slots and summed by the
+// consumer in a fixed order: results are deterministic, no float atomics.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/h2b.h"
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define H2B_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(H2B_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+struct __align__(16) DTask {
+  int64_t data;   // mat offset of (row0, col0)
+  int64_t out;    // coef offset (slot) or tree position (final)
+  int64_t bias;   // coef offset or -1
+  int32_t m, ld, ncols, kind;
+  int32_t seg0, seg1, dep0, dep1;
+  int32_t bias_nslots, bias_stride;
+};
+static_assert(sizeof(DTask) == 64, "DTask layout");
+
+struct __align__(8) DSeg {
+  int64_t src;
+  int32_t ncols;
+  int32_t kind;
+  int32_t nslots;
+  int32_t stride;
+};
+static_assert(sizeof(DSeg) == 24, "DSeg layout");
+
+struct Ctl {
+  unsigned ticket;
+  unsigned exited;
+  unsigned epoch;
+  unsigned pad;
+};
+
+struct KParams {
+  const DTask* __restrict__ tasks;
+  const DSeg* __restrict__ segs;
+  const int32_t* __restrict__ deps;
+  const double* __restrict__ mat;
+  double* coef;
+  const int64_t* __restrict__ perm;
+  const double* __restrict__ x;
+  double* y;
+  unsigned* flags;
+  Ctl* ctl;
+  int32_t ntasks;
+};
+
+constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
+
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One work item, NRHS right-hand sides, rows r0 = lane, r1 = lane + 32.
+template <int NRHS>
+__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, double* xs, double* red,
+                                         int lane) {
+  constexpr int kCols = kChunkBytes / (8 * NRHS);
+  const int m = T.m, ld = T.ld;
+  const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
+  const int G = grouped ? (32 / m) : 1;
+  const int g = grouped ? (lane / m) : 0;
+  const int rr = grouped ? (lane - g * m) : lane;
+  const bool v0 = grouped ? (g < G) : (lane < m);
+  const bool v1 = !grouped && (lane + 32 < m);
+
+  double acc0[NRHS], acc1[NRHS];
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) { acc0[r] = 0.0; acc1[r] = 0.0; }
+
+  // bias: near-field partial slots of a leaf (summed in slot order)
+  if (T.bias >= 0 && !grouped) {
+    for (int s = 0; s < T.bias_nslots; ++s) {
+      const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        if (v0) acc0[r] += __ldcg(b + (int64_t)lane * NRHS + r);
+        if (v1) acc1[r] += __ldcg(b + (int64_t)(lane + 32) * NRHS + r);
+      }
+    }
+  }
+
+  const double* A = p.mat + T.data;
+  int si = T.seg0, soff = 0;
+  for (int col = 0; col < T.ncols; col += kCols) {
+    const int cc = min(kCols, T.ncols - col);
+    // ---- gather the sources of columns [col, col + cc) into shared memory
+    int filled = 0;
+    while (filled < cc) {
+      const DSeg S = p.segs[si];
+      const int take = min(S.ncols - soff, cc - filled);
+      for (int j = lane; j < take * NRHS; j += 32) {
+        const int c = j / NRHS, r = j - c * NRHS;
+        double v;
+        if (S.kind == h2b::kSegX) {
+          const int64_t node = __ldg(p.perm + S.src + soff + c);
+          v = __ldg(p.x + node * NRHS + r);
+        } else {
+          v = 0.0;
+          for (int s = 0; s < S.nslots; ++s)
+            v += __ldcg(p.coef + (S.src + (int64_t)s * S.stride + soff + c) * NRHS + r);
+        }
+        xs[(filled + c) * NRHS + r] = v;
+      }
+      filled += take;
+      soff += take;
+      if (soff == S.ncols) { ++si; soff = 0; }
+    }
+    __syncwarp();
+    // ---- stream the matrix columns
+    const double* Ac = A + (int64_t)col * ld;
+    if (grouped) {
+      // G columns per step; lane (g, rr) reads element (rr, c0 + g): the
+      // warp touches G*m consecutive doubles.
+      int c = g;
+      for (; c + 7 * G < cc; c += 8 * G) {
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = v0 ? ld_stream(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc0[0] = fma(a[u], xs[c + u * G], acc0[0]);
+      }
+      for (; c < cc; c += G)
+        if (v0) acc0[0] = fma(ld_stream(Ac + (int64_t)c * m + rr), xs[c], acc0[0]);
+    } else {
+      int c = 0;
+      constexpr int U = (NRHS == 1) ? 8 : 4;
+      for (; c + U <= cc; c += U) {
+        double a0[U], a1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a0[u] = v0 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
+          a1[u] = v1 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            const double xv = xs[(c + u) * NRHS + r];
+            acc0[r] = fma(a0[u], xv, acc0[r]);
+            acc1[r] = fma(a1[u], xv, acc1[r]);
+          }
+        }
+      }
+      for (; c < cc; ++c) {
+        const double a0 = v0 ? ld_stream(Ac + (int64_t)c * ld + lane) : 0.0;
+        const double a1 = v1 ? ld_stream(Ac + (int64_t)c * ld + lane + 32) : 0.0;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          const double xv = xs[c * NRHS + r];
+          acc0[r] = fma(a0, xv, acc0[r]);
+          acc1[r] = fma(a1, xv, acc1[r]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  if (grouped) {
+    red[lane] = acc0[0];
+    __syncwarp();
+    double s = 0.0;
+    if (lane < m) {
+      for (int q = 0; q < G; ++q) s += red[q * m + lane];
+      if (T.bias >= 0)
+        for (int b = 0; b < T.bias_nslots; ++b)
+          s += __ldcg(p.coef + T.bias + (int64_t)b * T.bias_stride + lane);
+    }
+    __syncwarp();
+    acc0[0] = s;
+  }
+  const bool w0 = lane < m, w1 = lane + 32 < m;
+  if (T.kind == h2b::kFinal) {
+    if (w0) {
+      const int64_t node = __ldg(p.perm + T.out + lane);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc0[r];
+    }
+    if (w1) {
+      const int64_t node = __ldg(p.perm + T.out + lane + 32);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc1[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      if (w0) p.coef[(T.out + lane) * NRHS + r] = acc0[r];
+      if (w1) p.coef[(T.out + lane + 32) * NRHS + r] = acc1[r];
+    }
+  }
+}
+
+template <int NRHS>
+__global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  double* xs = smem + (size_t)wib * (kChunkBytes / 8);
+  double* red = smem + (size_t)nw * (kChunkBytes / 8) + wib * 32;
+
+  const unsigned done = *((volatile unsigned*)&p.ctl->epoch) + 1u;
+  int t = 0;
+  if (lane == 0) t = (int)atomicAdd(&p.ctl->ticket, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  while (t < p.ntasks) {
+    int tn = 0;
+    if (lane == 0) tn = (int)atomicAdd(&p.ctl->ticket, 1u);  // prefetch next ticket
+    const DTask T = p.tasks[t];
+    for (int d = T.dep0 + lane; d < T.dep1; d += 32) {
+      const unsigned* f = p.flags + __ldg(p.deps + d);
+      while (ld_acquire(f) != done) __nanosleep(32);
+    }
+    __syncwarp();
+    run_item<NRHS>(p, T, xs, red, lane);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(p.flags + t, done);
+    t = __shfl_sync(0xffffffffu, tn, 0);
+  }
+  if (lane == 0) {
+    const unsigned total = gridDim.x * (unsigned)nw;
+    __threadfence();
+    const unsigned prev = atomicAdd(&p.ctl->exited, 1u);
+    if (prev == total - 1) {
+      // every warp drew its terminating ticket: reset for the next launch
+      p.ctl->ticket = 0;
+      p.ctl->exited = 0;
+      __threadfence();
+      atomicAdd(&p.ctl->epoch, 1u);
+    }
+  }
+}
+
+template <int NRHS>
+size_t smem_bytes(int wpc) {
+  return (size_t)wpc * (kChunkBytes + 32 * 8);
+}
+
+}  // namespace
+
+struct h2b_op {
+  int device = 0;
+  int64_t n = 0;
+  int64_t ntasks = 0;
+  int64_t coef_len = 0;
+  int max_nrhs = 16;
+  int wpc = 8;
+  int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
+  double* d_mat = nullptr;
+  double* d_coef = nullptr;
+  DTask* d_tasks = nullptr;
+  DSeg* d_segs = nullptr;
+  int32_t* d_deps = nullptr;
+  int64_t* d_perm = nullptr;
+  unsigned* d_flags = nullptr;
+  Ctl* d_ctl = nullptr;
+  double* d_x = nullptr;
+  double* d_y = nullptr;
+  size_t xy_cap = 0;
+  std::mutex mu;
+  h2b_stats stats{};
+};
+
+struct h2b_plan {
+  h2b::Plan plan;
+  h2b_stats stats{};
+};
+
+namespace {
+
+h2b::PlanOptions to_plan_options(const h2b_options* o) {
+  h2b::PlanOptions po;
+  if (o) {
+    if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
+    po.interleave = o->interleave >= 0;  // 0 (zero-init) = default = interleave
+    po.rank = o->rank;
+    po.world_size = o->world_size > 0 ? o->world_size : 1;
+  }
+  return po;
+}
+
+void fill_stats(const h2b::Plan& P, h2b_stats* s) {
+  std::memset(s, 0, sizeof(*s));
+  s->n = P.n;
+  s->stream_bytes = P.stream_bytes;
+  s->pool_bytes = 8 * (int64_t)P.mat.size();
+  s->coef_doubles = P.coef_len;
+  s->ntasks = P.ntasks();
+  s->nsegs = P.nsegs();
+  s->ndeps = (int64_t)P.deps.size();
+  for (int k = 0; k < 5; ++k) {
+    s->tasks_by_kind[k] = P.tasks_by_kind[k];
+    s->bytes_by_kind[k] = P.bytes_by_kind[k];
+  }
+  s->rank = P.rank;
+  s->world_size = P.world_size;
+  s->local_bytes = P.local_bytes;
+}
+
+int nrhs_index(int nrhs) {
+  switch (nrhs) {
+    case 1: return 0;
+    case 2: return 1;
+    case 4: return 2;
+    case 8: return 3;
+    case 16: return 4;
+    default: return -1;
+  }
+}
+
+template <int NRHS>
+int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
+  const size_t sm = smem_bytes<NRHS>(wpc);
+  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0;
+  H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
+  int dev = 0, nsm = 0;
+  H2B_CUDA(cudaGetDevice(&dev));
+  H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (per_sm < 1) return fail(H2B_ECUDA, "kernel does not fit on an SM");
+  if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
+  *grid = per_sm * nsm;  // every CTA co-resident: required by the dependency waits
+  return H2B_OK;
+}
+
+template <int NRHS>
+int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+  KParams p;
+  p.tasks = op->d_tasks;
+  p.segs = op->d_segs;
+  p.deps = op->d_deps;
+  p.mat = op->d_mat;
+  p.coef = op->d_coef;
+  p.perm = op->d_perm;
+  p.x = x;
+  p.y = y;
+  p.flags = op->d_flags;
+  p.ctl = op->d_ctl;
+  p.ntasks = (int32_t)op->ntasks;
+  const int gi = nrhs_index(NRHS);
+  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem_bytes<NRHS>(op->wpc), st>>>(p);
+  H2B_CUDA(cudaGetLastError());
+  return H2B_OK;
+}
+
+template <typename T>
+int upload(T** dst, const T* src, size_t count) {
+  if (count == 0) count = 1;
+  H2B_CUDA(cudaMalloc((void**)dst, sizeof(T) * count));
+  if (src) H2B_CUDA(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+
+void free_op(h2b_op* op) {
+  if (!op) return;
+  cudaFree(op->d_mat);
+  cudaFree(op->d_coef);
+  cudaFree(op->d_tasks);
+  cudaFree(op->d_segs);
+  cudaFree(op->d_deps);
+  cudaFree(op->d_perm);
+  cudaFree(op->d_flags);
+  cudaFree(op->d_ctl);
+  cudaFree(op->d_x);
+  cudaFree(op->d_y);
+  delete op;
+}
+
+int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
+  if (!out) return fail(H2B_EINVAL, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(H2B_ENODEV, "no CUDA device available");
+  }
+  h2b::Plan P;
+  std::string err;
+  int rc = h2b::build_plan(d, to_plan_options(o), &P, &err);
+  if (rc != H2B_OK) return fail(rc, err);
+  if (P.ntasks() >= INT32_MAX) return fail(H2B_EINVAL, "too many work items");
+
+  std::unique_ptr<h2b_op, void (*)(h2b_op*)> op(new h2b_op(), free_op);
+  H2B_CUDA(cudaGetDevice(&op->device));
+  op->n = P.n;
+  op->ntasks = P.ntasks();
+  op->coef_len = P.coef_len;
+  op->max_nrhs = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
+  if (nrhs_index(op->max_nrhs) < 0) return fail(H2B_EINVAL, "max_nrhs must be 1, 2, 4, 8 or 16");
+  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
+  if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
+  const int cps = o ? o->ctas_per_sm : 0;
+
+  // device task / segment arrays
+  std::vector<DTask> tasks(P.ntasks());
+  for (int64_t i = 0; i < P.ntasks(); ++i) {
+    DTask& t = tasks[i];
+    t.data = P.t_data[i];
+    t.out = P.t_out[i];
+    t.bias = P.t_bias[i];
+    t.m = P.t_m[i];
+    t.ld = P.t_ld[i];
+    t.ncols = P.t_ncols[i];
+    t.kind = P.t_kind[i];
+    t.seg0 = P.t_seg0[i];
+    t.seg1 = P.t_seg0[i + 1];
+    t.dep0 = P.t_dep0[i];
+    t.dep1 = P.t_dep0[i + 1];
+    t.bias_nslots = P.t_bias_nslots[i];
+    t.bias_stride = P.t_bias_stride[i];
+  }
+  std::vector<DSeg> segs(P.nsegs());
+  for (int64_t i = 0; i < P.nsegs(); ++i) {
+    segs[i].src = P.s_src[i];
+    segs[i].ncols = P.s_ncols[i];
+    segs[i].kind = P.s_kind[i];
+    segs[i].nslots = P.s_nslots[i];
+    segs[i].stride = P.s_stride[i];
+  }
+  if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
+  if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
+  if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
+  if ((rc = upload(&op->d_deps, P.deps.data(), P.deps.size()))) return rc;
+  if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
+  if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
+  if ((rc = upload<unsigned>(&op->d_flags, nullptr, (size_t)P.ntasks()))) return rc;
+  if ((rc = upload<Ctl>(&op->d_ctl, nullptr, 1))) return rc;
+  H2B_CUDA(cudaMemset(op->d_flags, 0, sizeof(unsigned) * std::max<int64_t>(1, P.ntasks())));
+  H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
+  H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
+
+  if ((rc = occupancy_grid<1>(op->wpc, cps, &op->grid[0]))) return rc;
+  if ((rc = occupancy_grid<2>(op->wpc, cps, &op->grid[1]))) return rc;
+  if ((rc = occupancy_grid<4>(op->wpc, cps, &op->grid[2]))) return rc;
+  if ((rc = occupancy_grid<8>(op->wpc, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->wpc, cps, &op->grid[4]))) return rc;
+  H2B_CUDA(cudaDeviceSynchronize());
+
+  fill_stats(P, &op->stats);
+  op->stats.grid = op->grid[0];
+  op->stats.warps_per_cta = op->wpc;
+  *out = op.release();
+  return H2B_OK;
+}
+
+int matvec_dev_impl(h2b_op* op, const double* x, double* y, int nrhs, void* stream) {
+  if (!op) return fail(H2B_EINVAL, "null operator");
+  if (!x || !y) return fail(H2B_EINVAL, "null vector");
+  if (nrhs_index(nrhs) < 0 || nrhs > op->max_nrhs)
+    return fail(H2B_EINVAL, "nrhs must be 1, 2, 4, 8 or 16 and <= max_nrhs");
+  H2B_CUDA(cudaSetDevice(op->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (nrhs) {
+    case 1: return launch<1>(op, x, y, st);
+    case 2: return launch<2>(op, x, y, st);
+    case 4: return launch<4>(op, x, y, st);
+    case 8: return launch<8>(op, x, y, st);
+    default: return launch<16>(op, x, y, st);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2b_abi_version(void) { return H2B_ABI_VERSION; }
+
+const char* h2b_last_error(void) { return g_err.c_str(); }
+
+int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
+  if (!out) return fail(H2B_EINVAL, "null output pointer");
+  *out = nullptr;
+  try {
+    std::unique_ptr<h2b_plan> p(new h2b_plan());
+    std::string err;
+    int rc = h2b::build_plan(d, to_plan_options(opt), &p->plan, &err);
+    if (rc != H2B_OK) return fail(rc, err);
+    fill_stats(p->plan, &p->stats);
+    *out = p.release();
+    return H2B_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(H2B_ENOMEM, "host allocation failed while planning");
+  }
+}
+
+int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* v) {
+  if (!p || !v) return fail(H2B_EINVAL, "null argument");
+  const h2b::Plan& P = p->plan;
+  v->ntasks = P.ntasks();
+  v->nsegs = P.nsegs();
+  v->ndeps = (int64_t)P.deps.size();
+  v->mat_len = (int64_t)P.mat.size();
+  v->coef_len = P.coef_len;
+  v->mat = P.mat.data();
+  v->t_data = P.t_data.data();
+  v->t_out = P.t_out.data();
+  v->t_bias = P.t_bias.data();
+  v->t_m = P.t_m.data();
+  v->t_ld = P.t_ld.data();
+  v->t_ncols = P.t_ncols.data();
+  v->t_kind = P.t_kind.data();
+  v->t_seg0 = P.t_seg0.data();
+  v->t_dep0 = P.t_dep0.data();
+  v->t_bias_nslots = P.t_bias_nslots.data();
+  v->t_bias_stride = P.t_bias_stride.data();
+  v->s_src = P.s_src.data();
+  v->s_ncols = P.s_ncols.data();
+  v->s_kind = P.s_kind.data();
+  v->s_nslots = P.s_nslots.data();
+  v->s_stride = P.s_stride.data();
+  v->deps = P.deps.data();
+  return H2B_OK;
+}
+
+int h2b_plan_stats(const h2b_plan* p, h2b_stats* out) {
+  if (!p || !out) return fail(H2B_EINVAL, "null argument");
+  *out = p->stats;
+  return H2B_OK;
+}
+
+void h2b_plan_destroy(h2b_plan* p) { delete p; }
+
+int h2b_create(const h2b_desc* d, const h2b_options* opt, h2b_op** out) {
+  try {
+    return create_impl(d, opt, out);
+  } catch (const std::bad_alloc&) {
+    return fail(H2B_ENOMEM, "host allocation failed while creating the operator");
+  }
+}
+
+int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, void* stream) {
+  return matvec_dev_impl(op, x_dev, y_dev, nrhs, stream);
+}
+
+int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs) {
+  if (!op) return fail(H2B_EINVAL, "null operator");
+  if (n != op->n) return fail(H2B_EINVAL, "vector must have shape (" + std::to_string(op->n) + ",)");
+  if (!x_host || !y_host) return fail(H2B_EINVAL, "null vector");
+  std::lock_guard<std::mutex> lk(op->mu);
+  H2B_CUDA(cudaSetDevice(op->device));
+  const size_t bytes = sizeof(double) * (size_t)n * (size_t)std::max(1, nrhs);
+  if (op->xy_cap < bytes) {
+    cudaFree(op->d_x);
+    cudaFree(op->d_y);
+    op->d_x = op->d_y = nullptr;
+    op->xy_cap = 0;
+    H2B_CUDA(cudaMalloc(&op->d_x, bytes));
+    H2B_CUDA(cudaMalloc(&op->d_y, bytes));
+    op->xy_cap = bytes;
+  }
+  H2B_CUDA(cudaMemcpy(op->d_x, x_host, bytes, cudaMemcpyHostToDevice));
+  int rc = matvec_dev_impl(op, op->d_x, op->d_y, nrhs, nullptr);
+  if (rc != H2B_OK) return rc;
+  H2B_CUDA(cudaMemcpy(y_host, op->d_y, bytes, cudaMemcpyDeviceToHost));
+  return H2B_OK;
+}
+
+int64_t h2b_stream_bytes(const h2b_op* op) { return op ? op->stats.stream_bytes : -1; }
+
+int h2b_stats_get(const h2b_op* op, h2b_stats* out) {
+  if (!op || !out) return fail(H2B_EINVAL, "null argument");
+  *out = op->stats;
+  return H2B_OK;
+}
+
+void h2b_destroy(h2b_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->device);
+  cudaDeviceSynchronize();
+  free_op(op);
+}
+
+int h2b_nccl_unique_id(void* out128) {
+  if (!out128) return fail(H2B_EINVAL, "null argument");
+  return fail(H2B_ENCCL, "multi-GPU support is not built into this library yet");
+}
+
+}  // extern "C"

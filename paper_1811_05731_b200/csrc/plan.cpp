@@ -1,0 +1,471 @@
+// plan.cpp — builds the work-item queue for one H² operator (host only).
+//
+// Semantics follow the reference matvec h2_matvec (h2.py:186-244) exactly:
+//   forward   x^_leaf = W_t^T x|_t ; x^_p = sum_c F_c^T x^_c   (h2.py:195-209)
+//   coupling  y^_t   += S_b x^_s                               (h2.py:211-218)
+//   backward  coeff_c = E_c coeff_p + y^_c ; y|_t += V_t coeff  (h2.py:220-235)
+//   near      y|_t   += N_ts x|_s                              (h2.py:237-240)
+// The backward recursion's "coeff" of a cluster is materialised as the
+// vector y^_c (own coupling rows plus the transferred parent coefficient),
+// so coupling and the downward pass fuse into one item per cluster.
+#include "plan.h"
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <numeric>
+
+namespace h2b {
+namespace {
+
+struct Vec {
+  int64_t off = -1;   // coefficient-pool offset of slot 0
+  int32_t len = 0;    // entries per slot
+  int32_t nslots = 0; // partial sums to add
+  std::vector<int32_t> producers;  // provisional task ids
+  bool exists() const { return off >= 0 && len > 0; }
+};
+
+struct SegSpec {
+  int32_t kind;           // SegKind
+  int64_t src;            // tree position (x) or pool offset (coef)
+  int32_t ncols;
+  const Vec* vec;         // coef source (nullptr for x)
+  const double* a;        // source matrix block
+  bool transpose;         // false: a is (ncols x m) row-major == (m x ncols) col-major
+                          // true : a is (m x ncols) row-major with row stride a_ld
+  int64_t a_ld;
+};
+
+struct Piece {
+  int64_t col0 = 0, ncols = 0;
+  // (segment index, first column inside it, columns)
+  std::vector<std::array<int64_t, 3>> parts;
+};
+
+struct TaskTmp {
+  int64_t data, out, bias;
+  int32_t m, ld, ncols, kind, bias_nslots, bias_stride;
+  int32_t stage;
+  std::vector<int32_t> seg_idx;  // into seg tables
+  std::vector<int32_t> deps;     // provisional ids
+};
+
+class Builder {
+ public:
+  Builder(const h2b_desc* d, const PlanOptions& o, Plan* p) : d_(d), opt_(o), plan_(p) {}
+
+  int run(std::string* err);
+
+ private:
+  const h2b_desc* d_;
+  PlanOptions opt_;
+  Plan* plan_;
+
+  std::vector<int32_t> parent_, depth_, height_;
+  std::vector<int32_t> leaves_;             // preorder == position order
+  std::vector<Vec> xhat_, yhat_, nearv_;
+  std::vector<TaskTmp> tasks_;
+  // segment tables (final)
+  std::vector<int64_t> s_src_;
+  std::vector<int32_t> s_ncols_, s_kind_, s_nslots_, s_stride_;
+
+  int64_t size(int32_t c) const { return d_->cl_end[c] - d_->cl_start[c]; }
+  bool is_leaf(int32_t c) const { return d_->cl_child[2 * c] < 0; }
+
+  int validate(std::string* err);
+  void alloc_vec(Vec* v, int32_t len, int32_t nslots) {
+    v->len = len;
+    v->nslots = nslots;
+    v->off = plan_->coef_len;
+    plan_->coef_len += (int64_t)len * nslots;
+  }
+  // Packs the group's matrix, splits it into pieces, emits tasks.
+  void emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
+                  Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split);
+  void collect_leaves(int32_t c, std::vector<int32_t>* out) const {
+    if (is_leaf(c)) { out->push_back(c); return; }
+    collect_leaves((int32_t)d_->cl_child[2 * c], out);
+    collect_leaves((int32_t)d_->cl_child[2 * c + 1], out);
+  }
+};
+
+int Builder::validate(std::string* err) {
+  const h2b_desc* d = d_;
+  if (!d) { *err = "null descriptor"; return H2B_EINVAL; }
+  if (d->n < 1) { *err = "n must be >= 1"; return H2B_EINVAL; }
+  if (d->nclusters < 1 || d->nclusters > INT32_MAX / 2) { *err = "bad nclusters"; return H2B_EINVAL; }
+  if (!d->perm || !d->cl_start || !d->cl_end || !d->cl_child || !d->k_row || !d->k_col) {
+    *err = "null tree array"; return H2B_EINVAL;
+  }
+  const int64_t n = d->n, nc = d->nclusters;
+  {
+    std::vector<uint8_t> seen(n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t v = d->perm[i];
+      if (v < 0 || v >= n || seen[v]) { *err = "perm is not a permutation of range(n)"; return H2B_EINVAL; }
+      seen[v] = 1;
+    }
+  }
+  if (d->cl_start[0] != 0 || d->cl_end[0] != n) { *err = "cluster 0 must be the root [0, n)"; return H2B_EINVAL; }
+  parent_.assign(nc, -2);
+  depth_.assign(nc, 0);
+  height_.assign(nc, 0);
+  parent_[0] = -1;
+  // preorder walk with explicit stack; checks that children partition parents
+  std::vector<int32_t> order;
+  order.reserve(nc);
+  std::vector<int32_t> stack{0};
+  while (!stack.empty()) {
+    int32_t c = stack.back();
+    stack.pop_back();
+    order.push_back(c);
+    if (d->cl_start[c] < 0 || d->cl_end[c] > n || d->cl_start[c] >= d->cl_end[c]) {
+      *err = "cluster " + std::to_string(c) + " has an empty or out-of-range index range";
+      return H2B_EINVAL;
+    }
+    if (d->k_row[c] < 0 || d->k_col[c] < 0 || d->k_row[c] > INT32_MAX / 64 || d->k_col[c] > INT32_MAX / 64) {
+      *err = "negative or huge rank"; return H2B_EINVAL;
+    }
+    int64_t a = d->cl_child[2 * c], b = d->cl_child[2 * c + 1];
+    if (a < 0 && b < 0) {
+      if (d->cl_end[c] - d->cl_start[c] > INT32_MAX / 64) { *err = "leaf too large"; return H2B_EINVAL; }
+      continue;
+    }
+    if (a < 0 || b < 0 || a >= nc || b >= nc) { *err = "cluster " + std::to_string(c) + " must have 0 or 2 valid children"; return H2B_EINVAL; }
+    if (parent_[a] != -2 || parent_[b] != -2 || a == 0 || b == 0) { *err = "cluster tree is not a tree"; return H2B_EINVAL; }
+    if (d->cl_start[a] != d->cl_start[c] || d->cl_end[a] != d->cl_start[b] || d->cl_end[b] != d->cl_end[c]) {
+      *err = "children of cluster " + std::to_string(c) + " do not partition its range"; return H2B_EINVAL;
+    }
+    parent_[a] = c; parent_[b] = c;
+    depth_[a] = depth_[c] + 1; depth_[b] = depth_[c] + 1;
+    stack.push_back((int32_t)b);
+    stack.push_back((int32_t)a);
+  }
+  if ((int64_t)order.size() != nc) { *err = "clusters unreachable from the root"; return H2B_EINVAL; }
+  for (auto it = order.rbegin(); it != order.rend(); ++it) {
+    int32_t c = *it;
+    if (!is_leaf(c)) {
+      int32_t a = (int32_t)d->cl_child[2 * c], b = (int32_t)d->cl_child[2 * c + 1];
+      height_[c] = 1 + std::max(height_[a], height_[b]);
+    }
+  }
+  for (int32_t c : order) if (is_leaf(c)) leaves_.push_back(c);
+  // bases / transfers
+  for (int64_t c = 0; c < nc; ++c) {
+    if (is_leaf((int32_t)c)) {
+      if ((d->k_row[c] > 0 && (!d->row_basis || !d->row_basis[c])) ||
+          (d->k_col[c] > 0 && (!d->col_basis || !d->col_basis[c]))) {
+        *err = "missing leaf basis for cluster " + std::to_string(c); return H2B_EINVAL;
+      }
+    }
+    if (c != 0) {
+      int32_t p = parent_[c];
+      if ((d->k_row[c] * d->k_row[p] > 0 && (!d->row_transfer || !d->row_transfer[c])) ||
+          (d->k_col[c] * d->k_col[p] > 0 && (!d->col_transfer || !d->col_transfer[c]))) {
+        *err = "missing transfer matrix for cluster " + std::to_string(c); return H2B_EINVAL;
+      }
+    }
+  }
+  if (d->ncoupling < 0 || d->nnear < 0) { *err = "negative block count"; return H2B_EINVAL; }
+  for (int64_t b = 0; b < d->ncoupling; ++b) {
+    int64_t r = d->cp_row[b], s = d->cp_col[b];
+    if (r < 0 || r >= nc || s < 0 || s >= nc) { *err = "coupling block cluster id out of range"; return H2B_EINVAL; }
+    if (d->k_row[r] * d->k_col[s] > 0 && !d->cp_data[b]) { *err = "null coupling matrix"; return H2B_EINVAL; }
+  }
+  for (int64_t b = 0; b < d->nnear; ++b) {
+    int64_t r = d->nr_row[b], s = d->nr_col[b];
+    if (r < 0 || r >= nc || s < 0 || s >= nc) { *err = "near block cluster id out of range"; return H2B_EINVAL; }
+    if (!d->nr_data[b]) { *err = "null near-field matrix"; return H2B_EINVAL; }
+  }
+  return H2B_OK;
+}
+
+void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
+                         Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split) {
+  Plan& P = *plan_;
+  if (m_total <= 0) return;
+  // 1. pack the group matrix (m_total x C, column-major, ld = m_total)
+  int64_t C = 0;
+  for (auto& s : segs) C += s.ncols;
+  const int64_t base = (int64_t)P.mat.size();
+  P.mat.resize(base + (size_t)m_total * C);
+  double* dst = P.mat.data() + base;
+  for (auto& s : segs) {
+    const int64_t cnt = (int64_t)m_total * s.ncols;
+    if (!s.transpose) {
+      std::memcpy(dst, s.a, sizeof(double) * cnt);
+    } else {
+      for (int64_t j = 0; j < s.ncols; ++j)
+        for (int64_t i = 0; i < m_total; ++i) dst[j * m_total + i] = s.a[i * s.a_ld + j];
+    }
+    dst += cnt;
+  }
+  P.bytes_by_kind[kind] += 8 * (int64_t)m_total * C;
+  // 2. split columns into pieces of <= task_bytes (at segment boundaries when possible)
+  std::vector<Piece> pieces;
+  const int64_t maxc = allow_split ? std::max<int64_t>(1, opt_.task_bytes / (8 * (int64_t)m_total)) : INT64_MAX;
+  Piece cur;
+  int64_t col = 0;
+  for (int64_t si = 0; si < (int64_t)segs.size(); ++si) {
+    int64_t nc = segs[si].ncols, c0 = 0;
+    if (nc == 0) continue;
+    if (cur.ncols > 0 && cur.ncols + nc > maxc) { pieces.push_back(cur); cur = Piece(); cur.col0 = col; }
+    while (nc - c0 > 0) {
+      int64_t take = std::min(nc - c0, maxc - cur.ncols);
+      if (take <= 0) { pieces.push_back(cur); cur = Piece(); cur.col0 = col; continue; }
+      if (cur.ncols == 0) cur.col0 = col;
+      cur.parts.push_back({si, c0, take});
+      cur.ncols += take; c0 += take; col += take;
+    }
+  }
+  if (cur.ncols > 0 || pieces.empty()) pieces.push_back(cur);
+  // 3. output vector
+  if (outv) alloc_vec(outv, m_total, (int32_t)pieces.size());
+  // 4. tasks: one per (piece, row tile)
+  for (size_t pi = 0; pi < pieces.size(); ++pi) {
+    const Piece& pc = pieces[pi];
+    // segment records of this piece (shared by its row tiles)
+    std::vector<int32_t> seg_ids;
+    std::vector<int32_t> deps;
+    for (auto& part : pc.parts) {
+      const SegSpec& s = segs[part[0]];
+      seg_ids.push_back((int32_t)s_ncols_.size());
+      s_ncols_.push_back((int32_t)part[2]);
+      s_kind_.push_back(s.kind);
+      if (s.kind == kSegX) {
+        s_src_.push_back(s.src + part[1]);
+        s_nslots_.push_back(1);
+        s_stride_.push_back(0);
+      } else {
+        s_src_.push_back(s.vec->off + part[1]);
+        s_nslots_.push_back(s.vec->nslots);
+        s_stride_.push_back(s.vec->len);
+        deps.insert(deps.end(), s.vec->producers.begin(), s.vec->producers.end());
+      }
+    }
+    if (bias) deps.insert(deps.end(), bias->producers.begin(), bias->producers.end());
+    std::sort(deps.begin(), deps.end());
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    for (int32_t r0 = 0; r0 < m_total; r0 += kMaxRows) {
+      TaskTmp t;
+      t.data = base + pc.col0 * m_total + r0;
+      t.m = std::min<int32_t>(kMaxRows, m_total - r0);
+      t.ld = m_total;
+      t.ncols = (int32_t)pc.ncols;
+      t.kind = kind;
+      t.stage = stage;
+      t.out = outv ? outv->off + (int64_t)pi * m_total + r0 : y_pos + r0;
+      if (bias && bias->exists()) {
+        t.bias = bias->off + r0;
+        t.bias_nslots = bias->nslots;
+        t.bias_stride = bias->len;
+      } else {
+        t.bias = -1; t.bias_nslots = 0; t.bias_stride = 0;
+      }
+      t.seg_idx = seg_ids;
+      t.deps = deps;
+      if (outv) outv->producers.push_back((int32_t)tasks_.size());
+      tasks_.push_back(std::move(t));
+    }
+  }
+}
+
+int Builder::run(std::string* err) {
+  int rc = validate(err);
+  if (rc != H2B_OK) return rc;
+  const h2b_desc* d = d_;
+  Plan& P = *plan_;
+  const int64_t nc = d->nclusters;
+  P.n = d->n;
+  P.perm.assign(d->perm, d->perm + d->n);
+  P.rank = opt_.rank;
+  P.world_size = opt_.world_size;
+
+  // Algorithmic byte count, H2Matrix.storage_bytes() (h2.py:77-83).
+  int64_t entries = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    if (is_leaf((int32_t)c)) entries += size((int32_t)c) * (d->k_row[c] + d->k_col[c]);
+    if (c != 0) {
+      int32_t p = parent_[c];
+      entries += d->k_row[c] * d->k_row[p] + d->k_col[c] * d->k_col[p];
+    }
+  }
+  for (int64_t b = 0; b < d->ncoupling; ++b) entries += d->k_row[d->cp_row[b]] * d->k_col[d->cp_col[b]];
+  for (int64_t b = 0; b < d->nnear; ++b) entries += size((int32_t)d->nr_row[b]) * size((int32_t)d->nr_col[b]);
+  P.stream_bytes = 8 * entries;
+  P.mat.reserve((size_t)entries);
+
+  xhat_.assign(nc, Vec());
+  yhat_.assign(nc, Vec());
+  nearv_.assign(nc, Vec());
+
+  // ---- forward, leaves: x^_t = W_t^T x|_t (h2.py:199-200)
+  for (int32_t c : leaves_) {
+    int32_t k = (int32_t)d->k_col[c];
+    if (k == 0) continue;
+    std::vector<SegSpec> segs{{kSegX, d->cl_start[c], (int32_t)size(c), nullptr, d->col_basis[c], false, 0}};
+    emit_group(kUpLeaf, 0, k, segs, &xhat_[c], 0, nullptr, true);
+  }
+  // ---- forward, inner clusters bottom-up: x^_p = sum_c F_c^T x^_c (h2.py:201-205)
+  {
+    std::vector<int32_t> inner;
+    for (int32_t c = 0; c < nc; ++c) if (!is_leaf(c)) inner.push_back(c);
+    std::stable_sort(inner.begin(), inner.end(), [&](int32_t a, int32_t b) { return height_[a] < height_[b]; });
+    for (int32_t p : inner) {
+      int32_t k = (int32_t)d->k_col[p];
+      if (k == 0) continue;
+      std::vector<SegSpec> segs;
+      for (int j = 0; j < 2; ++j) {
+        int32_t ch = (int32_t)d->cl_child[2 * p + j];
+        if (!xhat_[ch].exists()) continue;
+        segs.push_back({kSegCoef, 0, (int32_t)d->k_col[ch], &xhat_[ch], d->col_transfer[ch], false, 0});
+      }
+      emit_group(kUpNode, height_[p], k, segs, &xhat_[p], 0, nullptr, true);
+    }
+  }
+  // ---- near field, grouped by target leaf (h2.py:237-240).  Blocks whose
+  // row cluster is not a leaf are split into their leaf row ranges.
+  {
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> by_leaf(nc);  // (block, row offset)
+    for (int64_t b = 0; b < d->nnear; ++b) {
+      int32_t r = (int32_t)d->nr_row[b];
+      if (is_leaf(r)) { by_leaf[r].push_back({b, 0}); continue; }
+      std::vector<int32_t> ls;
+      collect_leaves(r, &ls);
+      for (int32_t l : ls) by_leaf[l].push_back({b, d->cl_start[l] - d->cl_start[r]});
+    }
+    for (int32_t l : leaves_) {
+      if (by_leaf[l].empty()) continue;
+      std::vector<SegSpec> segs;
+      for (auto& br : by_leaf[l]) {
+        int64_t b = br.first;
+        int32_t s = (int32_t)d->nr_col[b];
+        int64_t ncol = size(s);
+        segs.push_back({kSegX, d->cl_start[s], (int32_t)ncol, nullptr, d->nr_data[b] + br.second * ncol, true, ncol});
+      }
+      emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true);
+    }
+  }
+  // ---- coupling + downward pass, top-down (h2.py:211-235)
+  {
+    std::vector<std::vector<int64_t>> cp_by_row(nc);
+    for (int64_t b = 0; b < d->ncoupling; ++b) cp_by_row[d->cp_row[b]].push_back(b);
+    std::vector<int32_t> order(nc);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return depth_[a] < depth_[b]; });
+    for (int32_t t : order) {
+      int32_t k = (int32_t)d->k_row[t];
+      if (k == 0) continue;
+      std::vector<SegSpec> segs;
+      if (t != 0) {
+        int32_t p = parent_[t];
+        if (yhat_[p].exists())
+          segs.push_back({kSegCoef, 0, (int32_t)d->k_row[p], &yhat_[p], d->row_transfer[t], true, d->k_row[p]});
+      }
+      for (int64_t b : cp_by_row[t]) {
+        int32_t s = (int32_t)d->cp_col[b];
+        if (!xhat_[s].exists()) continue;
+        int64_t ks = d->k_col[s];
+        segs.push_back({kSegCoef, 0, (int32_t)ks, &xhat_[s], d->cp_data[b], true, ks});
+      }
+      if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
+      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true);
+    }
+  }
+  // ---- leaf back-transform + near partials -> y (h2.py:227-229, 242-243)
+  for (int32_t l : leaves_) {
+    std::vector<SegSpec> segs;
+    int32_t k = (int32_t)d->k_row[l];
+    if (k > 0 && yhat_[l].exists())
+      segs.push_back({kSegCoef, 0, k, &yhat_[l], d->row_basis[l], true, k});
+    emit_group(kFinal, 0, (int32_t)size(l), segs, nullptr, d->cl_start[l], &nearv_[l], false);
+  }
+  // Entries never read by the product (e.g. row bases of an operator
+  // without coupling blocks) are not packed, so the pool can be smaller.
+  if ((int64_t)P.mat.size() > entries) {
+    *err = "internal: packed pool larger than storage_bytes";
+    return H2B_EINVAL;
+  }
+
+  // ---- queue order: up-leaf, [near chunk, chain stage]*, near chunk, final
+  const int32_t T = (int32_t)tasks_.size();
+  std::vector<int32_t> up_leaf, nearq, finalq;
+  std::vector<std::vector<int32_t>> stages;
+  int32_t max_h = 0, max_d = 0;
+  for (auto& t : tasks_) {
+    if (t.kind == kUpNode) max_h = std::max(max_h, t.stage);
+    if (t.kind == kDown) max_d = std::max(max_d, t.stage);
+  }
+  std::vector<std::vector<int32_t>> upn(max_h + 1), dn(max_d + 1);
+  for (int32_t i = 0; i < T; ++i) {
+    auto& t = tasks_[i];
+    switch (t.kind) {
+      case kUpLeaf: up_leaf.push_back(i); break;
+      case kUpNode: upn[t.stage].push_back(i); break;
+      case kDown: dn[t.stage].push_back(i); break;
+      case kNear: nearq.push_back(i); break;
+      default: finalq.push_back(i); break;
+    }
+  }
+  for (auto& v : upn) if (!v.empty()) stages.push_back(v);
+  for (auto& v : dn) if (!v.empty()) stages.push_back(v);
+  std::vector<int32_t> q;
+  q.reserve(T);
+  q.insert(q.end(), up_leaf.begin(), up_leaf.end());
+  const size_t S = stages.size();
+  if (opt_.interleave) {
+    size_t taken = 0;
+    for (size_t s = 0; s <= S; ++s) {
+      size_t upto = (nearq.size() * (s + 1)) / (S + 1);
+      q.insert(q.end(), nearq.begin() + taken, nearq.begin() + upto);
+      taken = upto;
+      if (s < S) q.insert(q.end(), stages[s].begin(), stages[s].end());
+    }
+  } else {
+    for (auto& v : stages) q.insert(q.end(), v.begin(), v.end());
+    q.insert(q.end(), nearq.begin(), nearq.end());
+  }
+  q.insert(q.end(), finalq.begin(), finalq.end());
+  std::vector<int32_t> pos(T);
+  for (int32_t i = 0; i < T; ++i) pos[q[i]] = i;
+
+  P.t_data.resize(T); P.t_out.resize(T); P.t_bias.resize(T);
+  P.t_m.resize(T); P.t_ld.resize(T); P.t_ncols.resize(T); P.t_kind.resize(T);
+  P.t_bias_nslots.resize(T); P.t_bias_stride.resize(T);
+  P.t_seg0.assign(T + 1, 0); P.t_dep0.assign(T + 1, 0);
+  for (int32_t i = 0; i < T; ++i) {
+    const TaskTmp& t = tasks_[q[i]];
+    P.t_data[i] = t.data; P.t_out[i] = t.out; P.t_bias[i] = t.bias;
+    P.t_m[i] = t.m; P.t_ld[i] = t.ld; P.t_ncols[i] = t.ncols; P.t_kind[i] = t.kind;
+    P.t_bias_nslots[i] = t.bias_nslots; P.t_bias_stride[i] = t.bias_stride;
+    for (int32_t si : t.seg_idx) {
+      P.s_src.push_back(s_src_[si]); P.s_ncols.push_back(s_ncols_[si]); P.s_kind.push_back(s_kind_[si]);
+      P.s_nslots.push_back(s_nslots_[si]); P.s_stride.push_back(s_stride_[si]);
+    }
+    for (int32_t dp : t.deps) {
+      int32_t qd = pos[dp];
+      if (qd >= i) { *err = "internal: dependency not earlier in the queue"; return H2B_EINVAL; }
+      P.deps.push_back(qd);
+    }
+    P.t_seg0[i + 1] = (int32_t)P.s_ncols.size();
+    P.t_dep0[i + 1] = (int32_t)P.deps.size();
+    P.tasks_by_kind[t.kind] += 1;
+  }
+  P.local_bytes = P.stream_bytes;
+  return H2B_OK;
+}
+
+}  // namespace
+
+int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string* err) {
+  if (opt.world_size > 1) {
+    *err = "multi-GPU plans are built per rank by the partitioner (not yet available)";
+    return H2B_EINVAL;
+  }
+  if (opt.task_bytes < 8) { *err = "task_bytes must be >= 8"; return H2B_EINVAL; }
+  Builder b(d, opt, out);
+  return b.run(err);
+}
+
+}  // namespace h2b

@@ -1,0 +1,76 @@
+// plan.h — host-side execution plan of the H² matvec (no CUDA dependencies).
+//
+// The reference applies the operator with four Python loops over small
+// GEMVs (h2.py:195-240).  Here every one of those GEMVs becomes a "work item"
+// of one uniform shape:
+//
+//     out[0:m] (+)= bias[0:m] + A[0:m, 0:ncols] @ gather(segments)
+//
+// where A is a column-major slice of one packed matrix pool and the gathered
+// source vector is the concatenation of the item's segments (x through the
+// cluster permutation, or cluster coefficients x^ / y^ held in a workspace).
+// Items are stored in a topologically ordered queue; each lists the items it
+// depends on.  A persistent CUDA kernel drains the queue.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/h2b.h"
+
+namespace h2b {
+
+enum TaskKind : int32_t {
+  kUpLeaf = 0,   // x^_t = W_t^T x|_t                       h2.py:199-200
+  kUpNode = 1,   // x^_p = sum_c F_c^T x^_c                 h2.py:201-205
+  kDown = 2,     // y^_t = E_t y^_parent + sum_b S_b x^_s    h2.py:211-218, 231-233
+  kNear = 3,     // partial_t = sum_s N_ts x|_s              h2.py:237-240
+  kFinal = 4,    // y[perm[t]] = sum partial_t + V_t y^_t    h2.py:227-229, 242-243
+};
+
+enum SegKind : int32_t {
+  kSegX = 0,     // x[perm[src + c]]         (permutation gather, h2.py:192-193)
+  kSegCoef = 1,  // sum_j coef[src + j*stride + c], j < nslots
+};
+
+constexpr int kMaxRows = 64;  // rows per work item (lanes own rows l, l+32)
+
+struct Plan {
+  int64_t n = 0;
+  std::vector<int64_t> perm;
+  std::vector<double> mat;  // packed matrix pool
+  int64_t coef_len = 0;     // doubles per right-hand side
+  int64_t stream_bytes = 0; // == H2Matrix.storage_bytes()
+
+  // tasks (queue order)
+  std::vector<int64_t> t_data, t_out, t_bias;
+  std::vector<int32_t> t_m, t_ld, t_ncols, t_kind, t_seg0, t_dep0;
+  std::vector<int32_t> t_bias_nslots, t_bias_stride;
+  // segments
+  std::vector<int64_t> s_src;
+  std::vector<int32_t> s_ncols, s_kind, s_nslots, s_stride;
+  // dependencies
+  std::vector<int32_t> deps;
+
+  int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
+  int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
+  int32_t rank = 0, world_size = 1;
+  int64_t local_bytes = 0;
+
+  int64_t ntasks() const { return (int64_t)t_m.size(); }
+  int64_t nsegs() const { return (int64_t)s_ncols.size(); }
+};
+
+struct PlanOptions {
+  int64_t task_bytes = 32768;
+  bool interleave = true;
+  int32_t rank = 0;
+  int32_t world_size = 1;
+};
+
+// Validates the descriptor and builds the plan.  Returns H2B_OK or an error
+// code with a message in *err.
+int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string* err);
+
+}  // namespace h2b

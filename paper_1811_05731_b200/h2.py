@@ -1,0 +1,325 @@
+"""H² operator data model and the drop-in GPU ``h2_matvec``.
+
+Reference interface being replaced (all /root/reference/pkg/src/strayfield):
+
+* ``h2_matvec(op, x)``            hmatrix/h2.py:186-244
+* ``H2Matrix.matvec(self, x)``    hmatrix/h2.py:74-75 (module-global lookup)
+* ``H2Matrix.storage_bytes()``    hmatrix/h2.py:77-83
+* ``H2Matrix.row_rank/col_rank``  hmatrix/h2.py:44-54
+
+``h2_matvec`` keeps the reference's signature and contract: ``x`` is coerced
+with ``np.asarray(x, dtype=float64)``; any shape other than ``(op.n,)`` raises
+``ValueError("vector must have shape (n,)")``; a fresh array in original node
+order is returned; ``x`` and ``op`` are never mutated.  The product runs in
+libh2b.so (one persistent sm_100a kernel); there is no CPU
+fallback.  The device copy of an operator is cached per operator object
+(``H2Matrix`` is ``eq=False``, hence identity-hashable), so operators must
+not be mutated after their first product — the reference treats them as
+immutable too.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .cluster import ClusterTree
+
+__all__ = ["H2Matrix", "h2_matvec", "h2_matmat", "DeviceOperator", "device_operator",
+           "describe", "plan_view", "install_into_reference", "rank_arrays"]
+
+
+@dataclass(eq=False)
+class H2Matrix:
+    """Nested-basis operator with the reference's field layout
+    (hmatrix/h2.py:23-42): per-cluster dicts keyed by preorder id, coupling
+    and near-field block lists ``(row_cid, col_cid, matrix)``."""
+
+    tree: ClusterTree
+    n: int
+    row_basis: dict[int, np.ndarray] = field(default_factory=dict)
+    row_transfer: dict[int, np.ndarray] = field(default_factory=dict)
+    col_basis: dict[int, np.ndarray] = field(default_factory=dict)
+    col_transfer: dict[int, np.ndarray] = field(default_factory=dict)
+    coupling: list[tuple[int, int, np.ndarray]] = field(default_factory=list)
+    near: list[tuple[int, int, np.ndarray]] = field(default_factory=list)
+
+    def row_rank(self, cid: int) -> int:
+        c = self.tree.clusters[cid]
+        if c.is_leaf:
+            return self.row_basis[cid].shape[1]
+        return self.row_transfer[c.children[0].cid].shape[1]
+
+    def col_rank(self, cid: int) -> int:
+        c = self.tree.clusters[cid]
+        if c.is_leaf:
+            return self.col_basis[cid].shape[1]
+        return self.col_transfer[c.children[0].cid].shape[1]
+
+    def explicit_row_basis(self, cid: int) -> np.ndarray:
+        c = self.tree.clusters[cid]
+        if c.is_leaf:
+            return self.row_basis[cid]
+        return np.vstack([self.explicit_row_basis(ch.cid) @ self.row_transfer[ch.cid]
+                          for ch in c.children])
+
+    def explicit_col_basis(self, cid: int) -> np.ndarray:
+        c = self.tree.clusters[cid]
+        if c.is_leaf:
+            return self.col_basis[cid]
+        return np.vstack([self.explicit_col_basis(ch.cid) @ self.col_transfer[ch.cid]
+                          for ch in c.children])
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        return h2_matvec(self, x)
+
+    def storage_bytes(self) -> int:
+        total = 0
+        for d in (self.row_basis, self.row_transfer, self.col_basis, self.col_transfer):
+            total += sum(m.size for m in d.values())
+        total += sum(s.size for _, _, s in self.coupling)
+        total += sum(m.size for _, _, m in self.near)
+        return total * 8
+
+
+def rank_arrays(op) -> tuple[np.ndarray, np.ndarray]:
+    """Per-cluster (k_row, k_col), the reference's row_rank/col_rank
+    (h2.py:44-54) for every preorder id."""
+    nc = len(op.tree.clusters)
+    k_row = np.zeros(nc, np.int64)
+    k_col = np.zeros(nc, np.int64)
+    for c in op.tree.clusters:
+        if c.is_leaf:
+            k_row[c.cid] = op.row_basis[c.cid].shape[1]
+            k_col[c.cid] = op.col_basis[c.cid].shape[1]
+        else:
+            k_row[c.cid] = op.row_transfer[c.children[0].cid].shape[1]
+            k_col[c.cid] = op.col_transfer[c.children[0].cid].shape[1]
+    return k_row, k_col
+
+
+class _DescHolder:
+    """A filled ``h2b_desc`` plus the numpy arrays its pointers refer to."""
+
+    def __init__(self, op):
+        from .cluster import tree_arrays
+        ta = tree_arrays(op.tree)
+        n = int(op.n)
+        if ta["perm"].shape != (n,):
+            raise ValueError("tree.perm does not match op.n")
+        nc = ta["cl_start"].shape[0]
+        k_row, k_col = rank_arrays(op)
+        keep = []
+
+        def cont(m):
+            a = np.ascontiguousarray(m, dtype=np.float64)
+            keep.append(a)
+            return a
+
+        rb = [None] * nc
+        cb = [None] * nc
+        rt = [None] * nc
+        ct = [None] * nc
+        for cid, m in op.row_basis.items():
+            rb[cid] = cont(m)
+        for cid, m in op.col_basis.items():
+            cb[cid] = cont(m)
+        for cid, m in op.row_transfer.items():
+            rt[cid] = cont(m)
+        for cid, m in op.col_transfer.items():
+            ct[cid] = cont(m)
+        cp_row = np.array([b[0] for b in op.coupling], np.int64)
+        cp_col = np.array([b[1] for b in op.coupling], np.int64)
+        cp = [cont(b[2]) for b in op.coupling]
+        nr_row = np.array([b[0] for b in op.near], np.int64)
+        nr_col = np.array([b[1] for b in op.near], np.int64)
+        nr = [cont(b[2]) for b in op.near]
+        # shape checks against the tree (cheap, catches malformed payloads)
+        size = ta["cl_end"] - ta["cl_start"]
+        for (r, s), m in zip(zip(nr_row, nr_col), nr):
+            if m.shape != (size[r], size[s]):
+                raise ValueError(f"near block ({r},{s}) has shape {m.shape}, expected {(size[r], size[s])}")
+        for (r, s), m in zip(zip(cp_row, cp_col), cp):
+            if m.shape != (k_row[r], k_col[s]):
+                raise ValueError(f"coupling block ({r},{s}) has shape {m.shape}")
+        self.arrays = dict(ta, k_row=k_row, k_col=k_col, cp_row=cp_row, cp_col=cp_col,
+                           nr_row=nr_row, nr_col=nr_col)
+        self.keep = keep
+        self.ptrs = [nat.ptr_array(rb), nat.ptr_array(cb), nat.ptr_array(rt), nat.ptr_array(ct),
+                     nat.ptr_array(cp), nat.ptr_array(nr)]
+        a = self.arrays
+        d = nat.Desc()
+        d.n = n
+        d.nclusters = nc
+        d.perm = nat.as_i64_ptr(a["perm"])
+        d.cl_start = nat.as_i64_ptr(a["cl_start"])
+        d.cl_end = nat.as_i64_ptr(a["cl_end"])
+        d.cl_child = nat.as_i64_ptr(np.ascontiguousarray(a["cl_child"]))
+        d.k_row = nat.as_i64_ptr(k_row)
+        d.k_col = nat.as_i64_ptr(k_col)
+        d.row_basis, d.col_basis, d.row_transfer, d.col_transfer = self.ptrs[:4]
+        d.ncoupling = len(op.coupling)
+        d.cp_row = nat.as_i64_ptr(cp_row)
+        d.cp_col = nat.as_i64_ptr(cp_col)
+        d.cp_data = self.ptrs[4]
+        d.nnear = len(op.near)
+        d.nr_row = nat.as_i64_ptr(nr_row)
+        d.nr_col = nat.as_i64_ptr(nr_col)
+        d.nr_data = self.ptrs[5]
+        self.desc = d
+
+
+def describe(op) -> _DescHolder:
+    """Flatten a (reference or mirror) H2Matrix into an ``h2b_desc``."""
+    return _DescHolder(op)
+
+
+def _options(task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, interleave=0,
+             rank=0, world_size=1) -> nat.Options:
+    o = nat.Options()
+    o.task_bytes = int(task_bytes)
+    o.warps_per_cta = int(warps_per_cta)
+    o.ctas_per_sm = int(ctas_per_sm)
+    o.max_nrhs = int(max_nrhs)
+    o.interleave = int(interleave)
+    o.rank = int(rank)
+    o.world_size = int(world_size)
+    return o
+
+
+def plan_view(op, **options) -> dict:
+    """Host-only execution plan (no GPU needed), returned as numpy copies:
+    the arrays the kernel consumes plus stats.  Used by the CPU tests, which
+    execute the plan with a numpy interpreter (oracle/flat_matvec.py)."""
+    h = describe(op)
+    lib = nat.lib()
+    handle = C.c_void_p()
+    nat.check(lib.h2b_plan_create(C.byref(h.desc), C.byref(_options(**options)), C.byref(handle)),
+              "h2b_plan_create")
+    try:
+        v = nat.PlanView()
+        nat.check(lib.h2b_plan_view_get(handle, C.byref(v)))
+        st = nat.Stats()
+        nat.check(lib.h2b_plan_stats(handle, C.byref(st)))
+        T, S, D = v.ntasks, v.nsegs, v.ndeps
+
+        def grab(ptr, count, dtype):
+            if count == 0:
+                return np.zeros(0, dtype)
+            return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+
+        out = {
+            "mat": grab(v.mat, v.mat_len, np.float64),
+            "coef_len": int(v.coef_len),
+            "t_data": grab(v.t_data, T, np.int64), "t_out": grab(v.t_out, T, np.int64),
+            "t_bias": grab(v.t_bias, T, np.int64), "t_m": grab(v.t_m, T, np.int32),
+            "t_ld": grab(v.t_ld, T, np.int32), "t_ncols": grab(v.t_ncols, T, np.int32),
+            "t_kind": grab(v.t_kind, T, np.int32), "t_seg0": grab(v.t_seg0, T + 1, np.int32),
+            "t_dep0": grab(v.t_dep0, T + 1, np.int32),
+            "t_bias_nslots": grab(v.t_bias_nslots, T, np.int32),
+            "t_bias_stride": grab(v.t_bias_stride, T, np.int32),
+            "s_src": grab(v.s_src, S, np.int64), "s_ncols": grab(v.s_ncols, S, np.int32),
+            "s_kind": grab(v.s_kind, S, np.int32), "s_nslots": grab(v.s_nslots, S, np.int32),
+            "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
+            "perm": np.ascontiguousarray(h.arrays["perm"]).copy(),
+            "n": int(op.n),
+            "stats": st.as_dict(),
+        }
+        return out
+    finally:
+        lib.h2b_plan_destroy(handle)
+
+
+class DeviceOperator:
+    """An H² operator resident on the current CUDA device (``h2b_op``)."""
+
+    def __init__(self, op, **options):
+        self.n = int(op.n)
+        h = describe(op)
+        self._lib = nat.lib()
+        handle = C.c_void_p()
+        nat.check(self._lib.h2b_create(C.byref(h.desc), C.byref(_options(**options)), C.byref(handle)),
+                  "h2b_create")
+        self._h = handle
+        self._lock = threading.Lock()
+
+    def stats(self) -> dict:
+        st = nat.Stats()
+        nat.check(self._lib.h2b_stats_get(self._h, C.byref(st)))
+        return st.as_dict()
+
+    def stream_bytes(self) -> int:
+        return int(self._lib.h2b_stream_bytes(self._h))
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        """Host arrays in/out: (n,) or (n, nrhs) with nrhs in {1,2,4,8,16}."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        nrhs = 1 if x.ndim == 1 else x.shape[1]
+        y = np.empty_like(x)
+        with self._lock:
+            nat.check(self._lib.h2b_matvec(self._h, nat.as_d_ptr(x), nat.as_d_ptr(y),
+                                           self.n, nrhs), "h2b_matvec")
+        return y
+
+    def matvec_dev(self, x_ptr: int, y_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
+        """Device pointers (e.g. ``tensor.data_ptr()``); asynchronous on ``stream``."""
+        nat.check(self._lib.h2b_matvec_dev(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                           int(nrhs), C.c_void_p(stream)), "h2b_matvec_dev")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.h2b_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_cache_lock = threading.Lock()
+
+
+def device_operator(op, **options) -> DeviceOperator:
+    """Cached device copy of ``op`` (created on first use)."""
+    with _cache_lock:
+        dev = _cache.get(op)
+        if dev is None:
+            dev = DeviceOperator(op, **options)
+            _cache[op] = dev
+        return dev
+
+
+def h2_matvec(op, x: np.ndarray) -> np.ndarray:
+    """Drop-in for the reference ``h2_matvec`` (h2.py:186-244), on the GPU."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (op.n,):
+        raise ValueError(f"vector must have shape ({op.n},)")
+    return device_operator(op).matvec(x)
+
+
+def h2_matmat(op, X: np.ndarray) -> np.ndarray:
+    """Multi-RHS product Y = M X, X of shape (n, nrhs), nrhs in {1,2,4,8,16}.
+    The reference has no such entry point (it rejects 2-D input); this is the
+    batched form of ``h2_matvec`` applied column by column."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[0] != op.n:
+        raise ValueError(f"matrix must have shape ({op.n}, nrhs)")
+    return device_operator(op).matvec(X)
+
+
+def install_into_reference(h2_module, package_module=None) -> None:
+    """Route the reference's ``H2Matrix.matvec`` (which looks up the
+    module-global ``h2_matvec`` at call time, h2.py:74-75) to the GPU path.
+    Patch both ``strayfield.hmatrix.h2`` and the re-export in
+    ``strayfield.hmatrix`` (hmatrix/__init__.py:13)."""
+    h2_module.h2_matvec = h2_matvec
+    if package_module is not None:
+        package_module.h2_matvec = h2_matvec
