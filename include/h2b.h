@@ -158,6 +158,25 @@ void h2b_destroy(h2b_op* op);
  * broadcasts the bytes to the other ranks, e.g. over torch.distributed). */
 int h2b_nccl_unique_id(void* out128);
 
+/* ---- Operator construction helper (not on the matvec path) ----------------
+ * Collocation entries of M = K + D (bem.py:99-153, 207-235) evaluated on the
+ * GPU for the operator builder.  `panels` holds 34 doubles per triangle:
+ * v0 v1 v2 (9), unit normal (3), shape-function gradients (9), gradient .
+ * edge-normal table (9), coplanarity scale (1), edge lengths (3)
+ * (bem.py:67-96).  inc_ptr/inc_tri/inc_loc: node -> incident triangles CSR
+ * (ascending triangle id) with the node's local vertex index. */
+typedef struct h2b_colloc h2b_colloc;
+int h2b_colloc_create(int64_t n, int64_t ntri, const double* panels, const int64_t* inc_ptr,
+                      const int64_t* inc_tri, const int8_t* inc_loc, const double* diag,
+                      h2b_colloc** out);
+/* Row job j: point points[3j..3j+2]; columns colidx[col_begin[j] .. +col_count[j]];
+ * diag[diag_node[j]] is added on the column equal to diag_node[j] (-1: none);
+ * values land in out[out_off[j] + c].  Host arrays; synchronous. */
+int h2b_colloc_eval(h2b_colloc* c, int64_t njobs, const double* points, const int64_t* col_begin,
+                    const int32_t* col_count, const int64_t* diag_node, const int64_t* out_off,
+                    int64_t ncolidx, const int64_t* colidx, int64_t out_len, double* out);
+void h2b_colloc_destroy(h2b_colloc* c);
+
 #ifdef __cplusplus
 }
 #endif

@@ -291,6 +291,10 @@ size_t smem_bytes(int wpc) {
 
 }  // namespace
 
+namespace h2b_detail {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace h2b_detail
+
 struct h2b_op {
   int device = 0;
   int64_t n = 0;
@@ -391,8 +395,14 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
   const int gi = nrhs_index(NRHS);
+  const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem_bytes<NRHS>(op->wpc), st>>>(p);
-  H2B_CUDA(cudaGetLastError());
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
+                               std::to_string(op->grid[gi]) + ", block=" + std::to_string(op->wpc * 32) +
+                               ", smem=" + std::to_string(smem_bytes<NRHS>(op->wpc)) +
+                               "): " + cudaGetErrorString(e) + " (stale: " + cudaGetErrorString(stale) + ")");
   return H2B_OK;
 }
 

@@ -93,7 +93,9 @@ def make(name: str) -> None:
     extra = dict(X=X, y_full=y_full, y_near=y_near, y_far=y_far,
                  storage_bytes=np.array(h2.storage_bytes()),
                  config=np.array([cfg.leaf_size, cfg.eta, cfg.cheb_order, cfg.eps, cfg.eps_rec]),
-                 boundary_coords=coords)
+                 boundary_coords=coords,
+                 diag=mesh.boundary_solid_angles() / (4.0 * np.pi) - 1.0,
+                 surface_triangles=mesh.surface.triangles)
     if want_dense:
         dense = bem.assemble_dense(mesh)
         extra["y_dense"] = dense.payload @ X
