@@ -1,0 +1,88 @@
+"""The BASELINE.json configurations as reproducible, seeded workloads.
+
+Each workload is a closed boundary surface plus the compression parameters
+the north star names (leaf size, eta, Chebyshev order); eps = 1e-5 and
+eps_rec = 2e-4 are the reference code's defaults (hmat.py:26-27) because
+BASELINE.json does not set them.  All inputs are synthetic: the reference
+measures on generated meshes too (there is no dataset).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import time
+from pathlib import Path
+
+import numpy as np
+
+from .assembly import geometry as G
+from .assembly.hbuild import CompressionConfig, assemble_h2
+
+__all__ = ["WORKLOADS", "surface_for", "build_workload", "vector_for"]
+
+WORKLOADS = {
+    "config1": dict(desc="unit icosphere level 4 (N=2562), leaf 32, eta 2, order 4",
+                    surface=lambda: G.icosphere_surface(4),
+                    cfg=CompressionConfig(leaf_size=32, eta=2.0, cheb_order=4)),
+    "config2": dict(desc="cube [-1,1]^3, 130x130 quads/face, 2 tri/quad (N=101402), leaf 64, eta 2, order 5",
+                    surface=lambda: G.cube_surface(130),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+    "config3": dict(desc="thin disk r=1 t=0.05, jittered Delaunay faces + structured rim (N~1.0M), "
+                         "leaf 64, eta 2, order 5",
+                    surface=lambda: G.disk_surface(0.0025),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+    "config5": dict(desc="icosphere level 10 decimated to 4194304 nodes, convex-hull re-triangulated, "
+                         "leaf 64, eta 2, order 5",
+                    surface=lambda: G.sphere_subsample_surface(10, 4_194_304),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+    # small variants for tests and quick runs
+    "cube40": dict(desc="cube [-1,1]^3, 40x40 quads/face (N=9602), leaf 64, eta 2, order 5",
+                   surface=lambda: G.cube_surface(40),
+                   cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+    "disk16k": dict(desc="thin disk, h=0.02 (N=16338), leaf 64, eta 2, order 5",
+                    surface=lambda: G.disk_surface(0.02),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+}
+WORKLOADS["config4"] = dict(WORKLOADS["config3"], desc=WORKLOADS["config3"]["desc"] + ", 16 right-hand sides")
+
+
+def surface_for(name: str):
+    return WORKLOADS[name]["surface"]()
+
+
+def build_workload(name: str, *, cache_dir: str | None = None, log=print, workers=None):
+    """Build (or load from ``cache_dir``) the H² operator of a workload.
+    The cache only saves build time; it is keyed by the workload recipe."""
+    w = WORKLOADS[name]
+    key = hashlib.sha256(repr((name, w["desc"], w["cfg"], 1)).encode()).hexdigest()[:16]
+    path = Path(cache_dir) / f"h2b_{name}_{key}.npz" if cache_dir else None
+    if path is not None and path.exists():
+        from .io import load_npz
+        t = time.perf_counter()
+        op, extra = load_npz(path)
+        log(f"[workload] {name}: loaded cached operator {path} ({time.perf_counter() - t:.1f}s)")
+        return op, {"cached": True, "n": op.n}
+    t = time.perf_counter()
+    surf = w["surface"]()
+    log(f"[workload] {name}: surface N={surf.n} T={surf.triangles.shape[0]} ({time.perf_counter() - t:.1f}s)")
+    op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"))
+    info = {"cached": False, "n": surf.n, "build_seconds": rep.seconds, "n_admissible": rep.n_admissible,
+            "n_dense": rep.n_dense, "n_fallback": rep.n_fallback}
+    if path is not None:
+        try:
+            os.makedirs(path.parent, exist_ok=True)
+            from .io import h2_to_arrays
+            tmp = path.with_suffix(".tmp.npz")
+            np.savez(tmp, **h2_to_arrays(op))
+            os.replace(tmp, path)
+        except OSError:
+            pass
+    return op, info
+
+
+def vector_for(name: str, n: int, nrhs: int = 1, seed: int = 1234) -> np.ndarray:
+    """u1 = seeded N(0,1) per node (BASELINE.json), node-major (n, nrhs)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, nrhs))
+    return x[:, 0].copy() if nrhs == 1 else x
