@@ -338,12 +338,34 @@ class BuildReport:
     seconds: dict = None
 
 
-_G: dict = {}  # fork-shared state of the worker pool
+_G: dict = {}  # state shared with the worker pool (sent once per worker)
+
+
+def _worker_init(state: dict) -> None:
+    _G.clear()
+    _G.update(state)
+    try:  # one BLAS thread per worker process
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
 
 
 def _pool(workers: int):
+    # spawn, not fork: the parent usually holds a CUDA context and BLAS/driver
+    # threads, and forking a multi-threaded process can deadlock the children
     import multiprocessing as mp
-    return mp.get_context("fork").Pool(workers)
+    import sys
+    main = sys.modules.get("__main__")
+    main_file = getattr(main, "__file__", None)
+    hide = main_file is not None and not os.path.exists(main_file)   # e.g. `python -` (stdin)
+    if hide:
+        del main.__file__
+    try:  # workers are started here; the main-module fixup happens now
+        return mp.get_context("spawn").Pool(workers, initializer=_worker_init, initargs=(dict(_G),))
+    finally:
+        if hide:
+            main.__file__ = main_file
 
 
 def _hca_prepare(bi: int):

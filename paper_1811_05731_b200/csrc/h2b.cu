@@ -368,7 +368,10 @@ int nrhs_index(int nrhs) {
 template <int NRHS>
 int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
   const size_t sm = smem_bytes<NRHS>(wpc);
-  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  // The attribute is per function, shared by every operator in the process:
+  // always allow the largest configuration (8 warps), never a smaller one.
+  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_bytes<NRHS>(8)));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
   int dev = 0, nsm = 0;
