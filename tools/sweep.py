@@ -1,0 +1,63 @@
+"""Time the H² product of a workload under several plan/launch options.
+
+    python tools/sweep.py --config config2 [--steps 100]
+
+Prints one line per option set: ms per product, GB/s of algorithmic bytes.
+Used to choose defaults; bench.py reports the chosen configuration."""
+
+import argparse
+import itertools
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="config2")
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
+    ap.add_argument("--grid", default='{"task_bytes":[16384,32768,65536],"interleave":[0,-1]}')
+    a = ap.parse_args()
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1811_05731_b200.h2 import DeviceOperator
+    from paper_1811_05731_b200.workloads import build_workload, vector_for
+    op, _ = build_workload(a.config, cache_dir=a.cache_dir, log=lambda m: print(m, file=sys.stderr))
+    grid = json.loads(a.grid)
+    keys = list(grid)
+    x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
+    y = torch.empty_like(x)
+    s = torch.cuda.current_stream()
+    ref = None
+    for vals in itertools.product(*[grid[k] for k in keys]):
+        opts = dict(zip(keys, vals))
+        dev = DeviceOperator(op, **opts)
+        st = dev.stats()
+        for _ in range(5):
+            dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.steps
+        yy = y.cpu().numpy()
+        if ref is None:
+            ref = yy
+        err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref))
+        gbs = (st["stream_bytes"] + 16 * op.n) / (ms * 1e-3) / 1e9
+        print(json.dumps({"opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1), "items": st["ntasks"],
+                          "grid": st["grid"], "rel_vs_first": err}), flush=True)
+        dev.close()
+
+
+if __name__ == "__main__":
+    main()
