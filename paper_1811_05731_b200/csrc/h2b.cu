@@ -66,25 +66,36 @@ struct __align__(8) DSeg {
 };
 static_assert(sizeof(DSeg) == 24, "DSeg layout");
 
+// Scheduler state (one per operator).  Every counter is reset by the last
+// warp to leave a launch, and `epoch` counts launches, so nothing has to be
+// cleared between products.
 struct Ctl {
-  unsigned ticket;
-  unsigned exited;
-  unsigned epoch;
-  unsigned pad;
+  unsigned ready_head;   // next slot of the dynamic ready queue to pop
+  unsigned ready_tail;   // next slot to push
+  unsigned static_head;  // next initially-ready item to take
+  unsigned completed;    // items finished in this launch
+  unsigned exited;       // warps that left the scheduler loop
+  unsigned epoch;        // launches completed so far
+  unsigned pad[2];
 };
 
 struct KParams {
   const DTask* __restrict__ tasks;
   const DSeg* __restrict__ segs;
-  const int32_t* __restrict__ deps;
+  const int32_t* __restrict__ succ0;    // [ntasks+1] successor CSR
+  const int32_t* __restrict__ succ;
+  const int32_t* __restrict__ ready0;   // initially ready items, issue order
   const double* __restrict__ mat;
   double* coef;
   const int64_t* __restrict__ perm;
   const double* __restrict__ x;
   double* y;
-  unsigned* flags;
+  unsigned long long* arrived;          // per item: finished predecessors, all launches
+  int32_t* ready_q;                     // dynamic ready queue (item ids)
+  unsigned* ready_flag;                 // per slot: epoch+1 once the id is written
   Ctl* ctl;
   int32_t ntasks;
+  int32_t nready0;
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -97,6 +108,11 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -251,35 +267,73 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
   double* xs = smem + (size_t)wib * (kChunkBytes / 8);
   double* red = smem + (size_t)nw * (kChunkBytes / 8) + wib * 32;
 
-  const unsigned done = *((volatile unsigned*)&p.ctl->epoch) + 1u;
-  int t = 0;
-  if (lane == 0) t = (int)atomicAdd(&p.ctl->ticket, 1u);
-  t = __shfl_sync(0xffffffffu, t, 0);
-  while (t < p.ntasks) {
-    int tn = 0;
-    if (lane == 0) tn = (int)atomicAdd(&p.ctl->ticket, 1u);  // prefetch next ticket
-    const DTask T = p.tasks[t];
-    for (int d = T.dep0 + lane; d < T.dep1; d += 32) {
-      const unsigned* f = p.flags + __ldg(p.deps + d);
-      while (ld_acquire(f) != done) __nanosleep(32);
+  // Completion-driven scheduling: a warp only ever runs items whose inputs
+  // are complete.  Items that became ready during this launch (the far-field
+  // chain and the finals) are served first from the dynamic queue; otherwise
+  // the warp takes the next initially-ready item (up-leaf, then near field).
+  Ctl* ctl = p.ctl;
+  const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
+  for (;;) {
+    int item = -1;
+    if (lane == 0) {
+      unsigned backoff = 64;
+      for (;;) {
+        const unsigned h = ld_relaxed(&ctl->ready_head);
+        if (h < ld_relaxed(&ctl->ready_tail)) {
+          if (atomicCAS(&ctl->ready_head, h, h + 1u) == h) {
+            while (ld_acquire(p.ready_flag + h) != e1) __nanosleep(32);
+            item = __ldcg(p.ready_q + h);
+            break;
+          }
+          continue;
+        }
+        if (ld_relaxed(&ctl->static_head) < (unsigned)p.nready0) {
+          const unsigned s = atomicAdd(&ctl->static_head, 1u);
+          if (s < (unsigned)p.nready0) {
+            item = __ldg(p.ready0 + s);
+            break;
+          }
+        }
+        if (ld_relaxed(&ctl->completed) >= (unsigned)p.ntasks) break;  // all done
+        __nanosleep(backoff);
+        backoff = min(backoff * 2u, 2048u);
+      }
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item < 0) break;
+    const DTask T = p.tasks[item];
+    run_item<NRHS>(p, T, xs, red, lane);
+    // publish: outputs visible GPU-wide, then count this item into each
+    // successor; the warp that completes a successor's count enqueues it
+    __syncwarp();
+    __threadfence();
+    const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
+    for (int k = s0 + lane; k < s1; k += 32) {
+      const int d = __ldg(p.succ + k);
+      const unsigned long long need =
+          (unsigned long long)e1 * (unsigned long long)(__ldg(&p.tasks[d].dep1) - __ldg(&p.tasks[d].dep0));
+      if (atomicAdd(p.arrived + d, 1ull) + 1ull == need) {
+        __threadfence();
+        const unsigned slot = atomicAdd(&ctl->ready_tail, 1u);
+        p.ready_q[slot] = d;
+        st_release(p.ready_flag + slot, e1);
+      }
     }
     __syncwarp();
-    run_item<NRHS>(p, T, xs, red, lane);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(p.flags + t, done);
-    t = __shfl_sync(0xffffffffu, tn, 0);
+    if (lane == 0) atomicAdd(&ctl->completed, 1u);
   }
   if (lane == 0) {
     const unsigned total = gridDim.x * (unsigned)nw;
     __threadfence();
-    const unsigned prev = atomicAdd(&p.ctl->exited, 1u);
-    if (prev == total - 1) {
-      // every warp drew its terminating ticket: reset for the next launch
-      p.ctl->ticket = 0;
-      p.ctl->exited = 0;
+    if (atomicAdd(&ctl->exited, 1u) == total - 1) {
+      // every warp has left the loop: reset the counters for the next launch
+      ctl->ready_head = 0;
+      ctl->ready_tail = 0;
+      ctl->static_head = 0;
+      ctl->completed = 0;
+      ctl->exited = 0;
       __threadfence();
-      atomicAdd(&p.ctl->epoch, 1u);
+      atomicAdd(&ctl->epoch, 1u);
     }
   }
 }
@@ -307,9 +361,14 @@ struct h2b_op {
   double* d_coef = nullptr;
   DTask* d_tasks = nullptr;
   DSeg* d_segs = nullptr;
-  int32_t* d_deps = nullptr;
+  int32_t* d_succ0 = nullptr;
+  int32_t* d_succ = nullptr;
+  int32_t* d_ready0 = nullptr;
+  int32_t nready0 = 0;
+  unsigned long long* d_arrived = nullptr;
+  int32_t* d_ready_q = nullptr;
   int64_t* d_perm = nullptr;
-  unsigned* d_flags = nullptr;
+  unsigned* d_ready_flag = nullptr;
   Ctl* d_ctl = nullptr;
   double* d_x = nullptr;
   double* d_y = nullptr;
@@ -388,13 +447,18 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   KParams p;
   p.tasks = op->d_tasks;
   p.segs = op->d_segs;
-  p.deps = op->d_deps;
+  p.succ0 = op->d_succ0;
+  p.succ = op->d_succ;
+  p.ready0 = op->d_ready0;
+  p.nready0 = op->nready0;
+  p.arrived = op->d_arrived;
+  p.ready_q = op->d_ready_q;
   p.mat = op->d_mat;
   p.coef = op->d_coef;
   p.perm = op->d_perm;
   p.x = x;
   p.y = y;
-  p.flags = op->d_flags;
+  p.ready_flag = op->d_ready_flag;
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
   const int gi = nrhs_index(NRHS);
@@ -423,9 +487,13 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_coef);
   cudaFree(op->d_tasks);
   cudaFree(op->d_segs);
-  cudaFree(op->d_deps);
+  cudaFree(op->d_succ0);
+  cudaFree(op->d_succ);
+  cudaFree(op->d_ready0);
+  cudaFree(op->d_arrived);
+  cudaFree(op->d_ready_q);
   cudaFree(op->d_perm);
-  cudaFree(op->d_flags);
+  cudaFree(op->d_ready_flag);
   cudaFree(op->d_ctl);
   cudaFree(op->d_x);
   cudaFree(op->d_y);
@@ -486,12 +554,19 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
   if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
   if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
-  if ((rc = upload(&op->d_deps, P.deps.data(), P.deps.size()))) return rc;
+  if ((rc = upload(&op->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
+  if ((rc = upload(&op->d_succ, P.succ.data(), P.succ.size()))) return rc;
+  if ((rc = upload(&op->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
+  op->nready0 = (int32_t)P.ready0.size();
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
-  if ((rc = upload<unsigned>(&op->d_flags, nullptr, (size_t)P.ntasks()))) return rc;
+  const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
+  if ((rc = upload<unsigned long long>(&op->d_arrived, nullptr, T1))) return rc;
+  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, T1))) return rc;
+  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, T1))) return rc;
   if ((rc = upload<Ctl>(&op->d_ctl, nullptr, 1))) return rc;
-  H2B_CUDA(cudaMemset(op->d_flags, 0, sizeof(unsigned) * std::max<int64_t>(1, P.ntasks())));
+  H2B_CUDA(cudaMemset(op->d_arrived, 0, sizeof(unsigned long long) * T1));
+  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * T1));
   H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 

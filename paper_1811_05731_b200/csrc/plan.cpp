@@ -452,6 +452,25 @@ int Builder::run(std::string* err) {
     P.t_dep0[i + 1] = (int32_t)P.deps.size();
     P.tasks_by_kind[t.kind] += 1;
   }
+  // successor lists for the completion-driven scheduler
+  P.succ0.assign(T + 1, 0);
+  for (int32_t dp : P.deps) P.succ0[dp + 1] += 1;
+  for (int32_t i = 0; i < T; ++i) P.succ0[i + 1] += P.succ0[i];
+  P.succ.assign(P.deps.size(), 0);
+  {
+    std::vector<int32_t> fill(P.succ0.begin(), P.succ0.end() - 1);
+    for (int32_t i = 0; i < T; ++i)
+      for (int32_t k = P.t_dep0[i]; k < P.t_dep0[i + 1]; ++k) P.succ[fill[P.deps[k]]++] = i;
+  }
+  // initially ready items: up-leaf first (they start the far-field chain),
+  // then the near field, then anything else without dependencies
+  for (int pass = 0; pass < 3; ++pass)
+    for (int32_t i = 0; i < T; ++i) {
+      if (P.t_dep0[i + 1] != P.t_dep0[i]) continue;
+      const int32_t k = P.t_kind[i];
+      const int want = k == kUpLeaf ? 0 : (k == kNear ? 1 : 2);
+      if (want == pass) P.ready0.push_back(i);
+    }
   P.local_bytes = P.stream_bytes;
   return H2B_OK;
 }

@@ -52,6 +52,10 @@ struct Plan {
   std::vector<int32_t> s_ncols, s_kind, s_nslots, s_stride;
   // dependencies
   std::vector<int32_t> deps;
+  // successors (inverse of deps, CSR) and the initially ready items in
+  // issue order: the kernel's dynamic scheduler
+  std::vector<int32_t> succ0, succ;
+  std::vector<int32_t> ready0;
 
   int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
   int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
