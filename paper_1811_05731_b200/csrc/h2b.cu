@@ -69,14 +69,18 @@ static_assert(sizeof(DSeg) == 24, "DSeg layout");
 // Scheduler state (one per operator).  Every counter is reset by the last
 // warp to leave a launch, and `epoch` counts launches, so nothing has to be
 // cleared between products.
+// Each hot counter sits on its own 128-byte line so that polling one does not
+// queue behind atomics on another in the same L2 slice.
 struct Ctl {
   unsigned ready_head;   // next slot of the dynamic ready queue to pop
+  unsigned pad0[31];
   unsigned ready_tail;   // next slot to push
+  unsigned pad1[31];
   unsigned static_head;  // next initially-ready item to take
-  unsigned completed;    // items finished in this launch
+  unsigned pad2[31];
   unsigned exited;       // warps that left the scheduler loop
   unsigned epoch;        // launches completed so far
-  unsigned pad[2];
+  unsigned pad3[30];
 };
 
 struct KParams {
@@ -273,12 +277,15 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
   // the warp takes the next initially-ready item (up-leaf, then near field).
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
+  const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);  // items pushed during a launch
+  bool static_done = false;
   for (;;) {
     int item = -1;
     if (lane == 0) {
       unsigned backoff = 64;
       for (;;) {
         const unsigned h = ld_relaxed(&ctl->ready_head);
+        if (h >= n_dynamic && static_done) break;  // every item has been claimed
         if (h < ld_relaxed(&ctl->ready_tail)) {
           if (atomicCAS(&ctl->ready_head, h, h + 1u) == h) {
             while (ld_acquire(p.ready_flag + h) != e1) __nanosleep(32);
@@ -287,16 +294,20 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
           }
           continue;
         }
-        if (ld_relaxed(&ctl->static_head) < (unsigned)p.nready0) {
+        if (!static_done) {
           const unsigned s = atomicAdd(&ctl->static_head, 1u);
           if (s < (unsigned)p.nready0) {
             item = __ldg(p.ready0 + s);
             break;
           }
+          static_done = true;
+          continue;
         }
-        if (ld_relaxed(&ctl->completed) >= (unsigned)p.ntasks) break;  // all done
+        // idle while the far-field chain catches up: keep two pollers per
+        // CTA, let the rest retire (the remaining work is latency-bound)
+        if (wib >= 2) break;
         __nanosleep(backoff);
-        backoff = min(backoff * 2u, 2048u);
+        backoff = min(backoff * 2u, 4096u);
       }
     }
     item = __shfl_sync(0xffffffffu, item, 0);
@@ -320,7 +331,6 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
       }
     }
     __syncwarp();
-    if (lane == 0) atomicAdd(&ctl->completed, 1u);
   }
   if (lane == 0) {
     const unsigned total = gridDim.x * (unsigned)nw;
@@ -330,7 +340,6 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
       ctl->ready_head = 0;
       ctl->ready_tail = 0;
       ctl->static_head = 0;
-      ctl->completed = 0;
       ctl->exited = 0;
       __threadfence();
       atomicAdd(&ctl->epoch, 1u);
