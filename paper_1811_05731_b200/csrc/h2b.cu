@@ -287,9 +287,13 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
         const unsigned h = ld_relaxed(&ctl->ready_head);
         if (h >= n_dynamic && static_done) break;  // every item has been claimed
         if (h < ld_relaxed(&ctl->ready_tail)) {
-          if (atomicCAS(&ctl->ready_head, h, h + 1u) == h) {
-            while (ld_acquire(p.ready_flag + h) != e1) __nanosleep(32);
-            item = __ldcg(p.ready_q + h);
+          // claim a slot with one atomicAdd (a CAS loop would serialise the
+          // claims of all contending warps).  Losing a race can hand out a
+          // slot that is not pushed yet: then wait for it, it will be.
+          const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
+          if (slot < n_dynamic) {
+            while (ld_acquire(p.ready_flag + slot) != e1) __nanosleep(64);
+            item = __ldcg(p.ready_q + slot);
             break;
           }
           continue;
