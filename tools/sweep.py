@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
     ap.add_argument("--grid", default='{"task_bytes":[16384,32768,65536],"interleave":[0,-1]}')
+    ap.add_argument("--ablate", default="", help="comma list of: far (near=[]), near (coupling=[])")
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -30,15 +31,19 @@ def main():
     from paper_1811_05731_b200.h2 import DeviceOperator
     from paper_1811_05731_b200.workloads import build_workload, vector_for
     op, _ = build_workload(a.config, cache_dir=a.cache_dir, log=lambda m: print(m, file=sys.stderr))
+    import dataclasses
+    ops = {"full": op}
+    for ab in filter(None, a.ablate.split(",")):
+        ops[ab] = dataclasses.replace(op, near=[]) if ab == "far" else dataclasses.replace(op, coupling=[])
     grid = json.loads(a.grid)
     keys = list(grid)
     x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
     y = torch.empty_like(x)
     s = torch.cuda.current_stream()
     ref = None
-    for vals in itertools.product(*[grid[k] for k in keys]):
+    for (name, opx), vals in itertools.product(ops.items(), itertools.product(*[grid[k] for k in keys])):
         opts = dict(zip(keys, vals))
-        dev = DeviceOperator(op, **opts)
+        dev = DeviceOperator(opx, **opts)
         st = dev.stats()
         for _ in range(5):
             dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
@@ -50,11 +55,11 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
         yy = y.cpu().numpy()
-        if ref is None:
-            ref = yy
-        err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref))
+        if ref is None or name != "full":
+            ref = yy if name == "full" or ref is None else ref
+        err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref)) if name == "full" else None
         gbs = (st["stream_bytes"] + 16 * op.n) / (ms * 1e-3) / 1e9
-        print(json.dumps({"opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1), "items": st["ntasks"],
+        print(json.dumps({"op": name, "opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1), "items": st["ntasks"],
                           "grid": st["grid"], "rel_vs_first": err}), flush=True)
         dev.close()
 
