@@ -77,8 +77,8 @@ typedef struct h2b_desc {
 
 /* Execution-plan knobs.  Zero-initialise for defaults. */
 typedef struct h2b_options {
-  int64_t task_bytes;   /* max streamed bytes per work item (default 32768)  */
-  int32_t warps_per_cta;/* persistent CTA width in warps (default 8)         */
+  int64_t task_bytes;   /* max streamed bytes per work item (default 8192)   */
+  int32_t warps_per_cta;/* persistent CTA width in warps (default 10, <= 16) */
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
   int32_t interleave;   /* 0 (default) = interleave near-field work items

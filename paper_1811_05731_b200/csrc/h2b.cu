@@ -100,6 +100,7 @@ struct KParams {
   Ctl* ctl;
   int32_t ntasks;
   int32_t nready0;
+  int32_t buf_bytes;                    // per TMA staging buffer (multiple of 128)
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -123,10 +124,46 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// ---- shared-memory staging with 1-D TMA (cp.async.bulk + mbarrier) -------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Copy [src, src + bytes) (16-byte aligned, multiple of 16) into dst and
+// signal `bar` when the bytes have landed.  Issued by one lane.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool SMEM>
+__device__ __forceinline__ double ldA(const double* p) {
+  if constexpr (SMEM) return *p;
+  else return ld_stream(p);
+}
+
 // One work item, NRHS right-hand sides, rows r0 = lane, r1 = lane + 32.
-template <int NRHS>
-__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, double* xs, double* red,
-                                         int lane) {
+// A is the item's column-major matrix: in shared memory (SMEM, staged by
+// TMA) or streamed straight from global memory.
+template <int NRHS, bool SMEM>
+__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const double* A, double* xs,
+                                         double* red, int lane) {
   constexpr int kCols = kChunkBytes / (8 * NRHS);
   const int m = T.m, ld = T.ld;
   const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
@@ -152,7 +189,6 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
     }
   }
 
-  const double* A = p.mat + T.data;
   int si = T.seg0, soff = 0;
   for (int col = 0; col < T.ncols; col += kCols) {
     const int cc = min(kCols, T.ncols - col);
@@ -179,7 +215,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
       if (soff == S.ncols) { ++si; soff = 0; }
     }
     __syncwarp();
-    // ---- stream the matrix columns
+    // ---- the matrix columns
     const double* Ac = A + (int64_t)col * ld;
     if (grouped) {
       // G columns per step; lane (g, rr) reads element (rr, c0 + g): the
@@ -188,12 +224,12 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
       for (; c + 7 * G < cc; c += 8 * G) {
         double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = v0 ? ld_stream(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
+        for (int u = 0; u < 8; ++u) a[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc0[0] = fma(a[u], xs[c + u * G], acc0[0]);
       }
       for (; c < cc; c += G)
-        if (v0) acc0[0] = fma(ld_stream(Ac + (int64_t)c * m + rr), xs[c], acc0[0]);
+        if (v0) acc0[0] = fma(ldA<SMEM>(Ac + (int64_t)c * m + rr), xs[c], acc0[0]);
     } else {
       int c = 0;
       constexpr int U = (NRHS == 1) ? 8 : 4;
@@ -201,8 +237,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
         double a0[U], a1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          a0[u] = v0 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
-          a1[u] = v1 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
+          a0[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
+          a1[u] = v1 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -215,8 +251,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
         }
       }
       for (; c < cc; ++c) {
-        const double a0 = v0 ? ld_stream(Ac + (int64_t)c * ld + lane) : 0.0;
-        const double a1 = v1 ? ld_stream(Ac + (int64_t)c * ld + lane + 32) : 0.0;
+        const double a0 = v0 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane) : 0.0;
+        const double a1 = v1 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane + 32) : 0.0;
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) {
           const double xv = xs[c * NRHS + r];
@@ -262,62 +298,123 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, doubl
   }
 }
 
+// Per-warp shared memory: two TMA staging buffers, the source chunk, the
+// small-item reduction scratch and the two mbarriers.
+__host__ __device__ constexpr size_t warp_smem_bytes(int buf_bytes) {
+  return (((size_t)2 * buf_bytes + kChunkBytes + 32 * 8 + 2 * 8) + 127) & ~(size_t)127;
+}
+
+// Lane 0: start staging `item` into buffer `b` if its matrix slice is
+// contiguous and fits; returns the element offset of the slice inside the
+// buffer, or -1 when the item must stream from global memory.
+__device__ __forceinline__ int stage_item(const KParams& p, int item, double* buf, uint64_t* bar) {
+  const DTask* t = p.tasks + item;
+  const int m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
+  if (ld != m || nc == 0) return -1;
+  const double* g0 = p.mat + __ldg(&t->data);
+  const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)m * nc) + 15) & ~(uintptr_t)15;
+  if (a1 - a0 > (uintptr_t)p.buf_bytes) return -1;
+  bulk_load(buf, (const void*)a0, (unsigned)(a1 - a0), bar);
+  return (int)(((uintptr_t)g0 - a0) >> 3);
+}
+
 template <int NRHS>
-__global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(512) h2b_dataflow_kernel(KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  double* xs = smem + (size_t)wib * (kChunkBytes / 8);
-  double* red = smem + (size_t)nw * (kChunkBytes / 8) + wib * 32;
+  unsigned char* ws = smem_raw + (size_t)wib * warp_smem_bytes(p.buf_bytes);
+  auto buf = [&](int b) { return (double*)(ws + (size_t)b * p.buf_bytes); };
+  double* xs = (double*)(ws + 2 * (size_t)p.buf_bytes);
+  double* red = xs + kChunkBytes / 8;
+  uint64_t* bars = (uint64_t*)(red + 32);
+  if (lane == 0) {
+    mbar_init(bars);
+    mbar_init(bars + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
 
   // Completion-driven scheduling: a warp only ever runs items whose inputs
   // are complete.  Items that became ready during this launch (the far-field
   // chain and the finals) are served first from the dynamic queue; otherwise
-  // the warp takes the next initially-ready item (up-leaf, then near field).
+  // the warp takes the next initially-ready item (up-leaf, then near field),
+  // whose matrix slice it has already started staging into its second buffer
+  // while the previous item was computed (double buffering with 1-D TMA).
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
-  const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);  // items pushed during a launch
-  bool static_done = false;
+  const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
+  bool static_done = false;               // lane 0 only
+  int pend = -1, pend_buf = 0, pend_off = -1;  // lane 0 only: prefetched static item
+  unsigned phase = 0;                     // per-buffer mbarrier parity, all lanes
   for (;;) {
-    int item = -1;
+    int item = -1, b = 0, off = -1;
     if (lane == 0) {
       unsigned backoff = 64;
       for (;;) {
         const unsigned h = ld_relaxed(&ctl->ready_head);
-        if (h >= n_dynamic && static_done) break;  // every item has been claimed
         if (h < ld_relaxed(&ctl->ready_tail)) {
-          // claim a slot with one atomicAdd (a CAS loop would serialise the
-          // claims of all contending warps).  Losing a race can hand out a
-          // slot that is not pushed yet: then wait for it, it will be.
+          // claim with one atomicAdd (a CAS loop serialises contending
+          // warps); a lost race may return a slot not pushed yet: wait for it
           const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
           if (slot < n_dynamic) {
             while (ld_acquire(p.ready_flag + slot) != e1) __nanosleep(64);
             item = __ldcg(p.ready_q + slot);
+            b = pend >= 0 ? 1 - pend_buf : 0;
+            off = stage_item(p, item, buf(b), bars + b);
             break;
           }
           continue;
+        }
+        if (pend >= 0) {
+          item = pend; b = pend_buf; off = pend_off;
+          pend = -1;
+          break;
         }
         if (!static_done) {
           const unsigned s = atomicAdd(&ctl->static_head, 1u);
           if (s < (unsigned)p.nready0) {
             item = __ldg(p.ready0 + s);
+            b = 0;
+            off = stage_item(p, item, buf(0), bars);
             break;
           }
           static_done = true;
           continue;
         }
+        if (h >= n_dynamic) break;  // every item has been claimed
         // idle while the far-field chain catches up: keep two pollers per
         // CTA, let the rest retire (the remaining work is latency-bound)
         if (wib >= 2) break;
         __nanosleep(backoff);
         backoff = min(backoff * 2u, 4096u);
       }
+      // prefetch the next initially-ready item into the other buffer
+      if (item >= 0 && pend < 0 && !static_done) {
+        const unsigned s = atomicAdd(&ctl->static_head, 1u);
+        if (s < (unsigned)p.nready0) {
+          pend = __ldg(p.ready0 + s);
+          pend_buf = 1 - b;
+          pend_off = stage_item(p, pend, buf(pend_buf), bars + pend_buf);
+        } else {
+          static_done = true;
+        }
+      }
     }
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
+    b = __shfl_sync(0xffffffffu, b, 0);
+    off = __shfl_sync(0xffffffffu, off, 0);
     const DTask T = p.tasks[item];
-    run_item<NRHS>(p, T, xs, red, lane);
+    if (off >= 0) {
+      mbar_wait(bars + b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+      run_item<NRHS, true>(p, T, buf(b) + off, xs, red, lane);
+    } else {
+      run_item<NRHS, false>(p, T, p.mat + T.data, xs, red, lane);
+    }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor; the warp that completes a successor's count enqueues it
     __syncwarp();
@@ -351,11 +448,6 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
   }
 }
 
-template <int NRHS>
-size_t smem_bytes(int wpc) {
-  return (size_t)wpc * (kChunkBytes + 32 * 8);
-}
-
 }  // namespace
 
 namespace h2b_detail {
@@ -369,6 +461,7 @@ struct h2b_op {
   int64_t coef_len = 0;
   int max_nrhs = 16;
   int wpc = 8;
+  int buf_bytes = 0;
   int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
   double* d_mat = nullptr;
   double* d_coef = nullptr;
@@ -438,20 +531,17 @@ int nrhs_index(int nrhs) {
 }
 
 template <int NRHS>
-int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
-  const size_t sm = smem_bytes<NRHS>(wpc);
-  // The attribute is per function, shared by every operator in the process:
-  // always allow the largest configuration (8 warps), never a smaller one.
-  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_bytes<NRHS>(8)));
+int occupancy_grid(int wpc, int buf_bytes, int ctas_per_sm, int* grid) {
+  const size_t sm = (size_t)wpc * warp_smem_bytes(buf_bytes);
+  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
   int dev = 0, nsm = 0;
   H2B_CUDA(cudaGetDevice(&dev));
   H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (per_sm < 1) return fail(H2B_ECUDA, "kernel does not fit on an SM");
+  if (per_sm < 1) return fail(H2B_EINVAL, "work-item buffers do not fit in shared memory: lower task_bytes or warps_per_cta");
   if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
-  *grid = per_sm * nsm;  // every CTA co-resident: required by the dependency waits
+  *grid = per_sm * nsm;
   return H2B_OK;
 }
 
@@ -474,14 +564,18 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.ready_flag = op->d_ready_flag;
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
+  p.buf_bytes = op->buf_bytes;
   const int gi = nrhs_index(NRHS);
+  const size_t smem = (size_t)op->wpc * warp_smem_bytes(op->buf_bytes);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
-  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem_bytes<NRHS>(op->wpc), st>>>(p);
+  // the attribute is per function and shared by every operator of the process
+  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
                                std::to_string(op->grid[gi]) + ", block=" + std::to_string(op->wpc * 32) +
-                               ", smem=" + std::to_string(smem_bytes<NRHS>(op->wpc)) +
+                               ", smem=" + std::to_string(smem) +
                                "): " + cudaGetErrorString(e) + " (stale: " + cudaGetErrorString(stale) + ")");
   return H2B_OK;
 }
@@ -534,8 +628,10 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->coef_len = P.coef_len;
   op->max_nrhs = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
   if (nrhs_index(op->max_nrhs) < 0) return fail(H2B_EINVAL, "max_nrhs must be 1, 2, 4, 8 or 16");
-  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
-  if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
+  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 10;
+  if (op->wpc > 16) return fail(H2B_EINVAL, "warps_per_cta must be <= 16");
+  // staging buffer: the largest split item plus 16 bytes of alignment slack
+  op->buf_bytes = (int)(((to_plan_options(o).task_bytes + 16) + 127) & ~(int64_t)127);
   const int cps = o ? o->ctas_per_sm : 0;
 
   // device task / segment arrays
@@ -564,7 +660,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     segs[i].nslots = P.s_nslots[i];
     segs[i].stride = P.s_stride[i];
   }
+  // +2 doubles: a 16-byte-rounded TMA copy of the last item may read past the end
+  P.mat.push_back(0.0);
+  P.mat.push_back(0.0);
   if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
+  P.mat.resize(P.mat.size() - 2);
   if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
   if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
   if ((rc = upload(&op->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
@@ -583,11 +683,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
-  if ((rc = occupancy_grid<1>(op->wpc, cps, &op->grid[0]))) return rc;
-  if ((rc = occupancy_grid<2>(op->wpc, cps, &op->grid[1]))) return rc;
-  if ((rc = occupancy_grid<4>(op->wpc, cps, &op->grid[2]))) return rc;
-  if ((rc = occupancy_grid<8>(op->wpc, cps, &op->grid[3]))) return rc;
-  if ((rc = occupancy_grid<16>(op->wpc, cps, &op->grid[4]))) return rc;
+  if ((rc = occupancy_grid<1>(op->wpc, op->buf_bytes, cps, &op->grid[0]))) return rc;
+  if ((rc = occupancy_grid<2>(op->wpc, op->buf_bytes, cps, &op->grid[1]))) return rc;
+  if ((rc = occupancy_grid<4>(op->wpc, op->buf_bytes, cps, &op->grid[2]))) return rc;
+  if ((rc = occupancy_grid<8>(op->wpc, op->buf_bytes, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->wpc, op->buf_bytes, cps, &op->grid[4]))) return rc;
   H2B_CUDA(cudaDeviceSynchronize());
 
   fill_stats(P, &op->stats);

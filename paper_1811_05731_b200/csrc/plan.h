@@ -67,7 +67,7 @@ struct Plan {
 };
 
 struct PlanOptions {
-  int64_t task_bytes = 32768;
+  int64_t task_bytes = 8192;
   bool interleave = true;
   int32_t rank = 0;
   int32_t world_size = 1;
