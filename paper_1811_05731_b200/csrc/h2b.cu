@@ -355,18 +355,16 @@ __global__ void __launch_bounds__(512) h2b_dataflow_kernel(KParams p) {
       unsigned backoff = 64;
       for (;;) {
         const unsigned h = ld_relaxed(&ctl->ready_head);
-        if (h < ld_relaxed(&ctl->ready_tail)) {
-          // claim with one atomicAdd (a CAS loop serialises contending
-          // warps); a lost race may return a slot not pushed yet: wait for it
-          const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
-          if (slot < n_dynamic) {
-            while (ld_acquire(p.ready_flag + slot) != e1) __nanosleep(64);
-            item = __ldcg(p.ready_q + slot);
-            b = pend >= 0 ? 1 - pend_buf : 0;
-            off = stage_item(p, item, buf(b), bars + b);
-            break;
-          }
-          continue;
+        // One CAS attempt per decision: a won slot is below the tail, so
+        // its pusher is already publishing it (bounded wait, never a wait on
+        // unfinished work); a lost race falls through to other work instead
+        // of retrying (retry loops serialise every contending warp).
+        if (h < ld_relaxed(&ctl->ready_tail) && atomicCAS(&ctl->ready_head, h, h + 1u) == h) {
+          while (ld_acquire(p.ready_flag + h) != e1) __nanosleep(32);
+          item = __ldcg(p.ready_q + h);
+          b = pend >= 0 ? 1 - pend_buf : 0;
+          off = stage_item(p, item, buf(b), bars + b);
+          break;
         }
         if (pend >= 0) {
           item = pend; b = pend_buf; off = pend_off;
