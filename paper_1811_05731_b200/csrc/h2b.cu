@@ -100,7 +100,6 @@ struct KParams {
   Ctl* ctl;
   int32_t ntasks;
   int32_t nready0;
-  int32_t buf_bytes;                    // per TMA staging buffer (multiple of 128)
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -298,76 +297,71 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
   }
 }
 
-// Per-warp shared memory: two TMA staging buffers, the source chunk, the
-// small-item reduction scratch and the two mbarriers.
-__host__ __device__ constexpr size_t warp_smem_bytes(int buf_bytes) {
-  return (((size_t)2 * buf_bytes + kChunkBytes + 32 * 8 + 2 * 8) + 127) & ~(size_t)127;
-}
+// Per-warp shared memory: the gathered-source chunk and the small-item
+// reduction scratch.
+__host__ __device__ constexpr size_t warp_smem_bytes() { return (size_t)kChunkBytes + 32 * 8; }
 
-// Lane 0: start staging `item` into buffer `b` if its matrix slice is
-// contiguous and fits; returns the element offset of the slice inside the
-// buffer, or -1 when the item must stream from global memory.
-__device__ __forceinline__ int stage_item(const KParams& p, int item, double* buf, uint64_t* bar) {
+// 1-D TMA prefetch of an item's matrix slice into L2 (cp.async.bulk.prefetch):
+// issued when the item is claimed, one item ahead, so that its column loads
+// hit L2 when the warp gets to it.
+__device__ __forceinline__ void prefetch_item(const KParams& p, int item) {
   const DTask* t = p.tasks + item;
   const int m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
-  if (ld != m || nc == 0) return -1;
+  if (nc <= 0) return;
   const double* g0 = p.mat + __ldg(&t->data);
   const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-  const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)m * nc) + 15) & ~(uintptr_t)15;
-  if (a1 - a0 > (uintptr_t)p.buf_bytes) return -1;
-  bulk_load(buf, (const void*)a0, (unsigned)(a1 - a0), bar);
-  return (int)(((uintptr_t)g0 - a0) >> 3);
+  const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)(nc - 1) * ld + m) + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const void*)a0), "r"((unsigned)(a1 - a0))
+               : "memory");
 }
 
 template <int NRHS>
-__global__ void __launch_bounds__(512) h2b_dataflow_kernel(KParams p) {
+__global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  unsigned char* ws = smem_raw + (size_t)wib * warp_smem_bytes(p.buf_bytes);
-  auto buf = [&](int b) { return (double*)(ws + (size_t)b * p.buf_bytes); };
-  double* xs = (double*)(ws + 2 * (size_t)p.buf_bytes);
+  double* xs = (double*)(smem_raw + (size_t)wib * warp_smem_bytes());
   double* red = xs + kChunkBytes / 8;
-  uint64_t* bars = (uint64_t*)(red + 32);
-  if (lane == 0) {
-    mbar_init(bars);
-    mbar_init(bars + 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
 
   // Completion-driven scheduling: a warp only ever runs items whose inputs
   // are complete.  Items that became ready during this launch (the far-field
   // chain and the finals) are served first from the dynamic queue; otherwise
-  // the warp takes the next initially-ready item (up-leaf, then near field),
-  // whose matrix slice it has already started staging into its second buffer
-  // while the previous item was computed (double buffering with 1-D TMA).
+  // the warp runs its prefetched initially-ready item (up-leaf, then near
+  // field) and claims + L2-prefetches the next one.
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
   const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
-  bool static_done = false;               // lane 0 only
-  int pend = -1, pend_buf = 0, pend_off = -1;  // lane 0 only: prefetched static item
-  unsigned phase = 0;                     // per-buffer mbarrier parity, all lanes
+  bool static_done = false;  // lane 0 state below
+  int pend = -1;             // claimed and prefetched static item
+  int owed = -1;             // claimed dynamic slot whose push is still in flight
   for (;;) {
-    int item = -1, b = 0, off = -1;
+    int item = -1;
     if (lane == 0) {
       unsigned backoff = 64;
       for (;;) {
-        const unsigned h = ld_relaxed(&ctl->ready_head);
-        // One CAS attempt per decision: a won slot is below the tail, so
-        // its pusher is already publishing it (bounded wait, never a wait on
-        // unfinished work); a lost race falls through to other work instead
-        // of retrying (retry loops serialise every contending warp).
-        if (h < ld_relaxed(&ctl->ready_tail) && atomicCAS(&ctl->ready_head, h, h + 1u) == h) {
-          while (ld_acquire(p.ready_flag + h) != e1) __nanosleep(32);
-          item = __ldcg(p.ready_q + h);
-          b = pend >= 0 ? 1 - pend_buf : 0;
-          off = stage_item(p, item, buf(b), bars + b);
-          break;
+        if (owed >= 0) {
+          if (ld_relaxed(p.ready_flag + owed) == e1) {
+            ld_acquire(p.ready_flag + owed);
+            item = __ldcg(p.ready_q + owed);
+            owed = -1;
+            break;
+          }
+        } else if (ld_relaxed(&ctl->ready_head) < ld_relaxed(&ctl->ready_tail)) {
+          // one atomicAdd per claim (CAS loops serialise contending warps);
+          // a lost race yields a slot whose push is still in flight: keep
+          // working on other items and serve it once published
+          const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
+          if (slot < n_dynamic) {
+            if (ld_acquire(p.ready_flag + slot) == e1) {
+              item = __ldcg(p.ready_q + slot);
+              break;
+            }
+            owed = (int)slot;
+          }
         }
         if (pend >= 0) {
-          item = pend; b = pend_buf; off = pend_off;
+          item = pend;
           pend = -1;
           break;
         }
@@ -375,27 +369,24 @@ __global__ void __launch_bounds__(512) h2b_dataflow_kernel(KParams p) {
           const unsigned s = atomicAdd(&ctl->static_head, 1u);
           if (s < (unsigned)p.nready0) {
             item = __ldg(p.ready0 + s);
-            b = 0;
-            off = stage_item(p, item, buf(0), bars);
             break;
           }
           static_done = true;
-          continue;
         }
-        if (h >= n_dynamic) break;  // every item has been claimed
-        // idle while the far-field chain catches up: keep two pollers per
-        // CTA, let the rest retire (the remaining work is latency-bound)
-        if (wib >= 2) break;
+        if (owed < 0) {
+          if (ld_relaxed(&ctl->ready_head) >= n_dynamic) break;  // every item claimed
+          // idle while the far-field chain catches up: keep two pollers per
+          // CTA, let the rest retire (the remaining work is latency-bound)
+          if (wib >= 2) break;
+        }
         __nanosleep(backoff);
-        backoff = min(backoff * 2u, 4096u);
+        backoff = min(backoff * 2u, 2048u);
       }
-      // prefetch the next initially-ready item into the other buffer
       if (item >= 0 && pend < 0 && !static_done) {
         const unsigned s = atomicAdd(&ctl->static_head, 1u);
         if (s < (unsigned)p.nready0) {
           pend = __ldg(p.ready0 + s);
-          pend_buf = 1 - b;
-          pend_off = stage_item(p, pend, buf(pend_buf), bars + pend_buf);
+          prefetch_item(p, pend);
         } else {
           static_done = true;
         }
@@ -403,16 +394,8 @@ __global__ void __launch_bounds__(512) h2b_dataflow_kernel(KParams p) {
     }
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
-    b = __shfl_sync(0xffffffffu, b, 0);
-    off = __shfl_sync(0xffffffffu, off, 0);
     const DTask T = p.tasks[item];
-    if (off >= 0) {
-      mbar_wait(bars + b, (phase >> b) & 1u);
-      phase ^= 1u << b;
-      run_item<NRHS, true>(p, T, buf(b) + off, xs, red, lane);
-    } else {
-      run_item<NRHS, false>(p, T, p.mat + T.data, xs, red, lane);
-    }
+    run_item<NRHS, false>(p, T, p.mat + T.data, xs, red, lane);
     // publish: outputs visible GPU-wide, then count this item into each
     // successor; the warp that completes a successor's count enqueues it
     __syncwarp();
@@ -459,7 +442,6 @@ struct h2b_op {
   int64_t coef_len = 0;
   int max_nrhs = 16;
   int wpc = 8;
-  int buf_bytes = 0;
   int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
   double* d_mat = nullptr;
   double* d_coef = nullptr;
@@ -529,8 +511,8 @@ int nrhs_index(int nrhs) {
 }
 
 template <int NRHS>
-int occupancy_grid(int wpc, int buf_bytes, int ctas_per_sm, int* grid) {
-  const size_t sm = (size_t)wpc * warp_smem_bytes(buf_bytes);
+int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
+  const size_t sm = (size_t)wpc * warp_smem_bytes();
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -562,9 +544,8 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.ready_flag = op->d_ready_flag;
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
-  p.buf_bytes = op->buf_bytes;
   const int gi = nrhs_index(NRHS);
-  const size_t smem = (size_t)op->wpc * warp_smem_bytes(op->buf_bytes);
+  const size_t smem = (size_t)op->wpc * warp_smem_bytes();
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   // the attribute is per function and shared by every operator of the process
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -626,10 +607,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->coef_len = P.coef_len;
   op->max_nrhs = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
   if (nrhs_index(op->max_nrhs) < 0) return fail(H2B_EINVAL, "max_nrhs must be 1, 2, 4, 8 or 16");
-  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 10;
-  if (op->wpc > 16) return fail(H2B_EINVAL, "warps_per_cta must be <= 16");
-  // staging buffer: the largest split item plus 16 bytes of alignment slack
-  op->buf_bytes = (int)(((to_plan_options(o).task_bytes + 16) + 127) & ~(int64_t)127);
+  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
+  if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
 
   // device task / segment arrays
@@ -681,11 +660,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
-  if ((rc = occupancy_grid<1>(op->wpc, op->buf_bytes, cps, &op->grid[0]))) return rc;
-  if ((rc = occupancy_grid<2>(op->wpc, op->buf_bytes, cps, &op->grid[1]))) return rc;
-  if ((rc = occupancy_grid<4>(op->wpc, op->buf_bytes, cps, &op->grid[2]))) return rc;
-  if ((rc = occupancy_grid<8>(op->wpc, op->buf_bytes, cps, &op->grid[3]))) return rc;
-  if ((rc = occupancy_grid<16>(op->wpc, op->buf_bytes, cps, &op->grid[4]))) return rc;
+  if ((rc = occupancy_grid<1>(op->wpc, cps, &op->grid[0]))) return rc;
+  if ((rc = occupancy_grid<2>(op->wpc, cps, &op->grid[1]))) return rc;
+  if ((rc = occupancy_grid<4>(op->wpc, cps, &op->grid[2]))) return rc;
+  if ((rc = occupancy_grid<8>(op->wpc, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->wpc, cps, &op->grid[4]))) return rc;
   H2B_CUDA(cudaDeviceSynchronize());
 
   fill_stats(P, &op->stats);
