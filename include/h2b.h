@@ -81,9 +81,8 @@ typedef struct h2b_options {
   int32_t warps_per_cta;/* persistent CTA width in warps (default 10, <= 16) */
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
-  int32_t interleave;   /* 0 (default) = interleave near-field work items
-                           between far-field tree levels in the queue;
-                           -1 = far field first, near field after            */
+  int32_t l2_prefetch;  /* 1: 1-D TMA L2 prefetch (cp.async.bulk.prefetch) of
+                           the work item claimed ahead; 0 (default): off     */
   /* Multi-GPU (one process per GPU).  world_size <= 1: whole operator. */
   int32_t rank;
   int32_t world_size;

@@ -1,24 +1,25 @@
 // h2b.cu — B200 (sm_100a) H² matvec: one persistent dataflow kernel + C ABI.
 //
-// The whole product y = M x (h2.py:186-244) is ONE kernel launch.  The host
-// planner (plan.cpp) turns every small GEMV of the reference's four loops into
-// a work item of the form
+// The whole product y = M x (h2.py:186-244) is one permutation-gather launch
+// (xp = x[perm]) plus ONE persistent kernel.  The host planner (plan.cpp)
+// turns every small GEMV of the reference's four loops into a work item
 //
 //     out[0:m] = bias[0:m] + A[0:m, 0:ncols] @ gather(segments)
 //
-// stored in a topologically ordered queue.  Persistent warps pull items with
-// an atomic ticket, wait (acquire) on the items they depend on, stream their
-// column-major slice of the matrix pool from HBM with 64-bit
-// ld.global.nc.L1::no_allocate loads, and publish (release) a per-item flag.
-// Near-field items (no dependencies, ~80% of the bytes) are interleaved
-// between the tree levels of the far field, so the level-by-level latency of
-// the upward/downward passes hides under the near-field stream.
+// over a column-major slice of one packed matrix pool.  Scheduling is
+// completion driven: items without inputs (up-leaf, near field) start in a
+// static queue; each finished item counts itself into its successors, and
+// the warp that completes a successor's count pushes it onto a dynamic
+// ready queue, which warps serve first (the far-field tree chain is the
+// critical path).  No warp ever waits on an unfinished item.
 //
-// Lanes own rows (r = lane, lane + 32) so every column is a contiguous,
-// coalesced read and no cross-lane reduction is needed; small items
-// (m <= 16) pack several columns per warp instruction and reduce once.
-// Partial sums of split rows are written to separate slots and summed by the
-// consumer in a fixed order: results are deterministic, no float atomics.
+// Streaming: lanes own rows (r = lane, lane + 32) so every column is one
+// contiguous, coalesced read with no cross-lane reduction; 16 columns of
+// 64-bit ld.global.nc.L1::no_allocate loads are in flight per lane, and the
+// first 16 are issued before the item's sources are gathered.  Items with
+// m <= 16 pack 32/m columns per warp instruction and reduce once.  Split
+// rows write partial slots that the consumer adds in a fixed order:
+// deterministic, no floating-point atomics.
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -67,16 +68,14 @@ struct __align__(8) DSeg {
 static_assert(sizeof(DSeg) == 24, "DSeg layout");
 
 // Scheduler state (one per operator).  Every counter is reset by the last
-// warp to leave a launch, and `epoch` counts launches, so nothing has to be
-// cleared between products.
-// Each hot counter sits on its own 128-byte line so that polling one does not
-// queue behind atomics on another in the same L2 slice.
+// warp to leave a launch and `epoch` counts launches, so nothing is cleared
+// between products.  Each hot counter sits on its own 128-byte line.
 struct Ctl {
-  unsigned ready_head;   // next slot of the dynamic ready queue to pop
+  unsigned ready_head;   // next slot of the dynamic ready queue to claim
   unsigned pad0[31];
   unsigned ready_tail;   // next slot to push
   unsigned pad1[31];
-  unsigned static_head;  // next initially-ready item to take
+  unsigned static_head;  // next initially-ready item to claim
   unsigned pad2[31];
   unsigned exited;       // warps that left the scheduler loop
   unsigned epoch;        // launches completed so far
@@ -92,7 +91,7 @@ struct KParams {
   const double* __restrict__ mat;
   double* coef;
   const int64_t* __restrict__ perm;
-  const double* __restrict__ x;
+  const double* __restrict__ xp;        // x in tree order (written by the gather launch)
   double* y;
   unsigned long long* arrived;          // per item: finished predecessors, all launches
   int32_t* ready_q;                     // dynamic ready queue (item ids)
@@ -100,9 +99,22 @@ struct KParams {
   Ctl* ctl;
   int32_t ntasks;
   int32_t nready0;
+  int32_t prefetch;                     // 1: 1-D TMA L2 prefetch of the claimed-ahead item
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
+
+// Per-warp shared memory: gathered sources, the item's segment table and
+// the small-item reduction scratch.
+struct WarpSmem {
+  double xs[kChunkBytes / 8];
+  double red[32];
+  long long seg_src[h2b::kMaxSegs];
+  int seg_off[h2b::kMaxSegs + 1];
+  int seg_kind[h2b::kMaxSegs];
+  int seg_nslots[h2b::kMaxSegs];
+  int seg_stride[h2b::kMaxSegs];
+};
 
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
@@ -123,159 +135,175 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// ---- shared-memory staging with 1-D TMA (cp.async.bulk + mbarrier) -------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// Copy [src, src + bytes) (16-byte aligned, multiple of 16) into dst and
-// signal `bar` when the bytes have landed.  Issued by one lane.
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+// xp = x[perm] (h2.py:192-193), node-major with NRHS columns.
+template <int NRHS>
+__global__ void __launch_bounds__(256) h2b_permute_kernel(const double* __restrict__ x,
+                                                          const int64_t* __restrict__ perm,
+                                                          double* __restrict__ xp, int64_t n) {
+  const int64_t total = n * NRHS;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = i / NRHS, r = i - pos * NRHS;
+    xp[i] = __ldg(x + __ldg(perm + pos) * NRHS + r);
+  }
 }
 
-template <bool SMEM>
-__device__ __forceinline__ double ldA(const double* p) {
-  if constexpr (SMEM) return *p;
-  else return ld_stream(p);
+// Source value (NRHS column r) of item column c, through the warp's segment table.
+template <int NRHS>
+__device__ __forceinline__ double gather_one(const KParams& p, const WarpSmem& w, int c, int r, int& k) {
+  while (w.seg_off[k + 1] <= c) ++k;
+  const int cs = c - w.seg_off[k];
+  if (w.seg_kind[k] == h2b::kSegX) return __ldg(p.xp + (w.seg_src[k] + cs) * NRHS + r);
+  const int64_t base = w.seg_src[k] + cs;
+  double v = 0.0;
+  for (int s = 0; s < w.seg_nslots[k]; ++s)
+    v += __ldcg(p.coef + (base + (int64_t)s * w.seg_stride[k]) * NRHS + r);
+  return v;
 }
 
-// One work item, NRHS right-hand sides, rows r0 = lane, r1 = lane + 32.
-// A is the item's column-major matrix: in shared memory (SMEM, staged by
-// TMA) or streamed straight from global memory.
-template <int NRHS, bool SMEM>
-__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const double* A, double* xs,
-                                         double* red, int lane) {
+// One work item with NRHS right-hand sides.
+template <int NRHS>
+__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpSmem& w, int lane) {
   constexpr int kCols = kChunkBytes / (8 * NRHS);
+  constexpr int U = (NRHS == 1) ? 16 : 4;  // columns in flight per lane
   const int m = T.m, ld = T.ld;
-  const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
-  const int G = grouped ? (32 / m) : 1;
-  const int g = grouped ? (lane / m) : 0;
-  const int rr = grouped ? (lane - g * m) : lane;
-  const bool v0 = grouped ? (g < G) : (lane < m);
-  const bool v1 = !grouped && (lane + 32 < m);
+  const double* A = p.mat + T.data;
 
+  // ---- segment table: one segment per lane, column offsets by warp scan
+  {
+    const int nseg = T.seg1 - T.seg0;  // <= kMaxSegs (planner)
+    int nc = 0;
+    if (lane < nseg) {
+      const DSeg S = p.segs[T.seg0 + lane];
+      nc = S.ncols;
+      w.seg_src[lane] = S.src;
+      w.seg_kind[lane] = S.kind;
+      w.seg_nslots[lane] = S.nslots;
+      w.seg_stride[lane] = S.stride;
+    }
+    int incl = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane < nseg) w.seg_off[lane] = incl - nc;
+    if (lane == nseg - 1 || (nseg == 0 && lane == 0)) w.seg_off[nseg] = incl;
+    if (lane == 0 && nseg < h2b::kMaxSegs) w.seg_off[h2b::kMaxSegs] = 0x7fffffff;
+    __syncwarp();
+  }
+
+  const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
   double acc0[NRHS], acc1[NRHS];
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) { acc0[r] = 0.0; acc1[r] = 0.0; }
 
-  // bias: near-field partial slots of a leaf (summed in slot order)
-  if (T.bias >= 0 && !grouped) {
-    for (int s = 0; s < T.bias_nslots; ++s) {
-      const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        if (v0) acc0[r] += __ldcg(b + (int64_t)lane * NRHS + r);
-        if (v1) acc1[r] += __ldcg(b + (int64_t)(lane + 32) * NRHS + r);
-      }
-    }
-  }
-
-  int si = T.seg0, soff = 0;
-  for (int col = 0; col < T.ncols; col += kCols) {
-    const int cc = min(kCols, T.ncols - col);
-    // ---- gather the sources of columns [col, col + cc) into shared memory
-    int filled = 0;
-    while (filled < cc) {
-      const DSeg S = p.segs[si];
-      const int take = min(S.ncols - soff, cc - filled);
-      for (int j = lane; j < take * NRHS; j += 32) {
-        const int c = j / NRHS, r = j - c * NRHS;
-        double v;
-        if (S.kind == h2b::kSegX) {
-          const int64_t node = __ldg(p.perm + S.src + soff + c);
-          v = __ldg(p.x + node * NRHS + r);
-        } else {
-          v = 0.0;
-          for (int s = 0; s < S.nslots; ++s)
-            v += __ldcg(p.coef + (S.src + (int64_t)s * S.stride + soff + c) * NRHS + r);
-        }
-        xs[(filled + c) * NRHS + r] = v;
-      }
-      filled += take;
-      soff += take;
-      if (soff == S.ncols) { ++si; soff = 0; }
-    }
-    __syncwarp();
-    // ---- the matrix columns
-    const double* Ac = A + (int64_t)col * ld;
-    if (grouped) {
-      // G columns per step; lane (g, rr) reads element (rr, c0 + g): the
-      // warp touches G*m consecutive doubles.
+  if (grouped) {
+    // G columns per step; lane (g, rr) reads element (rr, c + g): the warp
+    // touches G*m consecutive doubles per instruction.
+    const int G = 32 / m, g = lane / m, rr = lane - g * m;
+    const bool v0 = g < G;
+    for (int col = 0; col < T.ncols; col += kCols) {
+      const int cc = min(kCols, T.ncols - col);
+      int k = 0;
+      for (int j = lane; j < cc; j += 32) w.xs[j] = gather_one<NRHS>(p, w, col + j, 0, k);
+      __syncwarp();
+      const double* Ac = A + (int64_t)col * m;
       int c = g;
       for (; c + 7 * G < cc; c += 8 * G) {
         double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
+        for (int u = 0; u < 8; ++u) a[u] = v0 ? ld_stream(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc0[0] = fma(a[u], xs[c + u * G], acc0[0]);
+        for (int u = 0; u < 8; ++u) acc0[0] = fma(a[u], w.xs[c + u * G], acc0[0]);
       }
       for (; c < cc; c += G)
-        if (v0) acc0[0] = fma(ldA<SMEM>(Ac + (int64_t)c * m + rr), xs[c], acc0[0]);
-    } else {
-      int c = 0;
-      constexpr int U = (NRHS == 1) ? 8 : 4;
-      for (; c + U <= cc; c += U) {
-        double a0[U], a1[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          a0[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
-          a1[u] = v1 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            const double xv = xs[(c + u) * NRHS + r];
-            acc0[r] = fma(a0[u], xv, acc0[r]);
-            acc1[r] = fma(a1[u], xv, acc1[r]);
-          }
-        }
-      }
-      for (; c < cc; ++c) {
-        const double a0 = v0 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane) : 0.0;
-        const double a1 = v1 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane + 32) : 0.0;
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
-          const double xv = xs[c * NRHS + r];
-          acc0[r] = fma(a0, xv, acc0[r]);
-          acc1[r] = fma(a1, xv, acc1[r]);
-        }
-      }
+        if (v0) acc0[0] = fma(ld_stream(Ac + (int64_t)c * m + rr), w.xs[c], acc0[0]);
+      __syncwarp();
     }
-    __syncwarp();
-  }
-
-  if (grouped) {
-    red[lane] = acc0[0];
+    w.red[lane] = acc0[0];
     __syncwarp();
     double s = 0.0;
     if (lane < m) {
-      for (int q = 0; q < G; ++q) s += red[q * m + lane];
+      for (int q = 0; q < G; ++q) s += w.red[q * m + lane];
       if (T.bias >= 0)
         for (int b = 0; b < T.bias_nslots; ++b)
           s += __ldcg(p.coef + T.bias + (int64_t)b * T.bias_stride + lane);
     }
     __syncwarp();
     acc0[0] = s;
+  } else {
+    const bool v0 = lane < m, v1 = lane + 32 < m;
+    // bias: near-field partial slots of a leaf (summed in slot order)
+    if (T.bias >= 0) {
+      for (int s = 0; s < T.bias_nslots; ++s) {
+        const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          if (v0) acc0[r] += __ldcg(b + (int64_t)lane * NRHS + r);
+          if (v1) acc1[r] += __ldcg(b + (int64_t)(lane + 32) * NRHS + r);
+        }
+      }
+    }
+    for (int col = 0; col < T.ncols; col += kCols) {
+      const int cc = min(kCols, T.ncols - col);
+      const double* Ac = A + (int64_t)col * ld;
+      // issue the first U columns before gathering the sources (overlap)
+      const int np = min(U, cc);
+      double a0[U], a1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a0[u] = (u < np && v0) ? ld_stream(Ac + (int64_t)u * ld + lane) : 0.0;
+        a1[u] = (u < np && v1) ? ld_stream(Ac + (int64_t)u * ld + lane + 32) : 0.0;
+      }
+      int k = 0;
+      for (int j = lane; j < cc * NRHS; j += 32) {
+        const int c = j / NRHS, r = j - c * NRHS;
+        w.xs[j] = gather_one<NRHS>(p, w, col + c, r, k);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u < np) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            const double xv = w.xs[u * NRHS + r];
+            acc0[r] = fma(a0[u], xv, acc0[r]);
+            acc1[r] = fma(a1[u], xv, acc1[r]);
+          }
+        }
+      }
+      int c = np;
+      for (; c + U <= cc; c += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a0[u] = v0 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
+          a1[u] = v1 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            const double xv = w.xs[(c + u) * NRHS + r];
+            acc0[r] = fma(a0[u], xv, acc0[r]);
+            acc1[r] = fma(a1[u], xv, acc1[r]);
+          }
+        }
+      }
+      for (; c < cc; ++c) {
+        const double b0 = v0 ? ld_stream(Ac + (int64_t)c * ld + lane) : 0.0;
+        const double b1 = v1 ? ld_stream(Ac + (int64_t)c * ld + lane + 32) : 0.0;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          const double xv = w.xs[c * NRHS + r];
+          acc0[r] = fma(b0, xv, acc0[r]);
+          acc1[r] = fma(b1, xv, acc1[r]);
+        }
+      }
+      __syncwarp();
+    }
   }
+
   const bool w0 = lane < m, w1 = lane + 32 < m;
   if (T.kind == h2b::kFinal) {
     if (w0) {
@@ -297,13 +325,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
   }
 }
 
-// Per-warp shared memory: the gathered-source chunk and the small-item
-// reduction scratch.
-__host__ __device__ constexpr size_t warp_smem_bytes() { return (size_t)kChunkBytes + 32 * 8; }
-
-// 1-D TMA prefetch of an item's matrix slice into L2 (cp.async.bulk.prefetch):
-// issued when the item is claimed, one item ahead, so that its column loads
-// hit L2 when the warp gets to it.
+// 1-D TMA prefetch of an item's matrix slice into L2 (cp.async.bulk.prefetch).
 __device__ __forceinline__ void prefetch_item(const KParams& p, int item) {
   const DTask* t = p.tasks + item;
   const int m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
@@ -316,24 +338,23 @@ __device__ __forceinline__ void prefetch_item(const KParams& p, int item) {
 }
 
 template <int NRHS>
-__global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
+__global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  double* xs = (double*)(smem_raw + (size_t)wib * warp_smem_bytes());
-  double* red = xs + kChunkBytes / 8;
+  WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
 
-  // Completion-driven scheduling: a warp only ever runs items whose inputs
-  // are complete.  Items that became ready during this launch (the far-field
-  // chain and the finals) are served first from the dynamic queue; otherwise
-  // the warp runs its prefetched initially-ready item (up-leaf, then near
-  // field) and claims + L2-prefetches the next one.
+  // Completion-driven scheduling (lane 0 decides, the warp executes):
+  //  1. a claimed dynamic slot whose push has landed, or a fresh dynamic
+  //     claim (the far-field chain and the finals go first);
+  //  2. the static item claimed ahead during the previous item;
+  //  3. a fresh static item.
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
   const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
-  bool static_done = false;  // lane 0 state below
-  int pend = -1;             // claimed and prefetched static item
+  bool static_done = false;  // lane-0 state
+  int pend = -1;             // claimed-ahead static item
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   for (;;) {
     int item = -1;
@@ -348,9 +369,9 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
             break;
           }
         } else if (ld_relaxed(&ctl->ready_head) < ld_relaxed(&ctl->ready_tail)) {
-          // one atomicAdd per claim (CAS loops serialise contending warps);
-          // a lost race yields a slot whose push is still in flight: keep
-          // working on other items and serve it once published
+          // one atomicAdd per claim (CAS retry loops serialise contending
+          // warps); a lost race yields a slot whose push is in flight: keep
+          // working on static items and serve the slot once published
           const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
           if (slot < n_dynamic) {
             if (ld_acquire(p.ready_flag + slot) == e1) {
@@ -386,7 +407,7 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
         const unsigned s = atomicAdd(&ctl->static_head, 1u);
         if (s < (unsigned)p.nready0) {
           pend = __ldg(p.ready0 + s);
-          prefetch_item(p, pend);
+          if (p.prefetch) prefetch_item(p, pend);
         } else {
           static_done = true;
         }
@@ -395,7 +416,7 @@ __global__ void __launch_bounds__(256) h2b_dataflow_kernel(KParams p) {
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
     const DTask T = p.tasks[item];
-    run_item<NRHS, false>(p, T, p.mat + T.data, xs, red, lane);
+    run_item<NRHS>(p, T, w, lane);
     // publish: outputs visible GPU-wide, then count this item into each
     // successor; the warp that completes a successor's count enqueues it
     __syncwarp();
@@ -456,6 +477,8 @@ struct h2b_op {
   int64_t* d_perm = nullptr;
   unsigned* d_ready_flag = nullptr;
   Ctl* d_ctl = nullptr;
+  double* d_xp = nullptr;  // x in tree order
+  int prefetch = 0;
   double* d_x = nullptr;
   double* d_y = nullptr;
   size_t xy_cap = 0;
@@ -474,7 +497,6 @@ h2b::PlanOptions to_plan_options(const h2b_options* o) {
   h2b::PlanOptions po;
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
-    po.interleave = o->interleave >= 0;  // 0 (zero-init) = default = interleave
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
   }
@@ -512,7 +534,7 @@ int nrhs_index(int nrhs) {
 
 template <int NRHS>
 int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
-  const size_t sm = (size_t)wpc * warp_smem_bytes();
+  const size_t sm = (size_t)wpc * sizeof(WarpSmem);
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -539,14 +561,20 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.mat = op->d_mat;
   p.coef = op->d_coef;
   p.perm = op->d_perm;
-  p.x = x;
+  p.xp = op->d_xp;
   p.y = y;
+  p.prefetch = op->prefetch;
   p.ready_flag = op->d_ready_flag;
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
   const int gi = nrhs_index(NRHS);
-  const size_t smem = (size_t)op->wpc * warp_smem_bytes();
+  const size_t smem = (size_t)op->wpc * sizeof(WarpSmem);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
+  {
+    const int64_t total = op->n * NRHS;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
+  }
   // the attribute is per function and shared by every operator of the process
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
@@ -583,6 +611,7 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_ctl);
   cudaFree(op->d_x);
   cudaFree(op->d_y);
+  cudaFree(op->d_xp);
   delete op;
 }
 
@@ -610,6 +639,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
+  op->prefetch = (o && o->l2_prefetch > 0) ? 1 : 0;
 
   // device task / segment arrays
   std::vector<DTask> tasks(P.ntasks());
@@ -650,6 +680,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->nready0 = (int32_t)P.ready0.size();
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
+  if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
   if ((rc = upload<unsigned long long>(&op->d_arrived, nullptr, T1))) return rc;
   if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, T1))) return rc;

@@ -210,10 +210,12 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
   for (int64_t si = 0; si < (int64_t)segs.size(); ++si) {
     int64_t nc = segs[si].ncols, c0 = 0;
     if (nc == 0) continue;
-    if (cur.ncols > 0 && cur.ncols + nc > maxc) { pieces.push_back(cur); cur = Piece(); cur.col0 = col; }
+    if (cur.ncols > 0 && (cur.ncols + nc > maxc || (int)cur.parts.size() >= kMaxSegs)) {
+      pieces.push_back(cur); cur = Piece(); cur.col0 = col;
+    }
     while (nc - c0 > 0) {
       int64_t take = std::min(nc - c0, maxc - cur.ncols);
-      if (take <= 0) { pieces.push_back(cur); cur = Piece(); cur.col0 = col; continue; }
+      if (take <= 0 || (int)cur.parts.size() >= kMaxSegs) { pieces.push_back(cur); cur = Piece(); cur.col0 = col; continue; }
       if (cur.ncols == 0) cur.col0 = col;
       cur.parts.push_back({si, c0, take});
       cur.ncols += take; c0 += take; col += take;

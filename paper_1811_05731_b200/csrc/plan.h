@@ -30,11 +30,12 @@ enum TaskKind : int32_t {
 };
 
 enum SegKind : int32_t {
-  kSegX = 0,     // x[perm[src + c]]         (permutation gather, h2.py:192-193)
+  kSegX = 0,     // xp[src + c], xp = x[perm] (permutation gather, h2.py:192-193)
   kSegCoef = 1,  // sum_j coef[src + j*stride + c], j < nslots
 };
 
 constexpr int kMaxRows = 64;  // rows per work item (lanes own rows l, l+32)
+constexpr int kMaxSegs = 32;  // source segments per work item (one per lane)
 
 struct Plan {
   int64_t n = 0;

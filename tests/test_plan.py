@@ -49,9 +49,9 @@ def test_plan_far_and_near_ablations(golden):
         assert rel(y, ref) <= 1e-13, (name, key)
 
 
-def test_plan_without_interleave(golden):
+def test_plan_small_items(golden):
     name, op, ex = golden
-    P = plan_view(op, interleave=-1)
+    P = plan_view(op, task_bytes=256)
     check_plan_invariants(P)
     assert rel(run_plan(P, ex["X"][:, 0]), ex["y_full"][:, 0]) <= 1e-14
 
