@@ -77,6 +77,8 @@ struct Ctl {
   unsigned pad1[31];
   unsigned static_head;  // next initially-ready item to claim
   unsigned pad2[31];
+  unsigned dyn_started;  // dynamic items taken (queue or continuation)
+  unsigned pad4[31];
   unsigned exited;       // warps that left the scheduler loop
   unsigned epoch;        // launches completed so far
   unsigned pad3[30];
@@ -86,7 +88,7 @@ struct KParams {
   const DTask* __restrict__ tasks;
   const DSeg* __restrict__ segs;
   const int32_t* __restrict__ succ0;    // [ntasks+1] successor CSR
-  const int32_t* __restrict__ succ;
+  const int2* __restrict__ succ;         // (successor, its dependency count)
   const int32_t* __restrict__ ready0;   // initially ready items, issue order
   const double* __restrict__ mat;
   double* coef;
@@ -346,6 +348,8 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
 
   // Completion-driven scheduling (lane 0 decides, the warp executes):
+  //  0. a successor this warp just completed (continuation: the critical
+  //     far-field chain never waits for a queue round trip);
   //  1. a claimed dynamic slot whose push has landed, or a fresh dynamic
   //     claim (the far-field chain and the finals go first);
   //  2. the static item claimed ahead during the previous item;
@@ -356,9 +360,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   bool static_done = false;  // lane-0 state
   int pend = -1;             // claimed-ahead static item
   int owed = -1;             // claimed dynamic slot whose push is still in flight
+  int cont = -1;             // continuation (all lanes)
   for (;;) {
-    int item = -1;
-    if (lane == 0) {
+    int item = cont;
+    if (lane == 0 && item < 0) {
       unsigned backoff = 64;
       for (;;) {
         if (owed >= 0) {
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
             ld_acquire(p.ready_flag + owed);
             item = __ldcg(p.ready_q + owed);
             owed = -1;
+            atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
         } else if (ld_relaxed(&ctl->ready_head) < ld_relaxed(&ctl->ready_tail)) {
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           if (slot < n_dynamic) {
             if (ld_acquire(p.ready_flag + slot) == e1) {
               item = __ldcg(p.ready_q + slot);
+              atomicAdd(&ctl->dyn_started, 1u);
               break;
             }
             owed = (int)slot;
@@ -394,12 +401,15 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           }
           static_done = true;
         }
-        if (owed < 0) {
-          if (ld_relaxed(&ctl->ready_head) >= n_dynamic) break;  // every item claimed
-          // idle while the far-field chain catches up: keep two pollers per
-          // CTA, let the rest retire (the remaining work is latency-bound)
-          if (wib >= 2) break;
+        // every dynamic item has started (continuations skip the queue, so
+        // an over-claimed slot may never be pushed): nothing more will come
+        if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
+          owed = -1;
+          break;
         }
+        // idle while the far-field chain catches up: keep two pollers per
+        // CTA, let the rest retire (the remaining work is latency-bound)
+        if (owed < 0 && wib >= 2) break;
         __nanosleep(backoff);
         backoff = min(backoff * 2u, 2048u);
       }
@@ -418,20 +428,36 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     const DTask T = p.tasks[item];
     run_item<NRHS>(p, T, w, lane);
     // publish: outputs visible GPU-wide, then count this item into each
-    // successor; the warp that completes a successor's count enqueues it
+    // successor.  Of the successors whose count this warp completes, it runs
+    // the first one itself next and pushes the others.
     __syncwarp();
     __threadfence();
+    cont = -1;
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
-    for (int k = s0 + lane; k < s1; k += 32) {
-      const int d = __ldg(p.succ + k);
-      const unsigned long long need =
-          (unsigned long long)e1 * (unsigned long long)(__ldg(&p.tasks[d].dep1) - __ldg(&p.tasks[d].dep0));
-      if (atomicAdd(p.arrived + d, 1ull) + 1ull == need) {
+    for (int k0 = s0; k0 < s1; k0 += 32) {
+      const int k = k0 + lane;
+      int d = -1;
+      if (k < s1) {
+        const int2 sd = __ldg(p.succ + k);   // (successor, its dependency count)
+        if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * (unsigned)sd.y) d = sd.x;
+      }
+      unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
+      if (cont < 0 && ready) {
+        const int first = __ffs(ready) - 1;
+        cont = __shfl_sync(0xffffffffu, d, first);
+        if (lane == first) d = -1;
+        ready &= ready - 1;
+      }
+      if (d >= 0) {
         __threadfence();
         const unsigned slot = atomicAdd(&ctl->ready_tail, 1u);
         p.ready_q[slot] = d;
         st_release(p.ready_flag + slot, e1);
       }
+    }
+    if (cont >= 0) {
+      __threadfence();  // acquire side of the other predecessors' releases
+      if (lane == 0) atomicAdd(&ctl->dyn_started, 1u);
     }
     __syncwarp();
   }
@@ -443,6 +469,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       ctl->ready_head = 0;
       ctl->ready_tail = 0;
       ctl->static_head = 0;
+      ctl->dyn_started = 0;
       ctl->exited = 0;
       __threadfence();
       atomicAdd(&ctl->epoch, 1u);
@@ -469,7 +496,7 @@ struct h2b_op {
   DTask* d_tasks = nullptr;
   DSeg* d_segs = nullptr;
   int32_t* d_succ0 = nullptr;
-  int32_t* d_succ = nullptr;
+  int2* d_succ = nullptr;
   int32_t* d_ready0 = nullptr;
   int32_t nready0 = 0;
   unsigned long long* d_arrived = nullptr;
@@ -675,7 +702,14 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
   if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
   if ((rc = upload(&op->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
-  if ((rc = upload(&op->d_succ, P.succ.data(), P.succ.size()))) return rc;
+  {
+    std::vector<int2> sd(P.succ.size());
+    for (size_t k = 0; k < sd.size(); ++k) {
+      const int32_t d = P.succ[k];
+      sd[k] = make_int2(d, P.t_dep0[d + 1] - P.t_dep0[d]);
+    }
+    if ((rc = upload(&op->d_succ, sd.data(), sd.size()))) return rc;
+  }
   if ((rc = upload(&op->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
   op->nready0 = (int32_t)P.ready0.size();
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
