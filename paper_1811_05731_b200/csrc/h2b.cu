@@ -407,11 +407,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           owed = -1;
           break;
         }
-        // idle while the far-field chain catches up: keep two pollers per
-        // CTA, let the rest retire (the remaining work is latency-bound)
-        if (owed < 0 && wib >= 2) break;
+        // idle while the far-field chain catches up (its lower levels are
+        // wide: every warp stays available, polling with backoff)
         __nanosleep(backoff);
-        backoff = min(backoff * 2u, 2048u);
+        backoff = min(backoff * 2u, 1024u);
       }
       if (item >= 0 && pend < 0 && !static_done) {
         const unsigned s = atomicAdd(&ctl->static_head, 1u);
