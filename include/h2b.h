@@ -153,6 +153,12 @@ int64_t h2b_stream_bytes(const h2b_op* op);
 int h2b_stats_get(const h2b_op* op, h2b_stats* out);
 void h2b_destroy(h2b_op* op);
 
+/* Diagnostics: per-work-item timeline of the next products ({start ns,
+ * end ns, (smid << 32) | warp, continuation+1}, globaltimer) and item kinds. */
+int h2b_trace_enable(h2b_op* op, int on);
+int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems);
+int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems);
+
 /* Multi-GPU helper: fill a 128-byte NCCL unique id (rank 0 calls this and
  * broadcasts the bytes to the other ranks, e.g. over torch.distributed). */
 int h2b_nccl_unique_id(void* out128);

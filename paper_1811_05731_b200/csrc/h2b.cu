@@ -102,6 +102,7 @@ struct KParams {
   int32_t ntasks;
   int32_t nready0;
   int32_t prefetch;                     // 1: 1-D TMA L2 prefetch of the claimed-ahead item
+  unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -425,6 +426,8 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
     const DTask T = p.tasks[item];
+    unsigned long long t_start = 0;
+    if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     run_item<NRHS>(p, T, w, lane);
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
@@ -453,6 +456,16 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         p.ready_q[slot] = d;
         st_release(p.ready_flag + slot, e1);
       }
+    }
+    if (p.trace && lane == 0) {
+      unsigned long long t_end, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&smid));
+      smid &= 0xffffffffull;
+      p.trace[4 * item] = t_start;
+      p.trace[4 * item + 1] = t_end;
+      p.trace[4 * item + 2] = (smid << 32) | (unsigned)(blockIdx.x * nw + wib);
+      p.trace[4 * item + 3] = (unsigned long long)(cont >= 0 ? cont + 1 : 0);
     }
     if (cont >= 0) {
       __threadfence();  // acquire side of the other predecessors' releases
@@ -504,6 +517,7 @@ struct h2b_op {
   unsigned* d_ready_flag = nullptr;
   Ctl* d_ctl = nullptr;
   double* d_xp = nullptr;  // x in tree order
+  unsigned long long* d_trace = nullptr;
   int prefetch = 0;
   double* d_x = nullptr;
   double* d_y = nullptr;
@@ -590,6 +604,7 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.xp = op->d_xp;
   p.y = y;
   p.prefetch = op->prefetch;
+  p.trace = op->d_trace;
   p.ready_flag = op->d_ready_flag;
   p.ctl = op->d_ctl;
   p.ntasks = (int32_t)op->ntasks;
@@ -638,6 +653,7 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_xp);
+  cudaFree(op->d_trace);
   delete op;
 }
 
@@ -851,6 +867,33 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
 }
 
 int64_t h2b_stream_bytes(const h2b_op* op) { return op ? op->stats.stream_bytes : -1; }
+
+int h2b_trace_enable(h2b_op* op, int on) {
+  if (!op) return fail(H2B_EINVAL, "null operator");
+  H2B_CUDA(cudaSetDevice(op->device));
+  if (on && !op->d_trace) {
+    H2B_CUDA(cudaMalloc(&op->d_trace, sizeof(unsigned long long) * 4 * std::max<int64_t>(1, op->ntasks)));
+    H2B_CUDA(cudaMemset(op->d_trace, 0, sizeof(unsigned long long) * 4 * std::max<int64_t>(1, op->ntasks)));
+  } else if (!on && op->d_trace) {
+    cudaFree(op->d_trace);
+    op->d_trace = nullptr;
+  }
+  return H2B_OK;
+}
+
+int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems) {
+  if (!op || !out || nitems != op->ntasks || !op->d_trace) return fail(H2B_EINVAL, "trace not enabled or wrong size");
+  H2B_CUDA(cudaMemcpy(out, op->d_trace, sizeof(uint64_t) * 4 * nitems, cudaMemcpyDeviceToHost));
+  return H2B_OK;
+}
+
+int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems) {
+  if (!op || !out || nitems != op->ntasks) return fail(H2B_EINVAL, "wrong size");
+  std::vector<DTask> t(nitems);
+  H2B_CUDA(cudaMemcpy(t.data(), op->d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < nitems; ++i) out[i] = t[i].kind;
+  return H2B_OK;
+}
 
 int h2b_stats_get(const h2b_op* op, h2b_stats* out) {
   if (!op || !out) return fail(H2B_EINVAL, "null argument");

@@ -1,0 +1,105 @@
+"""Per-work-item timeline of one H² product (diagnostics).
+
+    python tools/trace.py --config config2 [--ablate far|near] [--opts '{}']
+
+Prints per-kind item statistics and the critical path: walking back from
+the last item to finish, each step goes to the predecessor that finished
+last, with the gap between that predecessor's end and the item's start
+(scheduling latency) and the item's own duration."""
+
+import argparse
+import ctypes as C
+import dataclasses
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+KINDS = ("up_leaf", "up_node", "down", "near", "final")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="config2")
+    ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
+    ap.add_argument("--ablate", default="")
+    ap.add_argument("--opts", default="{}")
+    ap.add_argument("--save", default="")
+    a = ap.parse_args()
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1811_05731_b200 import _native as nat
+    from paper_1811_05731_b200.h2 import DeviceOperator, plan_view
+    from paper_1811_05731_b200.workloads import build_workload, vector_for
+    op, _ = build_workload(a.config, cache_dir=a.cache_dir, log=lambda m: print(m, file=sys.stderr))
+    if a.ablate == "far":
+        op = dataclasses.replace(op, near=[])
+    elif a.ablate == "near":
+        op = dataclasses.replace(op, coupling=[])
+    opts = json.loads(a.opts)
+    plan = plan_view(op, **opts)
+    dev = DeviceOperator(op, **opts)
+    lib = nat.lib()
+    lib.h2b_trace_enable.argtypes = [C.c_void_p, C.c_int]
+    lib.h2b_trace_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
+    y = torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(5):
+        dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s)
+    nat.check(lib.h2b_trace_enable(dev._h, 1))
+    for _ in range(3):
+        dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s)
+    torch.cuda.synchronize()
+    T = plan["t_m"].size
+    tr = np.zeros((T, 4), np.uint64)
+    nat.check(lib.h2b_trace_read(dev._h, tr.ctypes.data, T))
+    start = tr[:, 0].astype(np.int64)
+    end = tr[:, 1].astype(np.int64)
+    t0 = start.min()
+    start -= t0
+    end -= t0
+    kind = plan["t_kind"]
+    dur = end - start
+    nbytes = 8 * plan["t_m"].astype(np.int64) * plan["t_ncols"]
+    print(f"items {T}, span {end.max() / 1e3:.1f} us, bytes {nbytes.sum() / 1e6:.1f} MB")
+    for k in range(5):
+        sel = kind == k
+        if sel.any():
+            print(f"  {KINDS[k]:8s} n={sel.sum():6d} dur mean {dur[sel].mean() / 1e3:6.2f} us  "
+                  f"p90 {np.percentile(dur[sel], 90) / 1e3:6.2f}  start [{start[sel].min() / 1e3:7.1f}, "
+                  f"{start[sel].max() / 1e3:7.1f}]  end max {end[sel].max() / 1e3:7.1f} us  "
+                  f"MB {nbytes[sel].sum() / 1e6:7.1f}")
+    # critical path
+    dep0, deps = plan["t_dep0"], plan["deps"]
+    cur = int(np.argmax(end))
+    path = []
+    while True:
+        d = deps[dep0[cur]:dep0[cur + 1]]
+        if d.size == 0:
+            path.append((cur, None))
+            break
+        last = int(d[np.argmax(end[d])])
+        path.append((cur, last))
+        cur = last
+    print(f"critical path: {len(path)} items")
+    for it, pred in path[::-1]:
+        gap = (start[it] - end[pred]) / 1e3 if pred is not None else start[it] / 1e3
+        print(f"  {KINDS[kind[it]]:8s} m={plan['t_m'][it]:3d} ncols={plan['t_ncols'][it]:4d} "
+              f"ndeps={dep0[it + 1] - dep0[it]:3d} start {start[it] / 1e3:7.1f} dur {dur[it] / 1e3:5.2f} "
+              f"gap {gap:5.2f} us cont={int(tr[it, 3]) > 0}")
+    # warps busy over time
+    bins = np.linspace(0, end.max(), 21)
+    busy = [(np.minimum(end, b1) - np.maximum(start, b0)).clip(0).sum() / (b1 - b0) for b0, b1 in zip(bins, bins[1:])]
+    print("avg busy warps per 5% of span:", " ".join(f"{b:.0f}" for b in busy))
+    if a.save:
+        np.savez_compressed(a.save, start=start, end=end, kind=kind, tr=tr)
+
+
+if __name__ == "__main__":
+    main()
