@@ -77,7 +77,9 @@ typedef struct h2b_desc {
 
 /* Execution-plan knobs.  Zero-initialise for defaults. */
 typedef struct h2b_options {
-  int64_t task_bytes;   /* max streamed bytes per work item (default 8192)   */
+  int64_t task_bytes;   /* max bytes per near-field work item (def. 16384)   */
+  int64_t far_task_bytes; /* max bytes per far-field item (default 4096): each
+                             is staged to shared memory by one TMA bulk copy */
   int32_t warps_per_cta;/* persistent CTA width in warps (default 10, <= 16) */
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */

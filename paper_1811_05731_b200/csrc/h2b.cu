@@ -106,11 +106,15 @@ struct KParams {
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
+constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
 
-// Per-warp shared memory: gathered sources, the item's segment table and
-// the small-item reduction scratch.
-struct WarpSmem {
+// Per-warp shared memory: the TMA-staged matrix of a far-field item,
+// gathered sources, the item's segment table, the small-item reduction
+// scratch and the staging mbarrier.
+struct __align__(128) WarpSmem {
+  double abuf[kStageBytes / 8];
   double xs[kChunkBytes / 8];
+  unsigned long long bar;
   double red[32];
   long long seg_src[h2b::kMaxSegs];
   int seg_off[h2b::kMaxSegs + 1];
@@ -136,6 +140,31 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
 }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- 1-D TMA (cp.async.bulk) staging into shared memory, mbarrier completion
+__device__ __forceinline__ uint32_t smem_u32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// One lane: copy [src, src + bytes) (16-byte aligned, multiple of 16) to dst,
+// completing the current phase of `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after generic reads of dst
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 // xp = x[perm] (h2.py:192-193), node-major with NRHS columns.
@@ -164,13 +193,21 @@ __device__ __forceinline__ double gather_one(const KParams& p, const WarpSmem& w
   return v;
 }
 
-// One work item with NRHS right-hand sides.
-template <int NRHS>
-__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpSmem& w, int lane) {
+template <bool SMEM>
+__device__ __forceinline__ double ldA(const double* q) {
+  if constexpr (SMEM) return *q;
+  else return ld_stream(q);
+}
+
+// One work item with NRHS right-hand sides.  A is the item's column-major
+// matrix: staged in shared memory by a TMA bulk copy that completes on `bar`
+// (SMEM), or streamed from global memory.
+template <int NRHS, bool SMEM>
+__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpSmem& w, int lane,
+                                         const double* A, uint64_t* bar, unsigned parity) {
   constexpr int kCols = kChunkBytes / (8 * NRHS);
   constexpr int U = (NRHS == 1) ? 16 : 4;  // columns in flight per lane
   const int m = T.m, ld = T.ld;
-  const double* A = p.mat + T.data;
 
   // ---- segment table: one segment per lane, column offsets by warp scan
   {
@@ -211,17 +248,18 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
       int k = 0;
       for (int j = lane; j < cc; j += 32) w.xs[j] = gather_one<NRHS>(p, w, col + j, 0, k);
       __syncwarp();
+      if (SMEM && col == 0) mbar_wait(bar, parity);
       const double* Ac = A + (int64_t)col * m;
       int c = g;
       for (; c + 7 * G < cc; c += 8 * G) {
         double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = v0 ? ld_stream(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
+        for (int u = 0; u < 8; ++u) a[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u * G) * m + rr) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc0[0] = fma(a[u], w.xs[c + u * G], acc0[0]);
       }
       for (; c < cc; c += G)
-        if (v0) acc0[0] = fma(ld_stream(Ac + (int64_t)c * m + rr), w.xs[c], acc0[0]);
+        if (v0) acc0[0] = fma(ldA<SMEM>(Ac + (int64_t)c * m + rr), w.xs[c], acc0[0]);
       __syncwarp();
     }
     w.red[lane] = acc0[0];
@@ -237,9 +275,31 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
     acc0[0] = s;
   } else {
     const bool v0 = lane < m, v1 = lane + 32 < m;
-    // bias: near-field partial slots of a leaf (summed in slot order)
+    // bias: near-field partial slots of a leaf, summed in slot order (loads
+    // batched four at a time: heavy rows have hundreds of slots)
     if (T.bias >= 0) {
-      for (int s = 0; s < T.bias_nslots; ++s) {
+      int s = 0;
+      constexpr int QB = NRHS <= 2 ? 4 : 1;
+      for (; s + QB <= T.bias_nslots; s += QB) {
+        double b0[QB][NRHS], b1[QB][NRHS];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const double* b = p.coef + (T.bias + (int64_t)(s + q) * T.bias_stride) * NRHS;
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            b0[q][r] = v0 ? __ldcg(b + (int64_t)lane * NRHS + r) : 0.0;
+            b1[q][r] = v1 ? __ldcg(b + (int64_t)(lane + 32) * NRHS + r) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q)
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            acc0[r] += b0[q][r];
+            acc1[r] += b1[q][r];
+          }
+      }
+      for (; s < T.bias_nslots; ++s) {
         const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) {
@@ -251,8 +311,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
     for (int col = 0; col < T.ncols; col += kCols) {
       const int cc = min(kCols, T.ncols - col);
       const double* Ac = A + (int64_t)col * ld;
-      // issue the first U columns before gathering the sources (overlap)
-      const int np = min(U, cc);
+      // global path: issue the first U columns before gathering the sources
+      const int np = SMEM ? 0 : min(U, cc);
       double a0[U], a1[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -265,6 +325,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
         w.xs[j] = gather_one<NRHS>(p, w, col + c, r, k);
       }
       __syncwarp();
+      if (SMEM && col == 0) mbar_wait(bar, parity);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u < np) {
@@ -280,8 +341,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
       for (; c + U <= cc; c += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          a0[u] = v0 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
-          a1[u] = v1 ? ld_stream(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
+          a0[u] = v0 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane) : 0.0;
+          a1[u] = v1 ? ldA<SMEM>(Ac + (int64_t)(c + u) * ld + lane + 32) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -294,8 +355,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
         }
       }
       for (; c < cc; ++c) {
-        const double b0 = v0 ? ld_stream(Ac + (int64_t)c * ld + lane) : 0.0;
-        const double b1 = v1 ? ld_stream(Ac + (int64_t)c * ld + lane + 32) : 0.0;
+        const double b0 = v0 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane) : 0.0;
+        const double b1 = v1 ? ldA<SMEM>(Ac + (int64_t)c * ld + lane + 32) : 0.0;
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) {
           const double xv = w.xs[c * NRHS + r];
@@ -328,18 +389,6 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
   }
 }
 
-// 1-D TMA prefetch of an item's matrix slice into L2 (cp.async.bulk.prefetch).
-__device__ __forceinline__ void prefetch_item(const KParams& p, int item) {
-  const DTask* t = p.tasks + item;
-  const int m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
-  if (nc <= 0) return;
-  const double* g0 = p.mat + __ldg(&t->data);
-  const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-  const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)(nc - 1) * ld + m) + 15) & ~(uintptr_t)15;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const void*)a0), "r"((unsigned)(a1 - a0))
-               : "memory");
-}
-
 template <int NRHS>
 __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -347,19 +396,24 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(&w.bar);
+  if (lane == 0) {
+    mbar_init(bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase = 0;  // parity of the staging mbarrier (all lanes)
 
   // Completion-driven scheduling (lane 0 decides, the warp executes):
   //  0. a successor this warp just completed (continuation: the critical
   //     far-field chain never waits for a queue round trip);
   //  1. a claimed dynamic slot whose push has landed, or a fresh dynamic
   //     claim (the far-field chain and the finals go first);
-  //  2. the static item claimed ahead during the previous item;
-  //  3. a fresh static item.
+  //  2. a static item (up-leaf first, then the near field).
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
   const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
   bool static_done = false;  // lane-0 state
-  int pend = -1;             // claimed-ahead static item
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   int cont = -1;             // continuation (all lanes)
   for (;;) {
@@ -389,11 +443,6 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
             owed = (int)slot;
           }
         }
-        if (pend >= 0) {
-          item = pend;
-          pend = -1;
-          break;
-        }
         if (!static_done) {
           const unsigned s = atomicAdd(&ctl->static_head, 1u);
           if (s < (unsigned)p.nready0) {
@@ -413,22 +462,36 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         __nanosleep(backoff);
         backoff = min(backoff * 2u, 1024u);
       }
-      if (item >= 0 && pend < 0 && !static_done) {
-        const unsigned s = atomicAdd(&ctl->static_head, 1u);
-        if (s < (unsigned)p.nready0) {
-          pend = __ldg(p.ready0 + s);
-          if (p.prefetch) prefetch_item(p, pend);
-        } else {
-          static_done = true;
-        }
-      }
     }
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
-    const DTask T = p.tasks[item];
     unsigned long long t_start = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    run_item<NRHS>(p, T, w, lane);
+    // Far-field items (the latency-critical chain) are staged whole into
+    // shared memory by one TMA bulk copy, overlapping the source gather;
+    // near-field items stream from global memory with 16 columns in flight.
+    int off = -1;
+    if (lane == 0) {
+      const DTask* t = p.tasks + item;
+      const int kind = __ldg(&t->kind), m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
+      if (kind != h2b::kNear && ld == m && nc > 0) {
+        const double* g0 = p.mat + __ldg(&t->data);
+        const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+        const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)m * nc) + 15) & ~(uintptr_t)15;
+        if (a1 - a0 <= (uintptr_t)kStageBytes) {
+          bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
+          off = (int)(((uintptr_t)g0 - a0) >> 3);
+        }
+      }
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
+    const DTask T = p.tasks[item];
+    if (off >= 0) {
+      run_item<NRHS, true>(p, T, w, lane, w.abuf + off, bar, phase);
+      phase ^= 1u;
+    } else {
+      run_item<NRHS, false>(p, T, w, lane, p.mat + T.data, bar, phase);
+    }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
     // the first one itself next and pushes the others.
@@ -537,6 +600,7 @@ h2b::PlanOptions to_plan_options(const h2b_options* o) {
   h2b::PlanOptions po;
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
+    if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
   }

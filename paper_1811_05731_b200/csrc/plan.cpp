@@ -204,7 +204,10 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
   P.bytes_by_kind[kind] += 8 * (int64_t)m_total * C;
   // 2. split columns into pieces of <= task_bytes (at segment boundaries when possible)
   std::vector<Piece> pieces;
-  const int64_t maxc = allow_split ? std::max<int64_t>(1, opt_.task_bytes / (8 * (int64_t)m_total)) : INT64_MAX;
+  // Far-field items are latency-critical (the tree chain): small pieces, each
+  // staged by one TMA bulk copy.  Near-field items are bandwidth work.
+  const int64_t cap = kind == kNear ? opt_.task_bytes : opt_.far_task_bytes;
+  const int64_t maxc = allow_split ? std::max<int64_t>(1, cap / (8 * (int64_t)m_total)) : INT64_MAX;
   Piece cur;
   int64_t col = 0;
   for (int64_t si = 0; si < (int64_t)segs.size(); ++si) {
@@ -484,7 +487,7 @@ int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string
     *err = "multi-GPU plans are built per rank by the partitioner (not yet available)";
     return H2B_EINVAL;
   }
-  if (opt.task_bytes < 8) { *err = "task_bytes must be >= 8"; return H2B_EINVAL; }
+  if (opt.task_bytes < 8 || opt.far_task_bytes < 8) { *err = "task_bytes must be >= 8"; return H2B_EINVAL; }
   Builder b(d, opt, out);
   return b.run(err);
 }

@@ -68,7 +68,8 @@ struct Plan {
 };
 
 struct PlanOptions {
-  int64_t task_bytes = 8192;
+  int64_t task_bytes = 16384;     // near-field items
+  int64_t far_task_bytes = 4096;  // up-leaf, up-node and down items
   bool interleave = true;
   int32_t rank = 0;
   int32_t world_size = 1;

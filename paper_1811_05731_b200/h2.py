@@ -179,10 +179,11 @@ def describe(op) -> _DescHolder:
     return _DescHolder(op)
 
 
-def _options(task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, l2_prefetch=0,
+def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, l2_prefetch=0,
              rank=0, world_size=1) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
+    o.far_task_bytes = int(far_task_bytes)
     o.warps_per_cta = int(warps_per_cta)
     o.ctas_per_sm = int(ctas_per_sm)
     o.max_nrhs = int(max_nrhs)
