@@ -138,6 +138,7 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -279,7 +280,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
     // batched four at a time: heavy rows have hundreds of slots)
     if (T.bias >= 0) {
       int s = 0;
-      constexpr int QB = NRHS <= 2 ? 4 : 1;
+      constexpr int QB = NRHS == 1 ? 16 : (NRHS == 2 ? 4 : 1);
       for (; s + QB <= T.bias_nslots; s += QB) {
         double b0[QB][NRHS], b1[QB][NRHS];
 #pragma unroll
@@ -435,7 +436,12 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           // working on static items and serve the slot once published
           const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
           if (slot < n_dynamic) {
-            if (ld_acquire(p.ready_flag + slot) == e1) {
+            // the pusher bumped the tail first and publishes the id a few
+            // instructions later: wait briefly before parking the claim
+            bool ready = false;
+            for (int spin = 0; spin < 64 && !(ready = ld_acquire(p.ready_flag + slot) == e1); ++spin)
+              __nanosleep(32);
+            if (ready) {
               item = __ldcg(p.ready_q + slot);
               atomicAdd(&ctl->dyn_started, 1u);
               break;
@@ -486,6 +492,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     }
     off = __shfl_sync(0xffffffffu, off, 0);
     const DTask T = p.tasks[item];
+    // successor list, fetched now so that its latency hides under the item
+    const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
+    int2 sd_first = make_int2(-1, 0);
+    if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (off >= 0) {
       run_item<NRHS, true>(p, T, w, lane, w.abuf + off, bar, phase);
       phase ^= 1u;
@@ -496,14 +506,14 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     // successor.  Of the successors whose count this warp completes, it runs
     // the first one itself next and pushes the others.
     __syncwarp();
-    __threadfence();
+    fence_acq_rel();
     cont = -1;
-    const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
     for (int k0 = s0; k0 < s1; k0 += 32) {
       const int k = k0 + lane;
       int d = -1;
       if (k < s1) {
-        const int2 sd = __ldg(p.succ + k);   // (successor, its dependency count)
+        // (successor, its dependency count)
+        const int2 sd = k0 == s0 ? sd_first : __ldg(p.succ + k);
         if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * (unsigned)sd.y) d = sd.x;
       }
       unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         ready &= ready - 1;
       }
       if (d >= 0) {
-        __threadfence();
+        fence_acq_rel();
         const unsigned slot = atomicAdd(&ctl->ready_tail, 1u);
         p.ready_q[slot] = d;
         st_release(p.ready_flag + slot, e1);
@@ -531,14 +541,14 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       p.trace[4 * item + 3] = (unsigned long long)(cont >= 0 ? cont + 1 : 0);
     }
     if (cont >= 0) {
-      __threadfence();  // acquire side of the other predecessors' releases
+      fence_acq_rel();  // acquire side of the other predecessors' releases
       if (lane == 0) atomicAdd(&ctl->dyn_started, 1u);
     }
     __syncwarp();
   }
   if (lane == 0) {
     const unsigned total = gridDim.x * (unsigned)nw;
-    __threadfence();
+    fence_acq_rel();
     if (atomicAdd(&ctl->exited, 1u) == total - 1) {
       // every warp has left the loop: reset the counters for the next launch
       ctl->ready_head = 0;
@@ -546,7 +556,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       ctl->static_head = 0;
       ctl->dyn_started = 0;
       ctl->exited = 0;
-      __threadfence();
+      fence_acq_rel();
       atomicAdd(&ctl->epoch, 1u);
     }
   }
