@@ -71,10 +71,14 @@ static_assert(sizeof(DSeg) == 24, "DSeg layout");
 // warp to leave a launch and `epoch` counts launches, so nothing is cleared
 // between products.  Each hot counter sits on its own 128-byte line.
 struct Ctl {
-  unsigned ready_head;   // next slot of the dynamic ready queue to claim
+  unsigned ready_head;   // class-0 dynamic queue: next slot to claim
   unsigned pad0[31];
-  unsigned ready_tail;   // next slot to push
+  unsigned ready_tail;   // class-0 dynamic queue: next slot to push
   unsigned pad1[31];
+  unsigned lo_head;      // class-1 dynamic queue (slack work)
+  unsigned pad5[31];
+  unsigned lo_tail;
+  unsigned pad6[31];
   unsigned static_head;  // next initially-ready item to claim
   unsigned pad2[31];
   unsigned dyn_started;  // dynamic items taken (queue or continuation)
@@ -101,6 +105,7 @@ struct KParams {
   Ctl* ctl;
   int32_t ntasks;
   int32_t nready0;
+  int32_t nready0_hi;                   // ready0[0:nready0_hi) are class 0
   int32_t prefetch;                     // 1: 1-D TMA L2 prefetch of the claimed-ahead item
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
 };
@@ -420,6 +425,28 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   for (;;) {
     int item = cont;
     if (lane == 0 && item < 0) {
+      // claim from dynamic queue q (0: critical chain, 1: slack); returns the
+      // item, or -1 with `owed` set when the claimed slot is still in flight
+      auto claim = [&](int q) -> int {
+        unsigned* head = q ? &ctl->lo_head : &ctl->ready_head;
+        unsigned* tail = q ? &ctl->lo_tail : &ctl->ready_tail;
+        if (ld_relaxed(head) >= ld_relaxed(tail)) return -1;
+        // one atomicAdd per claim (CAS retry loops serialise contending warps)
+        const unsigned slot = atomicAdd(head, 1u);
+        if (slot >= n_dynamic) return -1;
+        const unsigned abs = (unsigned)q * (unsigned)p.ntasks + slot;
+        // the pusher bumped the tail first and publishes the id a few
+        // instructions later: wait briefly before parking the claim
+        for (int spin = 0; spin < 64; ++spin) {
+          if (ld_acquire(p.ready_flag + abs) == e1) {
+            atomicAdd(&ctl->dyn_started, 1u);
+            return __ldcg(p.ready_q + abs);
+          }
+          __nanosleep(32);
+        }
+        owed = (int)abs;
+        return -1;
+      };
       unsigned backoff = 64;
       for (;;) {
         if (owed >= 0) {
@@ -430,25 +457,19 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
             atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
-        } else if (ld_relaxed(&ctl->ready_head) < ld_relaxed(&ctl->ready_tail)) {
-          // one atomicAdd per claim (CAS retry loops serialise contending
-          // warps); a lost race yields a slot whose push is in flight: keep
-          // working on static items and serve the slot once published
-          const unsigned slot = atomicAdd(&ctl->ready_head, 1u);
-          if (slot < n_dynamic) {
-            // the pusher bumped the tail first and publishes the id a few
-            // instructions later: wait briefly before parking the claim
-            bool ready = false;
-            for (int spin = 0; spin < 64 && !(ready = ld_acquire(p.ready_flag + slot) == e1); ++spin)
-              __nanosleep(32);
-            if (ready) {
-              item = __ldcg(p.ready_q + slot);
-              atomicAdd(&ctl->dyn_started, 1u);
-              break;
-            }
-            owed = (int)slot;
-          }
+        } else if ((item = claim(0)) >= 0) {
+          break;
         }
+        // class-0 static items (up-leaf) before any slack work
+        if (!static_done && ld_relaxed(&ctl->static_head) < (unsigned)p.nready0_hi) {
+          const unsigned s = atomicAdd(&ctl->static_head, 1u);
+          if (s < (unsigned)p.nready0) {
+            item = __ldg(p.ready0 + s);
+            break;
+          }
+          static_done = true;
+        }
+        if (owed < 0 && (item = claim(1)) >= 0) break;
         if (!static_done) {
           const unsigned s = atomicAdd(&ctl->static_head, 1u);
           if (s < (unsigned)p.nready0) {
@@ -457,7 +478,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           }
           static_done = true;
         }
-        // every dynamic item has started (continuations skip the queue, so
+        // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
         if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
           owed = -1;
@@ -510,11 +531,13 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     cont = -1;
     for (int k0 = s0; k0 < s1; k0 += 32) {
       const int k = k0 + lane;
-      int d = -1;
+      int d = -1, dq = 0;
       if (k < s1) {
         // (successor, its dependency count)
         const int2 sd = k0 == s0 ? sd_first : __ldg(p.succ + k);
-        if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * (unsigned)sd.y) d = sd.x;
+        const unsigned ndep = (unsigned)sd.y & 0xffffffu;
+        if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) d = sd.x;
+        dq = sd.y >> 24;
       }
       unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
       if (cont < 0 && ready) {
@@ -525,7 +548,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       }
       if (d >= 0) {
         fence_acq_rel();
-        const unsigned slot = atomicAdd(&ctl->ready_tail, 1u);
+        const unsigned slot = (unsigned)dq * (unsigned)p.ntasks + atomicAdd(dq ? &ctl->lo_tail : &ctl->ready_tail, 1u);
         p.ready_q[slot] = d;
         st_release(p.ready_flag + slot, e1);
       }
@@ -553,6 +576,8 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       // every warp has left the loop: reset the counters for the next launch
       ctl->ready_head = 0;
       ctl->ready_tail = 0;
+      ctl->lo_head = 0;
+      ctl->lo_tail = 0;
       ctl->static_head = 0;
       ctl->dyn_started = 0;
       ctl->exited = 0;
@@ -584,6 +609,7 @@ struct h2b_op {
   int2* d_succ = nullptr;
   int32_t* d_ready0 = nullptr;
   int32_t nready0 = 0;
+  int32_t nready0_hi = 0;
   unsigned long long* d_arrived = nullptr;
   int32_t* d_ready_q = nullptr;
   int64_t* d_perm = nullptr;
@@ -670,6 +696,7 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   p.succ = op->d_succ;
   p.ready0 = op->d_ready0;
   p.nready0 = op->nready0;
+  p.nready0_hi = op->nready0_hi;
   p.arrived = op->d_arrived;
   p.ready_q = op->d_ready_q;
   p.mat = op->d_mat;
@@ -795,22 +822,24 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     std::vector<int2> sd(P.succ.size());
     for (size_t k = 0; k < sd.size(); ++k) {
       const int32_t d = P.succ[k];
-      sd[k] = make_int2(d, P.t_dep0[d + 1] - P.t_dep0[d]);
+      // low 24 bits: dependency count; bit 24: the successor's queue class
+      sd[k] = make_int2(d, (P.t_dep0[d + 1] - P.t_dep0[d]) | ((int)P.t_qclass[d] << 24));
     }
     if ((rc = upload(&op->d_succ, sd.data(), sd.size()))) return rc;
   }
   if ((rc = upload(&op->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
   op->nready0 = (int32_t)P.ready0.size();
+  op->nready0_hi = P.n_ready0_hi;
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
   if ((rc = upload<unsigned long long>(&op->d_arrived, nullptr, T1))) return rc;
-  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, T1))) return rc;
-  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, T1))) return rc;
+  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, 2 * T1))) return rc;   // two classes
+  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, 2 * T1))) return rc;
   if ((rc = upload<Ctl>(&op->d_ctl, nullptr, 1))) return rc;
   H2B_CUDA(cudaMemset(op->d_arrived, 0, sizeof(unsigned long long) * T1));
-  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * T1));
+  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * 2 * T1));
   H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 

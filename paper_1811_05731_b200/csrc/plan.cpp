@@ -47,6 +47,7 @@ struct TaskTmp {
   int64_t data, out, bias;
   int32_t m, ld, ncols, kind, bias_nslots, bias_stride;
   int32_t stage;
+  int32_t qclass = 0;
   std::vector<int32_t> seg_idx;  // into seg tables
   std::vector<int32_t> deps;     // provisional ids
 };
@@ -82,7 +83,8 @@ class Builder {
   }
   // Packs the group's matrix, splits it into pieces, emits tasks.
   void emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
-                  Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split);
+                  Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split, int32_t qclass = 0,
+                  bool seg0_hi = false);
   void collect_leaves(int32_t c, std::vector<int32_t>* out) const {
     if (is_leaf(c)) { out->push_back(c); return; }
     collect_leaves((int32_t)d_->cl_child[2 * c], out);
@@ -182,7 +184,8 @@ int Builder::validate(std::string* err) {
 }
 
 void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
-                         Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split) {
+                         Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split, int32_t qclass,
+                         bool seg0_hi) {
   Plan& P = *plan_;
   if (m_total <= 0) return;
   // 1. pack the group matrix (m_total x C, column-major, ld = m_total)
@@ -206,7 +209,12 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
   std::vector<Piece> pieces;
   // Far-field items are latency-critical (the tree chain): small pieces, each
   // staged by one TMA bulk copy.  Near-field items are bandwidth work.
-  const int64_t cap = kind == kNear ? opt_.task_bytes : opt_.far_task_bytes;
+  // A heavy near-field row is cut into at most kMaxNearPieces items so that
+  // its final item sums a bounded number of partial slots.
+  const int64_t cap = kind == kNear
+                          ? std::max<int64_t>(opt_.task_bytes, (8 * (int64_t)m_total * C + kMaxNearPieces - 1) /
+                                                                   kMaxNearPieces)
+                          : opt_.far_task_bytes;
   const int64_t maxc = allow_split ? std::max<int64_t>(1, cap / (8 * (int64_t)m_total)) : INT64_MAX;
   Piece cur;
   int64_t col = 0;
@@ -270,6 +278,13 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       }
       t.seg_idx = seg_ids;
       t.deps = deps;
+      // scheduling class: the leaf-level coupling pieces without the parent
+      // transfer have slack (class 1); everything else is on or near the
+      // far-field critical chain (class 0)
+      t.qclass = qclass;
+      if (seg0_hi) {
+        for (auto& part : pc.parts) if (part[0] == 0) t.qclass = 0;
+      }
       if (outv) outv->producers.push_back((int32_t)tasks_.size());
       tasks_.push_back(std::move(t));
     }
@@ -349,7 +364,7 @@ int Builder::run(std::string* err) {
         int64_t ncol = size(s);
         segs.push_back({kSegX, d->cl_start[s], (int32_t)ncol, nullptr, d->nr_data[b] + br.second * ncol, true, ncol});
       }
-      emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true);
+      emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true, 1);
     }
   }
   // ---- coupling + downward pass, top-down (h2.py:211-235)
@@ -375,7 +390,8 @@ int Builder::run(std::string* err) {
         segs.push_back({kSegCoef, 0, (int32_t)ks, &xhat_[s], d->cp_data[b], true, ks});
       }
       if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
-      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true);
+      const bool transfer = t != 0 && yhat_[parent_[t]].exists();
+      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 1 : 0, transfer);
     }
   }
   // ---- leaf back-transform + near partials -> y (h2.py:227-229, 242-243)
@@ -437,13 +453,14 @@ int Builder::run(std::string* err) {
 
   P.t_data.resize(T); P.t_out.resize(T); P.t_bias.resize(T);
   P.t_m.resize(T); P.t_ld.resize(T); P.t_ncols.resize(T); P.t_kind.resize(T);
-  P.t_bias_nslots.resize(T); P.t_bias_stride.resize(T);
+  P.t_bias_nslots.resize(T); P.t_bias_stride.resize(T); P.t_qclass.resize(T);
   P.t_seg0.assign(T + 1, 0); P.t_dep0.assign(T + 1, 0);
   for (int32_t i = 0; i < T; ++i) {
     const TaskTmp& t = tasks_[q[i]];
     P.t_data[i] = t.data; P.t_out[i] = t.out; P.t_bias[i] = t.bias;
     P.t_m[i] = t.m; P.t_ld[i] = t.ld; P.t_ncols[i] = t.ncols; P.t_kind[i] = t.kind;
     P.t_bias_nslots[i] = t.bias_nslots; P.t_bias_stride[i] = t.bias_stride;
+    P.t_qclass[i] = t.qclass;
     for (int32_t si : t.seg_idx) {
       P.s_src.push_back(s_src_[si]); P.s_ncols.push_back(s_ncols_[si]); P.s_kind.push_back(s_kind_[si]);
       P.s_nslots.push_back(s_nslots_[si]); P.s_stride.push_back(s_stride_[si]);
@@ -467,15 +484,21 @@ int Builder::run(std::string* err) {
     for (int32_t i = 0; i < T; ++i)
       for (int32_t k = P.t_dep0[i]; k < P.t_dep0[i + 1]; ++k) P.succ[fill[P.deps[k]]++] = i;
   }
-  // initially ready items: up-leaf first (they start the far-field chain),
-  // then the near field, then anything else without dependencies
-  for (int pass = 0; pass < 3; ++pass)
-    for (int32_t i = 0; i < T; ++i) {
-      if (P.t_dep0[i + 1] != P.t_dep0[i]) continue;
-      const int32_t k = P.t_kind[i];
-      const int want = k == kUpLeaf ? 0 : (k == kNear ? 1 : 2);
-      if (want == pass) P.ready0.push_back(i);
-    }
+  // initially ready items: class 0 first (up-leaf: they start the far-field
+  // chain), then class 1 (the near field) longest first, so that heavy rows
+  // start early and the end of the launch is made of short items
+  for (int32_t i = 0; i < T; ++i)
+    if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] == 0) P.ready0.push_back(i);
+  P.n_ready0_hi = (int32_t)P.ready0.size();
+  {
+    std::vector<int32_t> lo;
+    for (int32_t i = 0; i < T; ++i)
+      if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] != 0) lo.push_back(i);
+    std::stable_sort(lo.begin(), lo.end(), [&](int32_t a, int32_t b) {
+      return (int64_t)P.t_m[a] * P.t_ncols[a] > (int64_t)P.t_m[b] * P.t_ncols[b];
+    });
+    P.ready0.insert(P.ready0.end(), lo.begin(), lo.end());
+  }
   P.local_bytes = P.stream_bytes;
   return H2B_OK;
 }

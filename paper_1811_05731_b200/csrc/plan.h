@@ -36,6 +36,7 @@ enum SegKind : int32_t {
 
 constexpr int kMaxRows = 64;  // rows per work item (lanes own rows l, l+32)
 constexpr int kMaxSegs = 32;  // source segments per work item (one per lane)
+constexpr int kMaxNearPieces = 32;  // near-field items per leaf row at most
 
 struct Plan {
   int64_t n = 0;
@@ -57,6 +58,8 @@ struct Plan {
   // issue order: the kernel's dynamic scheduler
   std::vector<int32_t> succ0, succ;
   std::vector<int32_t> ready0;
+  int32_t n_ready0_hi = 0;          // ready0[0:n_ready0_hi) are class 0
+  std::vector<int8_t> t_qclass;     // 0: critical chain, 1: slack (near field, leaf coupling)
 
   int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
   int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
