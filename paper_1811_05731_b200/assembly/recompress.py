@@ -7,9 +7,19 @@ relative truncated SVD (s > eps_rec * s[0]) gives the basis.  Leaves keep it
 explicitly, inner clusters only through the transfer matrices of their
 children (the basis is orthonormal and nested).  Coupling matrices are
 S_b = (V_t^T A_b)(B_b^T W_s) with the explicit bases.
+
+Parallelism (threads: the work is LAPACK/BLAS calls that release the GIL,
+one BLAS thread each): the per-block QR factors and products, the subtrees
+below a split depth, and the coupling products run concurrently.  The
+top-down inherited lists are built first and the subtrees' results are
+combined bottom-up with the serial code, so the result is identical to the
+serial recursion operation for operation.
 """
 
 from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -27,42 +37,76 @@ def _truncated_basis(z: np.ndarray, eps: float) -> np.ndarray:
     return u[:, : int(np.sum(s > eps * s[0]))]
 
 
-def basis_side(tree, anchored: dict, eps: float):
-    """One side of the nested basis.  ``anchored[cid]`` lists (factor,
-    weight) of the blocks whose cluster on this side is ``cid``."""
-    basis, transfer, explicit = {}, {}, {}
+class _Side:
+    def __init__(self, eps):
+        self.eps = eps
+        self.basis, self.transfer, self.explicit = {}, {}, {}
 
-    def visit(c, inherited):
-        mine = [(f @ w.T, c.start) for f, w in anchored.get(c.cid, ())]
-        current = inherited + mine
+    def combine(self, c, current, kids):
+        """Inner cluster: projection of the stacked restricted factors onto
+        the children's bases, truncated; children's transfers."""
         pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
-        if c.is_leaf:
-            v = _truncated_basis(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), eps)
-            basis[c.cid] = v
-            explicit[c.cid] = v
-            return v
-        kids = [visit(ch, current) for ch in c.children]
         if pieces:
             z = np.hstack(pieces)
             proj, off = [], 0
             for ch, v in zip(c.children, kids):
                 proj.append(v.T @ z[off: off + ch.size])
                 off += ch.size
-            vhat = _truncated_basis(np.vstack(proj), eps)
+            vhat = _truncated_basis(np.vstack(proj), self.eps)
         else:
             vhat = np.zeros((sum(v.shape[1] for v in kids), 0))
         parts, off = [], 0
         for ch, v in zip(c.children, kids):
             e = vhat[off: off + v.shape[1]]
-            transfer[ch.cid] = e
+            self.transfer[ch.cid] = e
             parts.append(v @ e)
             off += v.shape[1]
         full = np.vstack(parts)
-        explicit[c.cid] = full
+        self.explicit[c.cid] = full
         return full
 
-    visit(tree.root, [])
-    return basis, transfer, explicit
+    def visit(self, c, inherited, own):
+        current = inherited + own.get(c.cid, [])
+        if c.is_leaf:
+            pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
+            v = _truncated_basis(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), self.eps)
+            self.basis[c.cid] = v
+            self.explicit[c.cid] = v
+            return v
+        kids = [self.visit(ch, current, own) for ch in c.children]
+        return self.combine(c, current, kids)
+
+
+def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0):
+    """One side of the nested basis.  ``anchored[cid]`` lists (factor,
+    weight) of the blocks whose cluster on this side is ``cid``."""
+    side = _Side(eps)
+    items = [(cid, f, w) for cid, lst in anchored.items() for f, w in lst]
+    mats = list(pool.map(lambda t: t[1] @ t[2].T, items)) if pool else [f @ w.T for _, f, w in items]
+    own: dict = {}
+    for (cid, _, _), m in zip(items, mats):
+        own.setdefault(cid, []).append((m, tree.clusters[cid].start))
+    if pool is None or split_depth <= 0:
+        side.visit(tree.root, [], own)
+        return side.basis, side.transfer, side.explicit
+    # top-down: inherited lists down to the split depth
+    frontier, top = [(tree.root, [])], []
+    for _ in range(split_depth):
+        nxt = []
+        for c, inh in frontier:
+            if c.is_leaf:
+                nxt.append((c, inh))
+                continue
+            cur = inh + own.get(c.cid, [])
+            top.append((c, cur))
+            nxt.extend((ch, cur) for ch in c.children)
+        frontier = nxt
+    # subtrees in parallel (each writes its own clusters' entries)
+    list(pool.map(lambda ci: side.visit(ci[0], ci[1], own), frontier))
+    # bottom-up over the top part, children before parents
+    for c, cur in reversed(top):
+        side.combine(c, cur, [side.explicit[ch.cid] for ch in c.children])
+    return side.basis, side.transfer, side.explicit
 
 
 def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers: int = 1) -> H2Matrix:
@@ -70,21 +114,47 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
     block order; ``dense``: (row cid, col cid, matrix)."""
     if eps_rec < 0.0:
         raise ValueError("epsilon_rec must be >= 0")
-    rows: dict = {}
-    cols: dict = {}
-    for t, s, a, b in lowrank:
-        if a.shape[1] == 0:
-            continue
-        _, rb = np.linalg.qr(b)
-        _, ra = np.linalg.qr(a)
-        rows.setdefault(t, []).append((a, rb))
-        cols.setdefault(s, []).append((b, ra))
-    rbasis, rtrans, rexp = basis_side(tree, rows, eps_rec)
-    cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec)
-    op = H2Matrix(tree=tree, n=n, row_basis=rbasis, row_transfer=rtrans,
-                  col_basis=cbasis, col_transfer=ctrans)
-    for t, s, a, b in lowrank:
-        op.coupling.append((t, s, (rexp[t].T @ a) @ (b.T @ cexp[s])))
-    for t, s, m in dense:
-        op.near.append((t, s, m))
-    return op
+    pool = None
+    limiter = None
+    if workers > 1:
+        try:
+            from threadpoolctl import threadpool_limits
+            limiter = threadpool_limits(1)
+        except Exception:
+            limiter = None
+        pool = ThreadPoolExecutor(max_workers=workers)
+    try:
+        nz = [(t, s, a, b) for t, s, a, b in lowrank if a.shape[1] > 0]
+
+        def qr_r(t):
+            _, _, a, b = t
+            return np.linalg.qr(b)[1], np.linalg.qr(a)[1]
+
+        rs = list(pool.map(qr_r, nz)) if pool else [qr_r(t) for t in nz]
+        rows: dict = {}
+        cols: dict = {}
+        for (t, s, a, b), (rb, ra) in zip(nz, rs):
+            rows.setdefault(t, []).append((a, rb))
+            cols.setdefault(s, []).append((b, ra))
+        depth = max(1, int(np.ceil(np.log2(max(2, 4 * workers))))) if pool else 0
+        rbasis, rtrans, rexp = basis_side(tree, rows, eps_rec, pool, depth)
+        cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec, pool, depth)
+        op = H2Matrix(tree=tree, n=n, row_basis=rbasis, row_transfer=rtrans,
+                      col_basis=cbasis, col_transfer=ctrans)
+
+        def coupling(blk):
+            t, s, a, b = blk
+            return (t, s, (rexp[t].T @ a) @ (b.T @ cexp[s]))
+
+        op.coupling.extend(pool.map(coupling, lowrank) if pool else map(coupling, lowrank))
+        for t, s, m in dense:
+            op.near.append((t, s, m))
+        return op
+    finally:
+        if pool is not None:
+            pool.shutdown()
+        if limiter is not None:
+            try:
+                limiter.restore_original_limits()
+            except Exception:
+                pass

@@ -91,6 +91,7 @@ struct Ctl {
 struct KParams {
   const DTask* __restrict__ tasks;
   const DSeg* __restrict__ segs;
+  const DSeg* __restrict__ seg_inline;  // [ntasks * kInlineSegs]: segments of items with few of them
   const int32_t* __restrict__ succ0;    // [ntasks+1] successor CSR
   const int2* __restrict__ succ;         // (successor, its dependency count)
   const int32_t* __restrict__ ready0;   // initially ready items, issue order
@@ -111,6 +112,7 @@ struct KParams {
 };
 
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
+constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
 
 // Per-warp shared memory: the TMA-staged matrix of a far-field item,
@@ -209,8 +211,8 @@ __device__ __forceinline__ double ldA(const double* q) {
 // matrix: staged in shared memory by a TMA bulk copy that completes on `bar`
 // (SMEM), or streamed from global memory.
 template <int NRHS, bool SMEM>
-__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpSmem& w, int lane,
-                                         const double* A, uint64_t* bar, unsigned parity) {
+__device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                         int lane, const double* A, uint64_t* bar, unsigned parity) {
   constexpr int kCols = kChunkBytes / (8 * NRHS);
   constexpr int U = (NRHS == 1) ? 16 : 4;  // columns in flight per lane
   const int m = T.m, ld = T.ld;
@@ -220,7 +222,8 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, WarpS
     const int nseg = T.seg1 - T.seg0;  // <= kMaxSegs (planner)
     int nc = 0;
     if (lane < nseg) {
-      const DSeg S = p.segs[T.seg0 + lane];
+      // items with few segments carry them inline (fetched with the task)
+      const DSeg S = nseg <= kInlineSegs ? sin : p.segs[T.seg0 + lane];
       nc = S.ncols;
       w.seg_src[lane] = S.src;
       w.seg_kind[lane] = S.kind;
@@ -513,15 +516,17 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     }
     off = __shfl_sync(0xffffffffu, off, 0);
     const DTask T = p.tasks[item];
+    DSeg sin{0, 0, 0, 0, 0};
+    if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
     // successor list, fetched now so that its latency hides under the item
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
     int2 sd_first = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (off >= 0) {
-      run_item<NRHS, true>(p, T, w, lane, w.abuf + off, bar, phase);
+      run_item<NRHS, true>(p, T, sin, w, lane, w.abuf + off, bar, phase);
       phase ^= 1u;
     } else {
-      run_item<NRHS, false>(p, T, w, lane, p.mat + T.data, bar, phase);
+      run_item<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase);
     }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
@@ -605,6 +610,7 @@ struct h2b_op {
   double* d_coef = nullptr;
   DTask* d_tasks = nullptr;
   DSeg* d_segs = nullptr;
+  DSeg* d_seg_inline = nullptr;
   int32_t* d_succ0 = nullptr;
   int2* d_succ = nullptr;
   int32_t* d_ready0 = nullptr;
@@ -692,6 +698,7 @@ int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   KParams p;
   p.tasks = op->d_tasks;
   p.segs = op->d_segs;
+  p.seg_inline = op->d_seg_inline;
   p.succ0 = op->d_succ0;
   p.succ = op->d_succ;
   p.ready0 = op->d_ready0;
@@ -743,6 +750,7 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_coef);
   cudaFree(op->d_tasks);
   cudaFree(op->d_segs);
+  cudaFree(op->d_seg_inline);
   cudaFree(op->d_succ0);
   cudaFree(op->d_succ);
   cudaFree(op->d_ready0);
@@ -817,6 +825,15 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   P.mat.resize(P.mat.size() - 2);
   if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
   if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
+  {
+    std::vector<DSeg> inl((size_t)P.ntasks() * kInlineSegs, DSeg{0, 0, 0, 0, 0});
+    for (int64_t i = 0; i < P.ntasks(); ++i) {
+      const int32_t a = P.t_seg0[i], b = P.t_seg0[i + 1];
+      if (b - a <= kInlineSegs)
+        for (int32_t k = a; k < b; ++k) inl[(size_t)i * kInlineSegs + (k - a)] = segs[k];
+    }
+    if ((rc = upload(&op->d_seg_inline, inl.data(), inl.size()))) return rc;
+  }
   if ((rc = upload(&op->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
   {
     std::vector<int2> sd(P.succ.size());
