@@ -155,8 +155,9 @@ int64_t h2b_stream_bytes(const h2b_op* op);
 int h2b_stats_get(const h2b_op* op, h2b_stats* out);
 void h2b_destroy(h2b_op* op);
 
-/* Diagnostics: per-work-item timeline of the next products ({start ns,
- * end ns, (smid << 32) | warp, continuation+1}, globaltimer) and item kinds. */
+/* Diagnostics: per-work-item timeline of the next products, 8 words per item
+ * ({start, end, (smid << 32) | warp, continuation+1, compute done, fence
+ * done, 0, 0}, globaltimer ns) and item kinds. */
 int h2b_trace_enable(h2b_op* op, int on);
 int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems);
 int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems);

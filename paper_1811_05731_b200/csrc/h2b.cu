@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     // successor.  Of the successors whose count this warp completes, it runs
     // the first one itself next and pushes the others.
     __syncwarp();
+    unsigned long long t_run = 0, t_fence = 0;
+    if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_run));
     fence_acq_rel();
+    if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fence));
     cont = -1;
     for (int k0 = s0; k0 < s1; k0 += 32) {
       const int k = k0 + lane;
@@ -563,10 +566,13 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&smid));
       smid &= 0xffffffffull;
-      p.trace[4 * item] = t_start;
-      p.trace[4 * item + 1] = t_end;
-      p.trace[4 * item + 2] = (smid << 32) | (unsigned)(blockIdx.x * nw + wib);
-      p.trace[4 * item + 3] = (unsigned long long)(cont >= 0 ? cont + 1 : 0);
+      unsigned long long* tr = p.trace + 8 * (int64_t)item;
+      tr[0] = t_start;
+      tr[1] = t_end;
+      tr[2] = (smid << 32) | (unsigned)(blockIdx.x * nw + wib);
+      tr[3] = (unsigned long long)(cont >= 0 ? cont + 1 : 0);
+      tr[4] = t_run;
+      tr[5] = t_fence;
     }
     if (cont >= 0) {
       fence_acq_rel();  // acquire side of the other predecessors' releases
@@ -992,8 +998,8 @@ int h2b_trace_enable(h2b_op* op, int on) {
   if (!op) return fail(H2B_EINVAL, "null operator");
   H2B_CUDA(cudaSetDevice(op->device));
   if (on && !op->d_trace) {
-    H2B_CUDA(cudaMalloc(&op->d_trace, sizeof(unsigned long long) * 4 * std::max<int64_t>(1, op->ntasks)));
-    H2B_CUDA(cudaMemset(op->d_trace, 0, sizeof(unsigned long long) * 4 * std::max<int64_t>(1, op->ntasks)));
+    H2B_CUDA(cudaMalloc(&op->d_trace, sizeof(unsigned long long) * 8 * std::max<int64_t>(1, op->ntasks)));
+    H2B_CUDA(cudaMemset(op->d_trace, 0, sizeof(unsigned long long) * 8 * std::max<int64_t>(1, op->ntasks)));
   } else if (!on && op->d_trace) {
     cudaFree(op->d_trace);
     op->d_trace = nullptr;
@@ -1003,7 +1009,7 @@ int h2b_trace_enable(h2b_op* op, int on) {
 
 int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems) {
   if (!op || !out || nitems != op->ntasks || !op->d_trace) return fail(H2B_EINVAL, "trace not enabled or wrong size");
-  H2B_CUDA(cudaMemcpy(out, op->d_trace, sizeof(uint64_t) * 4 * nitems, cudaMemcpyDeviceToHost));
+  H2B_CUDA(cudaMemcpy(out, op->d_trace, sizeof(uint64_t) * 8 * nitems, cudaMemcpyDeviceToHost));
   return H2B_OK;
 }
 
