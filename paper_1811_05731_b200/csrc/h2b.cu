@@ -194,10 +194,21 @@ __device__ __forceinline__ double gather_one(const KParams& p, const WarpSmem& w
   while (w.seg_off[k + 1] <= c) ++k;
   const int cs = c - w.seg_off[k];
   if (w.seg_kind[k] == h2b::kSegX) return __ldg(p.xp + (w.seg_src[k] + cs) * NRHS + r);
-  const int64_t base = w.seg_src[k] + cs;
+  const double* q = p.coef + (w.seg_src[k] + cs) * NRHS + r;
+  const int64_t st = (int64_t)w.seg_stride[k] * NRHS;
+  const int ns = w.seg_nslots[k];
+  // partial slots of a split producer, added in slot order; eight loads in
+  // flight at a time (split rows of upper clusters have dozens of slots)
   double v = 0.0;
-  for (int s = 0; s < w.seg_nslots[k]; ++s)
-    v += __ldcg(p.coef + (base + (int64_t)s * w.seg_stride[k]) * NRHS + r);
+  int s = 0;
+  for (; s + 8 <= ns; s += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = __ldcg(q + (int64_t)(s + u) * st);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += t[u];
+  }
+  for (; s < ns; ++s) v += __ldcg(q + (int64_t)s * st);
   return v;
 }
 
@@ -554,11 +565,23 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         if (lane == first) d = -1;
         ready &= ready - 1;
       }
-      if (d >= 0) {
-        fence_acq_rel();
-        const unsigned slot = (unsigned)dq * (unsigned)p.ntasks + atomicAdd(dq ? &ctl->lo_tail : &ctl->ready_tail, 1u);
-        p.ready_q[slot] = d;
-        st_release(p.ready_flag + slot, e1);
+      if (ready) {
+        // push the rest: one tail atomic per queue per warp (the tails are
+        // the hottest lines of the scheduler)
+        fence_acq_rel();  // acquire side of the other predecessors' releases
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const unsigned mine = __ballot_sync(0xffffffffu, d >= 0 && dq == q);
+          if (!mine) continue;
+          unsigned base = 0;
+          if (lane == __ffs(mine) - 1) base = atomicAdd(q ? &ctl->lo_tail : &ctl->ready_tail, (unsigned)__popc(mine));
+          base = __shfl_sync(0xffffffffu, base, __ffs(mine) - 1);
+          if (d >= 0 && dq == q) {
+            const unsigned slot = (unsigned)q * (unsigned)p.ntasks + base + __popc(mine & ((1u << lane) - 1u));
+            p.ready_q[slot] = d;
+            st_release(p.ready_flag + slot, e1);
+          }
+        }
       }
     }
     if (p.trace && lane == 0) {
