@@ -433,18 +433,19 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
   const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
-  bool static_done = false;  // lane-0 state
+  bool static_done = false;  // lane-0 state below
+  bool static_lo = false;    // static claims have reached the class-1 (near) part
   int owed = -1;             // claimed dynamic slot whose push is still in flight
+  int pend = -1;             // near item claimed ahead (slack work, no priority cost)
   int cont = -1;             // continuation (all lanes)
   for (;;) {
     int item = cont;
     if (lane == 0 && item < 0) {
-      // claim from dynamic queue q (0: critical chain, 1: slack); returns the
-      // item, or -1 with `owed` set when the claimed slot is still in flight
+      // claim from dynamic queue q (0: critical chain, 1: slack) given the
+      // probed head/tail; returns the item, or -1 (with `owed` set when the
+      // claimed slot is still in flight)
       auto claim = [&](int q) -> int {
         unsigned* head = q ? &ctl->lo_head : &ctl->ready_head;
-        unsigned* tail = q ? &ctl->lo_tail : &ctl->ready_tail;
-        if (ld_relaxed(head) >= ld_relaxed(tail)) return -1;
         // one atomicAdd per claim (CAS retry loops serialise contending warps)
         const unsigned slot = atomicAdd(head, 1u);
         if (slot >= n_dynamic) return -1;
@@ -461,8 +462,20 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         owed = (int)abs;
         return -1;
       };
+      auto take_static = [&]() -> int {
+        const unsigned s = atomicAdd(&ctl->static_head, 1u);
+        if (s >= (unsigned)p.nready0) {
+          static_done = true;
+          return -1;
+        }
+        if (s >= (unsigned)p.nready0_hi) static_lo = true;
+        return __ldg(p.ready0 + s);
+      };
       unsigned backoff = 64;
       for (;;) {
+        // probe both queues in one round trip
+        const unsigned h0 = ld_relaxed(&ctl->ready_head), t0 = ld_relaxed(&ctl->ready_tail);
+        const unsigned h1 = ld_relaxed(&ctl->lo_head), t1 = ld_relaxed(&ctl->lo_tail);
         if (owed >= 0) {
           if (ld_relaxed(p.ready_flag + owed) == e1) {
             ld_acquire(p.ready_flag + owed);
@@ -471,27 +484,22 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
             atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
-        } else if ((item = claim(0)) >= 0) {
+        } else if (h0 < t0 && (item = claim(0)) >= 0) {
           break;
         }
         // class-0 static items (up-leaf) before any slack work
-        if (!static_done && ld_relaxed(&ctl->static_head) < (unsigned)p.nready0_hi) {
-          const unsigned s = atomicAdd(&ctl->static_head, 1u);
-          if (s < (unsigned)p.nready0) {
-            item = __ldg(p.ready0 + s);
-            break;
-          }
-          static_done = true;
+        if (!static_done && !static_lo && (item = take_static()) >= 0) {
+          if (!static_lo) break;
+          pend = item;  // already class 1: keep it for after the slack queue
+          item = -1;
         }
-        if (owed < 0 && (item = claim(1)) >= 0) break;
-        if (!static_done) {
-          const unsigned s = atomicAdd(&ctl->static_head, 1u);
-          if (s < (unsigned)p.nready0) {
-            item = __ldg(p.ready0 + s);
-            break;
-          }
-          static_done = true;
+        if (owed < 0 && h1 < t1 && (item = claim(1)) >= 0) break;
+        if (pend >= 0) {
+          item = pend;
+          pend = -1;
+          break;
         }
+        if (!static_done && (item = take_static()) >= 0) break;
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
         if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
@@ -504,6 +512,11 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         backoff = min(backoff * 2u, 1024u);
       }
     }
+    // claim the next near item ahead, so that the next decision costs no
+    // atomic round trip (its result is read after this item)
+    unsigned ahead = 0xffffffffu;
+    if (lane == 0 && item >= 0 && pend < 0 && static_lo && !static_done)
+      ahead = atomicAdd(&ctl->static_head, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
     unsigned long long t_start = 0;
@@ -583,6 +596,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           }
         }
       }
+    }
+    if (lane == 0 && ahead != 0xffffffffu) {
+      if (ahead < (unsigned)p.nready0) pend = __ldg(p.ready0 + ahead);
+      else static_done = true;
     }
     if (p.trace && lane == 0) {
       unsigned long long t_end, smid;
