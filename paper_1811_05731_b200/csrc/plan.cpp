@@ -211,17 +211,22 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
   // staged by one TMA bulk copy.  Near-field items are bandwidth work.
   // A heavy near-field row is cut into at most kMaxNearPieces items so that
   // its final item sums a bounded number of partial slots.
-  const int64_t cap = kind == kNear
-                          ? std::max<int64_t>(opt_.task_bytes, (8 * (int64_t)m_total * C + kMaxNearPieces - 1) /
-                                                                   kMaxNearPieces)
-                          : opt_.far_task_bytes;
+  // In a downward item the parent transfer (segment 0, seg0_hi) is the link
+  // of the far-field chain: it gets a small piece of its own; the coupling
+  // blocks after it are slack and streamed in large pieces.
+  const bool bulk = kind == kNear || kind == kDown;
+  const int64_t big = kind == kNear ? std::max<int64_t>(opt_.task_bytes, (8 * (int64_t)m_total * C + kMaxNearPieces - 1) /
+                                                                             kMaxNearPieces)
+                                    : opt_.task_bytes;
+  const int64_t cap = bulk ? big : opt_.far_task_bytes;
   const int64_t maxc = allow_split ? std::max<int64_t>(1, cap / (8 * (int64_t)m_total)) : INT64_MAX;
   Piece cur;
   int64_t col = 0;
   for (int64_t si = 0; si < (int64_t)segs.size(); ++si) {
     int64_t nc = segs[si].ncols, c0 = 0;
     if (nc == 0) continue;
-    if (cur.ncols > 0 && (cur.ncols + nc > maxc || (int)cur.parts.size() >= kMaxSegs)) {
+    const bool alone = seg0_hi && (si == 1);  // close the transfer-only piece
+    if (cur.ncols > 0 && (alone || cur.ncols + nc > maxc || (int)cur.parts.size() >= kMaxSegs)) {
       pieces.push_back(cur); cur = Piece(); cur.col0 = col;
     }
     while (nc - c0 > 0) {
@@ -278,9 +283,9 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       }
       t.seg_idx = seg_ids;
       t.deps = deps;
-      // scheduling class: the leaf-level coupling pieces without the parent
-      // transfer have slack (class 1); everything else is on or near the
-      // far-field critical chain (class 0)
+      // scheduling class: coupling pieces without the parent transfer have
+      // slack (class 1); the transfer pieces, the upward pass and the finals
+      // form the far-field critical chain (class 0)
       t.qclass = qclass;
       if (seg0_hi) {
         for (auto& part : pc.parts) if (part[0] == 0) t.qclass = 0;
@@ -391,7 +396,7 @@ int Builder::run(std::string* err) {
       }
       if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
       const bool transfer = t != 0 && yhat_[parent_[t]].exists();
-      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 1 : 0, transfer);
+      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, 1, transfer);
     }
   }
   // ---- leaf back-transform + near partials -> y (h2.py:227-229, 242-243)
