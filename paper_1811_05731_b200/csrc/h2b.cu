@@ -493,12 +493,14 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           pend = item;  // already class 1: keep it for after the slack queue
           item = -1;
         }
-        if (owed < 0 && h1 < t1 && (item = claim(1)) >= 0) break;
+        // the near item claimed ahead comes before the slack queue: near
+        // items are issued longest first, and a long one must not wait
         if (pend >= 0) {
           item = pend;
           pend = -1;
           break;
         }
+        if (owed < 0 && h1 < t1 && (item = claim(1)) >= 0) break;
         if (!static_done && (item = take_static()) >= 0) break;
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
