@@ -70,15 +70,14 @@ static_assert(sizeof(DSeg) == 24, "DSeg layout");
 // Scheduler state (one per operator).  Every counter is reset by the last
 // warp to leave a launch and `epoch` counts launches, so nothing is cleared
 // between products.  Each hot counter sits on its own 128-byte line.
+constexpr int kQueues = 3;  // 0: far-field chain, 1: upper coupling, 2: leaf coupling
+struct Line {
+  unsigned v;
+  unsigned pad[31];
+};
 struct Ctl {
-  unsigned ready_head;   // class-0 dynamic queue: next slot to claim
-  unsigned pad0[31];
-  unsigned ready_tail;   // class-0 dynamic queue: next slot to push
-  unsigned pad1[31];
-  unsigned lo_head;      // class-1 dynamic queue (slack work)
-  unsigned pad5[31];
-  unsigned lo_tail;
-  unsigned pad6[31];
+  Line head[kQueues];    // dynamic queue q: next slot to claim
+  Line tail[kQueues];    // dynamic queue q: next slot to push
   unsigned static_head;  // next initially-ready item to claim
   unsigned pad2[31];
   unsigned dyn_started;  // dynamic items taken (queue or continuation)
@@ -445,7 +444,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       // probed head/tail; returns the item, or -1 (with `owed` set when the
       // claimed slot is still in flight)
       auto claim = [&](int q) -> int {
-        unsigned* head = q ? &ctl->lo_head : &ctl->ready_head;
+        unsigned* head = &ctl->head[q].v;
         // one atomicAdd per claim (CAS retry loops serialise contending warps)
         const unsigned slot = atomicAdd(head, 1u);
         if (slot >= n_dynamic) return -1;
@@ -474,8 +473,12 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       unsigned backoff = 64;
       for (;;) {
         // probe both queues in one round trip
-        const unsigned h0 = ld_relaxed(&ctl->ready_head), t0 = ld_relaxed(&ctl->ready_tail);
-        const unsigned h1 = ld_relaxed(&ctl->lo_head), t1 = ld_relaxed(&ctl->lo_tail);
+        unsigned h[kQueues], t[kQueues];
+#pragma unroll
+        for (int q = 0; q < kQueues; ++q) {
+          h[q] = ld_relaxed(&ctl->head[q].v);
+          t[q] = ld_relaxed(&ctl->tail[q].v);
+        }
         if (owed >= 0) {
           if (ld_relaxed(p.ready_flag + owed) == e1) {
             ld_acquire(p.ready_flag + owed);
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
             atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
-        } else if (h0 < t0 && (item = claim(0)) >= 0) {
+        } else if (h[0] < t[0] && (item = claim(0)) >= 0) {
           break;
         }
         // class-0 static items (up-leaf) before any slack work
@@ -500,7 +503,9 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           pend = -1;
           break;
         }
-        if (owed < 0 && h1 < t1 && (item = claim(1)) >= 0) break;
+        // coupling rows of inner clusters: the chain needs them level by level
+        if (owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
+        if (owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) break;
         if (!static_done && (item = take_static()) >= 0) break;
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
@@ -563,38 +568,49 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     fence_acq_rel();
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fence));
     cont = -1;
-    for (int k0 = s0; k0 < s1; k0 += 32) {
-      const int k = k0 + lane;
-      int d = -1, dq = 0;
-      if (k < s1) {
-        // (successor, its dependency count)
-        const int2 sd = k0 == s0 ? sd_first : __ldg(p.succ + k);
-        const unsigned ndep = (unsigned)sd.y & 0xffffffu;
-        if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) d = sd.x;
-        dq = sd.y >> 24;
-      }
-      unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
-      if (cont < 0 && ready) {
-        const int first = __ffs(ready) - 1;
-        cont = __shfl_sync(0xffffffffu, d, first);
-        if (lane == first) d = -1;
-        ready &= ready - 1;
-      }
-      if (ready) {
-        // push the rest: one tail atomic per queue per warp (the tails are
-        // the hottest lines of the scheduler)
-        fence_acq_rel();  // acquire side of the other predecessors' releases
+    for (int k0 = s0; k0 < s1; k0 += 128) {
+      // arrival counts of up to 4 x 32 successors in flight at once
+      int dd[4], qq[4];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const unsigned mine = __ballot_sync(0xffffffffu, d >= 0 && dq == q);
-          if (!mine) continue;
-          unsigned base = 0;
-          if (lane == __ffs(mine) - 1) base = atomicAdd(q ? &ctl->lo_tail : &ctl->ready_tail, (unsigned)__popc(mine));
-          base = __shfl_sync(0xffffffffu, base, __ffs(mine) - 1);
-          if (d >= 0 && dq == q) {
-            const unsigned slot = (unsigned)q * (unsigned)p.ntasks + base + __popc(mine & ((1u << lane) - 1u));
-            p.ready_q[slot] = d;
-            st_release(p.ready_flag + slot, e1);
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 32 * u + lane;
+        dd[u] = -1;
+        qq[u] = 0;
+        if (k < s1) {
+          const int2 sd = (k0 == s0 && u == 0) ? sd_first : __ldg(p.succ + k);
+          const unsigned ndep = (unsigned)sd.y & 0xffffffu;
+          if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
+          qq[u] = sd.y >> 24;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int d = dd[u];
+        const int dq = qq[u];
+        unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
+        // of the successors this warp completes, run the first (chain class
+        // first) itself next and push the others
+        if (cont < 0 && ready) {
+          const unsigned chain = __ballot_sync(0xffffffffu, d >= 0 && dq == 0);
+          const int first = __ffs(chain ? chain : ready) - 1;
+          cont = __shfl_sync(0xffffffffu, d, first);
+          if (lane == first) d = -1;
+          ready = __ballot_sync(0xffffffffu, d >= 0);
+        }
+        if (ready) {
+          fence_acq_rel();  // acquire side of the other predecessors' releases
+#pragma unroll
+          for (int q = 0; q < kQueues; ++q) {
+            const unsigned mine = __ballot_sync(0xffffffffu, d >= 0 && dq == q);
+            if (!mine) continue;
+            unsigned base = 0;
+            if (lane == __ffs(mine) - 1) base = atomicAdd(&ctl->tail[q].v, (unsigned)__popc(mine));
+            base = __shfl_sync(0xffffffffu, base, __ffs(mine) - 1);
+            if (d >= 0 && dq == q) {
+              const unsigned slot = (unsigned)q * (unsigned)p.ntasks + base + __popc(mine & ((1u << lane) - 1u));
+              p.ready_q[slot] = d;
+              st_release(p.ready_flag + slot, e1);
+            }
           }
         }
       }
@@ -627,10 +643,8 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     fence_acq_rel();
     if (atomicAdd(&ctl->exited, 1u) == total - 1) {
       // every warp has left the loop: reset the counters for the next launch
-      ctl->ready_head = 0;
-      ctl->ready_tail = 0;
-      ctl->lo_head = 0;
-      ctl->lo_tail = 0;
+#pragma unroll
+      for (int q = 0; q < kQueues; ++q) ctl->head[q].v = ctl->tail[q].v = 0;
       ctl->static_head = 0;
       ctl->dyn_started = 0;
       ctl->exited = 0;
@@ -887,7 +901,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     std::vector<int2> sd(P.succ.size());
     for (size_t k = 0; k < sd.size(); ++k) {
       const int32_t d = P.succ[k];
-      // low 24 bits: dependency count; bit 24: the successor's queue class
+      // low 24 bits: dependency count; bits 24+: the successor's queue class
       sd[k] = make_int2(d, (P.t_dep0[d + 1] - P.t_dep0[d]) | ((int)P.t_qclass[d] << 24));
     }
     if ((rc = upload(&op->d_succ, sd.data(), sd.size()))) return rc;
@@ -900,11 +914,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
   if ((rc = upload<unsigned long long>(&op->d_arrived, nullptr, T1))) return rc;
-  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, 2 * T1))) return rc;   // two classes
-  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, 2 * T1))) return rc;
+  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, kQueues * T1))) return rc;
+  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, kQueues * T1))) return rc;
   if ((rc = upload<Ctl>(&op->d_ctl, nullptr, 1))) return rc;
   H2B_CUDA(cudaMemset(op->d_arrived, 0, sizeof(unsigned long long) * T1));
-  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * 2 * T1));
+  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));
   H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 

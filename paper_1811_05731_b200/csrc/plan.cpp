@@ -283,9 +283,10 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       }
       t.seg_idx = seg_ids;
       t.deps = deps;
-      // scheduling class: coupling pieces without the parent transfer have
-      // slack (class 1); the transfer pieces, the upward pass and the finals
-      // form the far-field critical chain (class 0)
+      // scheduling class: the transfer pieces, the upward pass and the finals
+      // form the far-field critical chain (class 0); coupling pieces of inner
+      // clusters are needed as the chain descends (class 1); coupling pieces
+      // of leaves and the near field only by the finals (class 2)
       t.qclass = qclass;
       if (seg0_hi) {
         for (auto& part : pc.parts) if (part[0] == 0) t.qclass = 0;
@@ -369,7 +370,7 @@ int Builder::run(std::string* err) {
         int64_t ncol = size(s);
         segs.push_back({kSegX, d->cl_start[s], (int32_t)ncol, nullptr, d->nr_data[b] + br.second * ncol, true, ncol});
       }
-      emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true, 1);
+      emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true, 2);
     }
   }
   // ---- coupling + downward pass, top-down (h2.py:211-235)
@@ -396,7 +397,7 @@ int Builder::run(std::string* err) {
       }
       if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
       const bool transfer = t != 0 && yhat_[parent_[t]].exists();
-      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, 1, transfer);
+      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 2 : 1, transfer);
     }
   }
   // ---- leaf back-transform + near partials -> y (h2.py:227-229, 242-243)
@@ -498,7 +499,7 @@ int Builder::run(std::string* err) {
   {
     std::vector<int32_t> lo;
     for (int32_t i = 0; i < T; ++i)
-      if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] != 0) lo.push_back(i);
+      if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] != 0) lo.push_back(i);  // near field
     std::stable_sort(lo.begin(), lo.end(), [&](int32_t a, int32_t b) {
       return (int64_t)P.t_m[a] * P.t_ncols[a] > (int64_t)P.t_m[b] * P.t_ncols[b];
     });
