@@ -583,36 +583,52 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           qq[u] = sd.y >> 24;
         }
       }
+      // of the successors this warp completed, run one itself next (chain
+      // class first) and push the others: one fence, one tail atomic per queue
+      unsigned any = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int d = dd[u];
-        const int dq = qq[u];
-        unsigned ready = __ballot_sync(0xffffffffu, d >= 0);
-        // of the successors this warp completes, run the first (chain class
-        // first) itself next and push the others
-        if (cont < 0 && ready) {
-          const unsigned chain = __ballot_sync(0xffffffffu, d >= 0 && dq == 0);
-          const int first = __ffs(chain ? chain : ready) - 1;
-          cont = __shfl_sync(0xffffffffu, d, first);
-          if (lane == first) d = -1;
-          ready = __ballot_sync(0xffffffffu, d >= 0);
-        }
-        if (ready) {
-          fence_acq_rel();  // acquire side of the other predecessors' releases
+      for (int u = 0; u < 4; ++u) any |= __ballot_sync(0xffffffffu, dd[u] >= 0);
+      if (!any) continue;
+      if (cont < 0) {
 #pragma unroll
-          for (int q = 0; q < kQueues; ++q) {
-            const unsigned mine = __ballot_sync(0xffffffffu, d >= 0 && dq == q);
-            if (!mine) continue;
-            unsigned base = 0;
-            if (lane == __ffs(mine) - 1) base = atomicAdd(&ctl->tail[q].v, (unsigned)__popc(mine));
-            base = __shfl_sync(0xffffffffu, base, __ffs(mine) - 1);
-            if (d >= 0 && dq == q) {
-              const unsigned slot = (unsigned)q * (unsigned)p.ntasks + base + __popc(mine & ((1u << lane) - 1u));
-              p.ready_q[slot] = d;
-              st_release(p.ready_flag + slot, e1);
+        for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned cand = __ballot_sync(0xffffffffu, dd[u] >= 0 && (pass == 1 || qq[u] == 0));
+            if (cont < 0 && cand) {
+              const int first = __ffs(cand) - 1;
+              cont = __shfl_sync(0xffffffffu, dd[u], first);
+              if (lane == first) dd[u] = -1;
             }
           }
+      }
+      unsigned cnt[kQueues], mask[4][kQueues];
+#pragma unroll
+      for (int q = 0; q < kQueues; ++q) cnt[q] = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < kQueues; ++q) {
+          mask[u][q] = __ballot_sync(0xffffffffu, dd[u] >= 0 && qq[u] == q);
+          cnt[q] += __popc(mask[u][q]);
         }
+      if (cnt[0] + cnt[1] + cnt[2] == 0) continue;
+      fence_acq_rel();  // acquire side of the other predecessors' releases
+      unsigned base = 0;
+      if (lane < kQueues && cnt[lane] > 0) base = atomicAdd(&ctl->tail[lane].v, cnt[lane]);
+      unsigned b[kQueues];
+#pragma unroll
+      for (int q = 0; q < kQueues; ++q) b[q] = __shfl_sync(0xffffffffu, base, q);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (dd[u] >= 0) {
+          const int q = qq[u];
+          const unsigned slot = (unsigned)q * (unsigned)p.ntasks + b[q] + __popc(mask[u][q] & ((1u << lane) - 1u));
+          p.ready_q[slot] = dd[u];
+          st_release(p.ready_flag + slot, e1);
+        }
+#pragma unroll
+        for (int q = 0; q < kQueues; ++q) b[q] += __popc(mask[u][q]);
       }
     }
     if (lane == 0 && ahead != 0xffffffffu) {
