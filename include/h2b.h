@@ -77,7 +77,7 @@ typedef struct h2b_desc {
 
 /* Execution-plan knobs.  Zero-initialise for defaults. */
 typedef struct h2b_options {
-  int64_t task_bytes;   /* max bytes per near-field work item (def. 16384)   */
+  int64_t task_bytes;   /* max bytes per near-field work item (def. 65536)   */
   int64_t far_task_bytes; /* max bytes per far-field item (default 4096): each
                              is staged to shared memory by one TMA bulk copy */
   int32_t warps_per_cta;/* persistent CTA width in warps (default 10, <= 16) */

@@ -71,7 +71,7 @@ struct Plan {
 };
 
 struct PlanOptions {
-  int64_t task_bytes = 16384;     // near-field items
+  int64_t task_bytes = 65536;     // near-field items (and leaf coupling rows)
   int64_t far_task_bytes = 4096;  // up-leaf, up-node and down items
   bool interleave = true;
   int32_t rank = 0;

@@ -28,9 +28,10 @@ WORKLOADS = {
     "config2": dict(desc="cube [-1,1]^3, 130x130 quads/face, 2 tri/quad (N=101402), leaf 64, eta 2, order 5",
                     surface=lambda: G.cube_surface(130),
                     cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
-    "config3": dict(desc="thin disk r=1 t=0.05, jittered Delaunay faces + structured rim (N~1.0M), "
+    # h = 0.00252 gives N = 1 040 147 <= 2^14 * 64: leaves of 32-64 nodes, depth 14
+    "config3": dict(desc="thin disk r=1 t=0.05, jittered Delaunay faces + structured rim (N=1040147), "
                          "leaf 64, eta 2, order 5",
-                    surface=lambda: G.disk_surface(0.0025),
+                    surface=lambda: G.disk_surface(0.00252),
                     cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
     "config5": dict(desc="icosphere level 10 decimated to 4194304 nodes, convex-hull re-triangulated, "
                          "leaf 64, eta 2, order 5",
