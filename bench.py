@@ -299,7 +299,7 @@ def run_b200(args):
                              "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic,
                              "peak_kind": peak_kind,
                              "algorithmic_bytes_per_launch": b_alg},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps, "clocks": clocks,
                 "parity_rel_err_vs_oracle": parity}
         print(json.dumps(line), flush=True)
     if ws > 1:
