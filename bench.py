@@ -8,9 +8,11 @@ A step is one H² product y = M x of the workload (default: BASELINE config 2,
 the 101 402-node cube, leaf 64, eta 2, order 5) with x already resident in
 HBM.  The operator is built on the box by the restated builder
 (paper_1811_05731_b200/assembly) before timing.  Rank 0 prints ONE JSON
-line.  Under torchrun (N > 1) every rank runs an independent replica of the
-product on its own GPU (weak scaling of throughput; the sharded product is
-DESIGN.md §7's next step) and the step time is the max over ranks.
+line.  Under torchrun (N > 1) the product is sharded over the GPUs
+(byte-balanced leaf ranges, the upward coefficients
+all-gathered over NCCL between the two phases of every rank): a step is one
+product of the whole operator, its time the max over ranks (strong
+scaling).
 
 ``--impl reference`` times the CPU restatement of the reference matvec
 (oracle/h2_matvec_ref.py, the "port": a Python loop over small numpy GEMVs,
@@ -128,7 +130,7 @@ def _build(args, rank, ws, log):
 def _config_block(args, n, op_bytes, extra=None):
     from paper_1811_05731_b200.workloads import WORKLOADS
     c = {"workload": f"{args.config}: {WORKLOADS[args.config]['desc']}", "n": n, "nrhs": args.nrhs,
-         "h2_bytes": op_bytes, "parallelism": f"replicas{args.world}" if args.world > 1 else "single",
+         "h2_bytes": op_bytes, "parallelism": f"shard{args.world}" if args.world > 1 else "single",
          "l2": "operator streamed per step is larger than the 126 MB L2 (no flush needed)"
          if op_bytes > 126e6 else "operator fits in L2 (latency-bound config)"}
     if extra:
@@ -212,23 +214,27 @@ def run_b200(args):
     torch.cuda.set_device(local)
     log = (lambda m: print(m, file=sys.stderr, flush=True)) if rank == 0 else (lambda m: None)
     op, info = _build(args, rank, ws, log)
-    from paper_1811_05731_b200.h2 import DeviceOperator, h2_matvec, h2_matmat
-    dev = DeviceOperator(op)
+    from paper_1811_05731_b200.h2 import DeviceOperator, h2_matvec, h2_matmat, nccl_unique_id
+    if ws > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        dev = DeviceOperator(op, rank=rank, world_size=ws, nccl_unique_id=obj[0])
+    else:
+        dev = DeviceOperator(op)
     st = dev.stats()
     n, nrhs = op.n, args.nrhs
     from paper_1811_05731_b200.workloads import vector_for
-    xh = vector_for(args.config, n, nrhs, seed=1234 + rank)
+    xh = vector_for(args.config, n, nrhs, seed=1234)
     x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     # parity spot-check of this very operator against the oracle (rank 0)
     parity = None
+    if not args.profile:
+        yg = dev.matvec(xh)   # full y on every rank (multi-GPU: rows assembled over NCCL)
     if rank == 0 and not args.profile:
         from oracle.h2_matvec_ref import h2_matvec_ref
-        dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, sp)
-        stream.synchronize()
-        yg = y.cpu().numpy()
         x0 = xh if nrhs == 1 else xh[:, 0]
         y0 = yg if nrhs == 1 else yg[:, 0]
         yr = h2_matvec_ref(op, x0)
@@ -256,14 +262,17 @@ def run_b200(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     clocks = clk.summary(peaks.get("sm_max_mhz"))
-    value = ws * n * nrhs / (ms * 1e-3)
+    value = n * nrhs / (ms * 1e-3)          # one product of the whole operator per step
     b_alg = st["stream_bytes"] + 16 * n * nrhs
-    achieved = b_alg / (ms * 1e-3) / 1e9
+    achieved = b_alg / (ms * 1e-3) / 1e9   # aggregate over the GPUs
     # end to end through the public API with host buffers (pinned), rank-local
     e2e = None
     if not args.profile:
         xp = torch.from_numpy(np.ascontiguousarray(xh)).pin_memory().numpy()
-        call = (lambda: h2_matvec(op, xp)) if nrhs == 1 else (lambda: h2_matmat(op, xp))
+        if ws > 1:
+            call = lambda: dev.matvec(xp)    # the rank operator's host entry point
+        else:
+            call = (lambda: h2_matvec(op, xp)) if nrhs == 1 else (lambda: h2_matmat(op, xp))
         for _ in range(3):
             call()
         k = max(5, min(args.steps, 200))
@@ -275,7 +284,7 @@ def run_b200(args):
             t = torch.tensor([te], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": ws * n * nrhs / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n * nrhs,
+        e2e = {"value": n * nrhs / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n * nrhs,
                "d2h_bytes_per_step": 8 * n * nrhs, "ms_per_step": te * 1e3, "steps": k}
     cpu = None
     if rank == 0 and ws == 1 and not args.profile and not args.no_cpu_baseline:
@@ -287,7 +296,8 @@ def run_b200(args):
                          f"{dt * 1e3:.1f} ms per product"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if ws > 1 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": _config_block(args, n, op.storage_bytes(),
                                         {"build": {k: v for k, v in info.items() if k != "build_seconds"},
@@ -297,9 +307,10 @@ def run_b200(args):
                                          "bytes_by_kind": st["bytes_by_kind"]}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                              "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic,
-                             "peak_kind": peak_kind,
+                             "peak_kind": peak_kind, "aggregate_over_gpus": ws,
                              "algorithmic_bytes_per_launch": b_alg},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps, "clocks": clocks,
+                "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": (2 if ws == 1 else 3) * args.steps, "clocks": clocks,
                 "parity_rel_err_vs_oracle": parity}
         print(json.dumps(line), flush=True)
     if ws > 1:

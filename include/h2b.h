@@ -142,6 +142,12 @@ const char* h2b_last_error(void);
 int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out);
 int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* out);
 int h2b_plan_stats(const h2b_plan* p, h2b_stats* out);
+/* Multi-GPU plans have two phases; single-GPU plans one. */
+int h2b_plan_phases(const h2b_plan* p);
+int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* out);
+/* rank_lo_hi[2*world]: tree-position range of each rank's leaves;
+ * exchange[2]: {offset, doubles per rank} of the x^ exchange regions. */
+int h2b_plan_partition(const h2b_plan* p, int64_t* rank_lo_hi, int64_t* exchange);
 void h2b_plan_destroy(h2b_plan* p);
 
 /* Device operator on the current CUDA device (cudaSetDevice beforehand). */
@@ -149,8 +155,15 @@ int h2b_create(const h2b_desc* d, const h2b_options* opt, h2b_op** out);
 /* y = M x with x, y device pointers (n x nrhs, node-major); asynchronous on
  * `stream` (cudaStream_t, NULL = legacy default).  The timed path. */
 int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, void* stream);
-/* Synchronous host convenience (the drop-in path): copies x in, y out. */
+/* Synchronous host convenience (the drop-in path): copies x in, y out.
+ * Multi-GPU rank operators return the full y on every rank. */
 int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs);
+/* One phase of a (multi-GPU) product and the exchange region between them
+ * (for drivers that move the x^ regions themselves instead of NCCL). */
+int h2b_matvec_phase(h2b_op* op, int phase, const double* x_dev, double* y_dev, int nrhs, void* stream);
+int h2b_exchange_region(h2b_op* op, int nrhs, double** base, int64_t* count_per_rank);
+/* Copy src's own exchange region into dst (same layout; async on stream). */
+int h2b_exchange_copy(h2b_op* dst, const h2b_op* src, int nrhs, void* stream);
 int64_t h2b_stream_bytes(const h2b_op* op);
 int h2b_stats_get(const h2b_op* op, h2b_stats* out);
 void h2b_destroy(h2b_op* op);

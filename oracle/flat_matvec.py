@@ -15,16 +15,50 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["run_plan", "check_plan_invariants"]
+__all__ = ["run_plan", "run_phase", "run_ranks", "check_plan_invariants"]
 
 
 def run_plan(plan: dict, x: np.ndarray) -> np.ndarray:
+    """Single-phase plan: y = M x."""
     x = np.asarray(x, dtype=np.float64)
     nrhs = 1 if x.ndim == 1 else x.shape[1]
-    X = x.reshape(plan["n"], nrhs)
-    mat, perm = plan["mat"], plan["perm"]
     coef = np.full((max(1, plan["coef_len"]), nrhs), np.nan)
     Y = np.full((plan["n"], nrhs), np.nan)
+    run_phase(plan, x, coef, Y)
+    return Y[:, 0].copy() if x.ndim == 1 else Y
+
+
+def run_ranks(rank_plans: list, x: np.ndarray) -> np.ndarray:
+    """Emulate a multi-GPU product: phase 0 on every rank, the all-gather of
+    the x^ exchange regions, phase 1 on every rank; each rank owns the rows
+    of its leaves."""
+    x = np.asarray(x, dtype=np.float64)
+    nrhs = 1 if x.ndim == 1 else x.shape[1]
+    W = len(rank_plans)
+    coefs = [np.full((max(1, p["coef_len"]), nrhs), np.nan) for p in rank_plans]
+    ys = [np.full((p["n"], nrhs), np.nan) for p in rank_plans]
+    for r, p in enumerate(rank_plans):
+        run_phase(p["phases"][0], x, coefs[r], ys[r])
+    off, cnt = rank_plans[0]["exchange"]
+    for r in range(W):
+        region = coefs[r][off + r * cnt: off + (r + 1) * cnt].copy()
+        for q in range(W):
+            coefs[q][off + r * cnt: off + (r + 1) * cnt] = region
+    for r, p in enumerate(rank_plans):
+        run_phase(p["phases"][1], x, coefs[r], ys[r])
+    Y = np.full_like(ys[0], np.nan)
+    for r, p in enumerate(rank_plans):
+        lo, hi = p["rank_lo_hi"][r]
+        rows = p["perm"][lo:hi]
+        assert not np.isnan(ys[r][rows]).any(), "rank left owned rows unwritten"
+        Y[rows] = ys[r][rows]
+    return Y[:, 0].copy() if x.ndim == 1 else Y
+
+
+def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray) -> None:
+    nrhs = coef.shape[1]
+    X = np.asarray(x, dtype=np.float64).reshape(plan["n"], nrhs)
+    mat, perm = plan["mat"], plan["perm"]
     done = np.zeros(len(plan["t_m"]), bool)
     t_seg0, t_dep0 = plan["t_seg0"], plan["t_dep0"]
     for t in range(len(plan["t_m"])):
@@ -59,7 +93,6 @@ def run_plan(plan: dict, x: np.ndarray) -> np.ndarray:
         else:
             coef[o:o + m] = acc
         done[t] = True
-    return Y[:, 0].copy() if x.ndim == 1 else Y
 
 
 def check_plan_invariants(plan: dict) -> None:

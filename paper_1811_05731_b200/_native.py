@@ -101,8 +101,16 @@ def _load():
     lib.h2b_destroy.argtypes = [C.c_void_p]
     lib.h2b_destroy.restype = None
     lib.h2b_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.h2b_plan_phases.argtypes = [C.c_void_p]
+    lib.h2b_plan_phase_view.argtypes = [C.c_void_p, C.c_int, C.POINTER(PlanView)]
+    lib.h2b_plan_partition.argtypes = [C.c_void_p, _p64, _p64]
+    lib.h2b_matvec_phase.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.h2b_exchange_region.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), _p64]
+    lib.h2b_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     for name in ("h2b_plan_create", "h2b_plan_view_get", "h2b_plan_stats", "h2b_create",
-                 "h2b_matvec_dev", "h2b_matvec", "h2b_stats_get", "h2b_nccl_unique_id"):
+                 "h2b_matvec_dev", "h2b_matvec", "h2b_stats_get", "h2b_nccl_unique_id",
+                 "h2b_plan_phases", "h2b_plan_phase_view", "h2b_plan_partition", "h2b_matvec_phase",
+                 "h2b_exchange_region", "h2b_exchange_copy"):
         getattr(lib, name).restype = C.c_int
     return lib
 

@@ -29,6 +29,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/h2b.h"
 #include "plan.h"
 
@@ -676,16 +678,9 @@ namespace h2b_detail {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 }  // namespace h2b_detail
 
-struct h2b_op {
-  int device = 0;
-  int64_t n = 0;
+// One kernel launch worth of device state (a Phase of the plan).
+struct PhaseDev {
   int64_t ntasks = 0;
-  int64_t coef_len = 0;
-  int max_nrhs = 16;
-  int wpc = 8;
-  int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
-  double* d_mat = nullptr;
-  double* d_coef = nullptr;
   DTask* d_tasks = nullptr;
   DSeg* d_segs = nullptr;
   DSeg* d_seg_inline = nullptr;
@@ -696,12 +691,29 @@ struct h2b_op {
   int32_t nready0_hi = 0;
   unsigned long long* d_arrived = nullptr;
   int32_t* d_ready_q = nullptr;
-  int64_t* d_perm = nullptr;
   unsigned* d_ready_flag = nullptr;
   Ctl* d_ctl = nullptr;
-  double* d_xp = nullptr;  // x in tree order
   unsigned long long* d_trace = nullptr;
+};
+
+struct h2b_op {
+  int device = 0;
+  int64_t n = 0;
+  int64_t coef_len = 0;
+  int max_nrhs = 16;
+  int wpc = 8;
+  int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
+  double* d_mat = nullptr;
+  double* d_coef = nullptr;
+  int64_t* d_perm = nullptr;
+  double* d_xp = nullptr;  // x in tree order
   int prefetch = 0;
+  std::vector<PhaseDev> ph;
+  // multi-GPU
+  int rank = 0, world = 1;
+  int64_t exch_off = 0, exch_count = 0;
+  ncclComm_t comm = nullptr;
+  // host path buffers
   double* d_x = nullptr;
   double* d_y = nullptr;
   size_t xy_cap = 0;
@@ -715,6 +727,12 @@ struct h2b_plan {
 };
 
 namespace {
+
+#define H2B_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) return fail(H2B_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
 
 h2b::PlanOptions to_plan_options(const h2b_options* o) {
   h2b::PlanOptions po;
@@ -733,13 +751,13 @@ void fill_stats(const h2b::Plan& P, h2b_stats* s) {
   s->stream_bytes = P.stream_bytes;
   s->pool_bytes = 8 * (int64_t)P.mat.size();
   s->coef_doubles = P.coef_len;
-  s->ntasks = P.ntasks();
-  s->nsegs = P.nsegs();
-  s->ndeps = (int64_t)P.deps.size();
-  for (int k = 0; k < 5; ++k) {
-    s->tasks_by_kind[k] = P.tasks_by_kind[k];
-    s->bytes_by_kind[k] = P.bytes_by_kind[k];
+  for (const auto& F : P.ph) {
+    s->ntasks += F.ntasks();
+    s->nsegs += F.nsegs();
+    s->ndeps += (int64_t)F.deps.size();
+    for (int k = 0; k < 5; ++k) s->tasks_by_kind[k] += F.tasks_by_kind[k];
   }
+  for (int k = 0; k < 5; ++k) s->bytes_by_kind[k] = P.bytes_by_kind[k];
   s->rank = P.rank;
   s->world_size = P.world_size;
   s->local_bytes = P.local_bytes;
@@ -765,52 +783,73 @@ int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
   int dev = 0, nsm = 0;
   H2B_CUDA(cudaGetDevice(&dev));
   H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (per_sm < 1) return fail(H2B_EINVAL, "work-item buffers do not fit in shared memory: lower task_bytes or warps_per_cta");
+  if (per_sm < 1) return fail(H2B_EINVAL, "per-warp shared memory does not fit: lower warps_per_cta");
   if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
   *grid = per_sm * nsm;
   return H2B_OK;
 }
 
+// xp = x[perm] then phase k of the plan.
 template <int NRHS>
-int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st) {
+  const PhaseDev& F = op->ph[k];
   KParams p;
-  p.tasks = op->d_tasks;
-  p.segs = op->d_segs;
-  p.seg_inline = op->d_seg_inline;
-  p.succ0 = op->d_succ0;
-  p.succ = op->d_succ;
-  p.ready0 = op->d_ready0;
-  p.nready0 = op->nready0;
-  p.nready0_hi = op->nready0_hi;
-  p.arrived = op->d_arrived;
-  p.ready_q = op->d_ready_q;
+  p.tasks = F.d_tasks;
+  p.segs = F.d_segs;
+  p.seg_inline = F.d_seg_inline;
+  p.succ0 = F.d_succ0;
+  p.succ = F.d_succ;
+  p.ready0 = F.d_ready0;
+  p.nready0 = F.nready0;
+  p.nready0_hi = F.nready0_hi;
+  p.arrived = F.d_arrived;
+  p.ready_q = F.d_ready_q;
+  p.ready_flag = F.d_ready_flag;
+  p.ctl = F.d_ctl;
+  p.trace = F.d_trace;
+  p.ntasks = (int32_t)F.ntasks;
   p.mat = op->d_mat;
   p.coef = op->d_coef;
   p.perm = op->d_perm;
   p.xp = op->d_xp;
   p.y = y;
   p.prefetch = op->prefetch;
-  p.trace = op->d_trace;
-  p.ready_flag = op->d_ready_flag;
-  p.ctl = op->d_ctl;
-  p.ntasks = (int32_t)op->ntasks;
   const int gi = nrhs_index(NRHS);
   const size_t smem = (size_t)op->wpc * sizeof(WarpSmem);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
-  {
+  if (k == 0) {
     const int64_t total = op->n * NRHS;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
     h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
   }
-  // the attribute is per function and shared by every operator of the process
-  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
+  if (F.ntasks > 0) {
+    // the attribute is per function and shared by every operator of the process
+    H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
                                std::to_string(op->grid[gi]) + ", block=" + std::to_string(op->wpc * 32) +
                                ", smem=" + std::to_string(smem) +
                                "): " + cudaGetErrorString(e) + " (stale: " + cudaGetErrorString(stale) + ")");
+  return H2B_OK;
+}
+
+// The whole product: all phases, with the x^ all-gather between them.
+template <int NRHS>
+int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+  for (int k = 0; k < (int)op->ph.size(); ++k) {
+    int rc = launch_phase<NRHS>(op, k, x, y, st);
+    if (rc != H2B_OK) return rc;
+    if (k == 0 && op->world > 1) {
+      if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
+      double* base = op->d_coef + op->exch_off * NRHS;
+      const size_t cnt = (size_t)op->exch_count * NRHS;
+      if (cnt > 0)
+        H2B_NCCL(ncclAllGather(base + (size_t)op->rank * cnt, base, cnt, ncclDouble, op->comm, st));
+    }
+  }
   return H2B_OK;
 }
 
@@ -822,55 +861,36 @@ int upload(T** dst, const T* src, size_t count) {
   return H2B_OK;
 }
 
+void free_phase(PhaseDev& F) {
+  cudaFree(F.d_tasks);
+  cudaFree(F.d_segs);
+  cudaFree(F.d_seg_inline);
+  cudaFree(F.d_succ0);
+  cudaFree(F.d_succ);
+  cudaFree(F.d_ready0);
+  cudaFree(F.d_arrived);
+  cudaFree(F.d_ready_q);
+  cudaFree(F.d_ready_flag);
+  cudaFree(F.d_ctl);
+  cudaFree(F.d_trace);
+}
+
 void free_op(h2b_op* op) {
   if (!op) return;
+  for (auto& F : op->ph) free_phase(F);
+  if (op->comm) ncclCommDestroy(op->comm);
   cudaFree(op->d_mat);
   cudaFree(op->d_coef);
-  cudaFree(op->d_tasks);
-  cudaFree(op->d_segs);
-  cudaFree(op->d_seg_inline);
-  cudaFree(op->d_succ0);
-  cudaFree(op->d_succ);
-  cudaFree(op->d_ready0);
-  cudaFree(op->d_arrived);
-  cudaFree(op->d_ready_q);
   cudaFree(op->d_perm);
-  cudaFree(op->d_ready_flag);
-  cudaFree(op->d_ctl);
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_xp);
-  cudaFree(op->d_trace);
   delete op;
 }
 
-int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
-  if (!out) return fail(H2B_EINVAL, "null output pointer");
-  *out = nullptr;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
-    cudaGetLastError();
-    return fail(H2B_ENODEV, "no CUDA device available");
-  }
-  h2b::Plan P;
-  std::string err;
-  int rc = h2b::build_plan(d, to_plan_options(o), &P, &err);
-  if (rc != H2B_OK) return fail(rc, err);
-  if (P.ntasks() >= INT32_MAX) return fail(H2B_EINVAL, "too many work items");
-
-  std::unique_ptr<h2b_op, void (*)(h2b_op*)> op(new h2b_op(), free_op);
-  H2B_CUDA(cudaGetDevice(&op->device));
-  op->n = P.n;
-  op->ntasks = P.ntasks();
-  op->coef_len = P.coef_len;
-  op->max_nrhs = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
-  if (nrhs_index(op->max_nrhs) < 0) return fail(H2B_EINVAL, "max_nrhs must be 1, 2, 4, 8 or 16");
-  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
-  if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
-  const int cps = o ? o->ctas_per_sm : 0;
-  op->prefetch = (o && o->l2_prefetch > 0) ? 1 : 0;
-
-  // device task / segment arrays
+int upload_phase(const h2b::Phase& P, PhaseDev* F) {
+  int rc;
+  F->ntasks = P.ntasks();
   std::vector<DTask> tasks(P.ntasks());
   for (int64_t i = 0; i < P.ntasks(); ++i) {
     DTask& t = tasks[i];
@@ -896,23 +916,18 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     segs[i].nslots = P.s_nslots[i];
     segs[i].stride = P.s_stride[i];
   }
-  // +2 doubles: a 16-byte-rounded TMA copy of the last item may read past the end
-  P.mat.push_back(0.0);
-  P.mat.push_back(0.0);
-  if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
-  P.mat.resize(P.mat.size() - 2);
-  if ((rc = upload(&op->d_tasks, tasks.data(), tasks.size()))) return rc;
-  if ((rc = upload(&op->d_segs, segs.data(), segs.size()))) return rc;
+  if ((rc = upload(&F->d_tasks, tasks.data(), tasks.size()))) return rc;
+  if ((rc = upload(&F->d_segs, segs.data(), segs.size()))) return rc;
   {
-    std::vector<DSeg> inl((size_t)P.ntasks() * kInlineSegs, DSeg{0, 0, 0, 0, 0});
+    std::vector<DSeg> inl((size_t)std::max<int64_t>(1, P.ntasks()) * kInlineSegs, DSeg{0, 0, 0, 0, 0});
     for (int64_t i = 0; i < P.ntasks(); ++i) {
       const int32_t a = P.t_seg0[i], b = P.t_seg0[i + 1];
       if (b - a <= kInlineSegs)
         for (int32_t k = a; k < b; ++k) inl[(size_t)i * kInlineSegs + (k - a)] = segs[k];
     }
-    if ((rc = upload(&op->d_seg_inline, inl.data(), inl.size()))) return rc;
+    if ((rc = upload(&F->d_seg_inline, inl.data(), inl.size()))) return rc;
   }
-  if ((rc = upload(&op->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
+  if ((rc = upload(&F->d_succ0, P.succ0.data(), P.succ0.size()))) return rc;
   {
     std::vector<int2> sd(P.succ.size());
     for (size_t k = 0; k < sd.size(); ++k) {
@@ -920,22 +935,63 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
       // low 24 bits: dependency count; bits 24+: the successor's queue class
       sd[k] = make_int2(d, (P.t_dep0[d + 1] - P.t_dep0[d]) | ((int)P.t_qclass[d] << 24));
     }
-    if ((rc = upload(&op->d_succ, sd.data(), sd.size()))) return rc;
+    if ((rc = upload(&F->d_succ, sd.data(), sd.size()))) return rc;
   }
-  if ((rc = upload(&op->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
-  op->nready0 = (int32_t)P.ready0.size();
-  op->nready0_hi = P.n_ready0_hi;
+  if ((rc = upload(&F->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
+  F->nready0 = (int32_t)P.ready0.size();
+  F->nready0_hi = P.n_ready0_hi;
+  const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
+  if ((rc = upload<unsigned long long>(&F->d_arrived, nullptr, T1))) return rc;
+  if ((rc = upload<int32_t>(&F->d_ready_q, nullptr, kQueues * T1))) return rc;
+  if ((rc = upload<unsigned>(&F->d_ready_flag, nullptr, kQueues * T1))) return rc;
+  if ((rc = upload<Ctl>(&F->d_ctl, nullptr, 1))) return rc;
+  H2B_CUDA(cudaMemset(F->d_arrived, 0, sizeof(unsigned long long) * T1));
+  H2B_CUDA(cudaMemset(F->d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));
+  H2B_CUDA(cudaMemset(F->d_ctl, 0, sizeof(Ctl)));
+  return H2B_OK;
+}
+
+int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
+  if (!out) return fail(H2B_EINVAL, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(H2B_ENODEV, "no CUDA device available");
+  }
+  h2b::Plan P;
+  std::string err;
+  int rc = h2b::build_plan(d, to_plan_options(o), &P, &err);
+  if (rc != H2B_OK) return fail(rc, err);
+  for (const auto& F : P.ph)
+    if (F.ntasks() >= INT32_MAX / kQueues) return fail(H2B_EINVAL, "too many work items");
+
+  std::unique_ptr<h2b_op, void (*)(h2b_op*)> op(new h2b_op(), free_op);
+  H2B_CUDA(cudaGetDevice(&op->device));
+  op->n = P.n;
+  op->coef_len = P.coef_len;
+  op->max_nrhs = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
+  if (nrhs_index(op->max_nrhs) < 0) return fail(H2B_EINVAL, "max_nrhs must be 1, 2, 4, 8 or 16");
+  op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
+  if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
+  const int cps = o ? o->ctas_per_sm : 0;
+  op->prefetch = (o && o->l2_prefetch > 0) ? 1 : 0;
+  op->rank = P.rank;
+  op->world = P.world_size;
+  op->exch_off = P.exch_off;
+  op->exch_count = P.exch_count;
+
+  // +2 doubles: a 16-byte-rounded TMA copy of the last item may read past the end
+  P.mat.push_back(0.0);
+  P.mat.push_back(0.0);
+  if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
+  P.mat.resize(P.mat.size() - 2);
+  op->ph.resize(P.ph.size());
+  for (size_t k = 0; k < P.ph.size(); ++k)
+    if ((rc = upload_phase(P.ph[k], &op->ph[k]))) return rc;
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
-  const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
-  if ((rc = upload<unsigned long long>(&op->d_arrived, nullptr, T1))) return rc;
-  if ((rc = upload<int32_t>(&op->d_ready_q, nullptr, kQueues * T1))) return rc;
-  if ((rc = upload<unsigned>(&op->d_ready_flag, nullptr, kQueues * T1))) return rc;
-  if ((rc = upload<Ctl>(&op->d_ctl, nullptr, 1))) return rc;
-  H2B_CUDA(cudaMemset(op->d_arrived, 0, sizeof(unsigned long long) * T1));
-  H2B_CUDA(cudaMemset(op->d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));
-  H2B_CUDA(cudaMemset(op->d_ctl, 0, sizeof(Ctl)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
   if ((rc = occupancy_grid<1>(op->wpc, cps, &op->grid[0]))) return rc;
@@ -943,6 +999,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = occupancy_grid<4>(op->wpc, cps, &op->grid[2]))) return rc;
   if ((rc = occupancy_grid<8>(op->wpc, cps, &op->grid[3]))) return rc;
   if ((rc = occupancy_grid<16>(op->wpc, cps, &op->grid[4]))) return rc;
+  if (op->world > 1 && o && o->nccl_unique_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, o->nccl_unique_id, sizeof(id));
+    H2B_NCCL(ncclCommInitRank(&op->comm, op->world, id, op->rank));
+  }
   H2B_CUDA(cudaDeviceSynchronize());
 
   fill_stats(P, &op->stats);
@@ -952,11 +1013,16 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   return H2B_OK;
 }
 
+int check_nrhs(const h2b_op* op, int nrhs) {
+  if (nrhs_index(nrhs) < 0 || nrhs > op->max_nrhs)
+    return fail(H2B_EINVAL, "nrhs must be 1, 2, 4, 8 or 16 and <= max_nrhs");
+  return H2B_OK;
+}
+
 int matvec_dev_impl(h2b_op* op, const double* x, double* y, int nrhs, void* stream) {
   if (!op) return fail(H2B_EINVAL, "null operator");
   if (!x || !y) return fail(H2B_EINVAL, "null vector");
-  if (nrhs_index(nrhs) < 0 || nrhs > op->max_nrhs)
-    return fail(H2B_EINVAL, "nrhs must be 1, 2, 4, 8 or 16 and <= max_nrhs");
+  if (check_nrhs(op, nrhs)) return H2B_EINVAL;
   H2B_CUDA(cudaSetDevice(op->device));
   cudaStream_t st = (cudaStream_t)stream;
   switch (nrhs) {
@@ -966,6 +1032,32 @@ int matvec_dev_impl(h2b_op* op, const double* x, double* y, int nrhs, void* stre
     case 8: return launch<8>(op, x, y, st);
     default: return launch<16>(op, x, y, st);
   }
+}
+
+void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
+  v->ntasks = F.ntasks();
+  v->nsegs = F.nsegs();
+  v->ndeps = (int64_t)F.deps.size();
+  v->mat_len = (int64_t)P.mat.size();
+  v->coef_len = P.coef_len;
+  v->mat = P.mat.data();
+  v->t_data = F.t_data.data();
+  v->t_out = F.t_out.data();
+  v->t_bias = F.t_bias.data();
+  v->t_m = F.t_m.data();
+  v->t_ld = F.t_ld.data();
+  v->t_ncols = F.t_ncols.data();
+  v->t_kind = F.t_kind.data();
+  v->t_seg0 = F.t_seg0.data();
+  v->t_dep0 = F.t_dep0.data();
+  v->t_bias_nslots = F.t_bias_nslots.data();
+  v->t_bias_stride = F.t_bias_stride.data();
+  v->s_src = F.s_src.data();
+  v->s_ncols = F.s_ncols.data();
+  v->s_kind = F.s_kind.data();
+  v->s_nslots = F.s_nslots.data();
+  v->s_stride = F.s_stride.data();
+  v->deps = F.deps.data();
 }
 
 }  // namespace
@@ -992,32 +1084,25 @@ int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
   }
 }
 
-int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* v) {
-  if (!p || !v) return fail(H2B_EINVAL, "null argument");
+int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* v) { return h2b_plan_phase_view(p, 0, v); }
+
+int h2b_plan_phases(const h2b_plan* p) { return p ? (int)p->plan.ph.size() : -1; }
+
+int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* v) {
+  if (!p || !v || phase < 0 || phase >= (int)p->plan.ph.size()) return fail(H2B_EINVAL, "bad plan or phase");
+  fill_view(p->plan, p->plan.ph[phase], v);
+  return H2B_OK;
+}
+
+int h2b_plan_partition(const h2b_plan* p, int64_t* rank_lo_hi, int64_t* exchange) {
+  if (!p || !rank_lo_hi || !exchange) return fail(H2B_EINVAL, "null argument");
   const h2b::Plan& P = p->plan;
-  v->ntasks = P.ntasks();
-  v->nsegs = P.nsegs();
-  v->ndeps = (int64_t)P.deps.size();
-  v->mat_len = (int64_t)P.mat.size();
-  v->coef_len = P.coef_len;
-  v->mat = P.mat.data();
-  v->t_data = P.t_data.data();
-  v->t_out = P.t_out.data();
-  v->t_bias = P.t_bias.data();
-  v->t_m = P.t_m.data();
-  v->t_ld = P.t_ld.data();
-  v->t_ncols = P.t_ncols.data();
-  v->t_kind = P.t_kind.data();
-  v->t_seg0 = P.t_seg0.data();
-  v->t_dep0 = P.t_dep0.data();
-  v->t_bias_nslots = P.t_bias_nslots.data();
-  v->t_bias_stride = P.t_bias_stride.data();
-  v->s_src = P.s_src.data();
-  v->s_ncols = P.s_ncols.data();
-  v->s_kind = P.s_kind.data();
-  v->s_nslots = P.s_nslots.data();
-  v->s_stride = P.s_stride.data();
-  v->deps = P.deps.data();
+  for (size_t r = 0; r < P.rank_lo.size(); ++r) {
+    rank_lo_hi[2 * r] = P.rank_lo[r];
+    rank_lo_hi[2 * r + 1] = P.rank_hi[r];
+  }
+  exchange[0] = P.exch_off;
+  exchange[1] = P.exch_count;
   return H2B_OK;
 }
 
@@ -1041,6 +1126,39 @@ int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, voi
   return matvec_dev_impl(op, x_dev, y_dev, nrhs, stream);
 }
 
+int h2b_matvec_phase(h2b_op* op, int phase, const double* x_dev, double* y_dev, int nrhs, void* stream) {
+  if (!op || phase < 0 || phase >= (int)op->ph.size()) return fail(H2B_EINVAL, "bad operator or phase");
+  if (!x_dev || !y_dev) return fail(H2B_EINVAL, "null vector");
+  if (check_nrhs(op, nrhs)) return H2B_EINVAL;
+  H2B_CUDA(cudaSetDevice(op->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (nrhs) {
+    case 1: return launch_phase<1>(op, phase, x_dev, y_dev, st);
+    case 2: return launch_phase<2>(op, phase, x_dev, y_dev, st);
+    case 4: return launch_phase<4>(op, phase, x_dev, y_dev, st);
+    case 8: return launch_phase<8>(op, phase, x_dev, y_dev, st);
+    default: return launch_phase<16>(op, phase, x_dev, y_dev, st);
+  }
+}
+
+int h2b_exchange_region(h2b_op* op, int nrhs, double** base, int64_t* count_per_rank) {
+  if (!op || !base || !count_per_rank) return fail(H2B_EINVAL, "null argument");
+  *base = op->d_coef + op->exch_off * nrhs;
+  *count_per_rank = op->exch_count * nrhs;
+  return H2B_OK;
+}
+
+int h2b_exchange_copy(h2b_op* dst, const h2b_op* src, int nrhs, void* stream) {
+  if (!dst || !src || dst->exch_count != src->exch_count || dst->exch_off != src->exch_off)
+    return fail(H2B_EINVAL, "operators do not share an exchange layout");
+  const size_t cnt = (size_t)src->exch_count * nrhs;
+  const size_t off = (size_t)src->exch_off * nrhs + (size_t)src->rank * cnt;
+  if (cnt)
+    H2B_CUDA(cudaMemcpyAsync(dst->d_coef + off, src->d_coef + off, sizeof(double) * cnt, cudaMemcpyDefault,
+                             (cudaStream_t)stream));
+  return H2B_OK;
+}
+
 int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs) {
   if (!op) return fail(H2B_EINVAL, "null operator");
   if (n != op->n) return fail(H2B_EINVAL, "vector must have shape (" + std::to_string(op->n) + ",)");
@@ -1058,8 +1176,15 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
     op->xy_cap = bytes;
   }
   H2B_CUDA(cudaMemcpy(op->d_x, x_host, bytes, cudaMemcpyHostToDevice));
+  if (op->world > 1) H2B_CUDA(cudaMemset(op->d_y, 0, bytes));
   int rc = matvec_dev_impl(op, op->d_x, op->d_y, nrhs, nullptr);
   if (rc != H2B_OK) return rc;
+  // multi-GPU: every rank wrote its own rows, the others are zero; one sum
+  // assembles the full y everywhere (exact: one nonzero term per entry)
+  if (op->world > 1) {
+    if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
+    H2B_NCCL(ncclAllReduce(op->d_y, op->d_y, (size_t)n * std::max(1, nrhs), ncclDouble, ncclSum, op->comm, nullptr));
+  }
   H2B_CUDA(cudaMemcpy(y_host, op->d_y, bytes, cudaMemcpyDeviceToHost));
   return H2B_OK;
 }
@@ -1069,26 +1194,29 @@ int64_t h2b_stream_bytes(const h2b_op* op) { return op ? op->stats.stream_bytes 
 int h2b_trace_enable(h2b_op* op, int on) {
   if (!op) return fail(H2B_EINVAL, "null operator");
   H2B_CUDA(cudaSetDevice(op->device));
-  if (on && !op->d_trace) {
-    H2B_CUDA(cudaMalloc(&op->d_trace, sizeof(unsigned long long) * 8 * std::max<int64_t>(1, op->ntasks)));
-    H2B_CUDA(cudaMemset(op->d_trace, 0, sizeof(unsigned long long) * 8 * std::max<int64_t>(1, op->ntasks)));
-  } else if (!on && op->d_trace) {
-    cudaFree(op->d_trace);
-    op->d_trace = nullptr;
+  PhaseDev& F = op->ph[0];
+  const size_t cnt = 8 * (size_t)std::max<int64_t>(1, F.ntasks);
+  if (on && !F.d_trace) {
+    H2B_CUDA(cudaMalloc(&F.d_trace, sizeof(unsigned long long) * cnt));
+    H2B_CUDA(cudaMemset(F.d_trace, 0, sizeof(unsigned long long) * cnt));
+  } else if (!on && F.d_trace) {
+    cudaFree(F.d_trace);
+    F.d_trace = nullptr;
   }
   return H2B_OK;
 }
 
 int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems) {
-  if (!op || !out || nitems != op->ntasks || !op->d_trace) return fail(H2B_EINVAL, "trace not enabled or wrong size");
-  H2B_CUDA(cudaMemcpy(out, op->d_trace, sizeof(uint64_t) * 8 * nitems, cudaMemcpyDeviceToHost));
+  if (!op || !out || nitems != op->ph[0].ntasks || !op->ph[0].d_trace)
+    return fail(H2B_EINVAL, "trace not enabled or wrong size");
+  H2B_CUDA(cudaMemcpy(out, op->ph[0].d_trace, sizeof(uint64_t) * 8 * nitems, cudaMemcpyDeviceToHost));
   return H2B_OK;
 }
 
 int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems) {
-  if (!op || !out || nitems != op->ntasks) return fail(H2B_EINVAL, "wrong size");
+  if (!op || !out || nitems != op->ph[0].ntasks) return fail(H2B_EINVAL, "wrong size");
   std::vector<DTask> t(nitems);
-  H2B_CUDA(cudaMemcpy(t.data(), op->d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
+  H2B_CUDA(cudaMemcpy(t.data(), op->ph[0].d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < nitems; ++i) out[i] = t[i].kind;
   return H2B_OK;
 }
@@ -1108,7 +1236,10 @@ void h2b_destroy(h2b_op* op) {
 
 int h2b_nccl_unique_id(void* out128) {
   if (!out128) return fail(H2B_EINVAL, "null argument");
-  return fail(H2B_ENCCL, "multi-GPU support is not built into this library yet");
+  ncclUniqueId id;
+  H2B_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return H2B_OK;
 }
 
 }  // extern "C"

@@ -48,6 +48,7 @@ struct TaskTmp {
   int32_t m, ld, ncols, kind, bias_nslots, bias_stride;
   int32_t stage;
   int32_t qclass = 0;
+  int32_t cl = 0;                // cluster (row cluster for down/near/final)
   std::vector<int32_t> seg_idx;  // into seg tables
   std::vector<int32_t> deps;     // provisional ids
 };
@@ -67,6 +68,10 @@ class Builder {
   std::vector<int32_t> leaves_;             // preorder == position order
   std::vector<Vec> xhat_, yhat_, nearv_;
   std::vector<TaskTmp> tasks_;
+  int32_t cur_cl_ = 0;  // cluster of the group being emitted
+  // finish one phase from provisional task ids (any order); deps outside
+  // `in_phase` are dropped (satisfied before the phase starts)
+  int finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char>& in_phase, std::string* err);
   // segment tables (final)
   std::vector<int64_t> s_src_;
   std::vector<int32_t> s_ncols_, s_kind_, s_nslots_, s_stride_;
@@ -289,6 +294,7 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       // clusters are needed as the chain descends (class 1); coupling pieces
       // of leaves and the near field only by the finals (class 2)
       t.qclass = qclass;
+      t.cl = cur_cl_;
       if (seg0_hi) {
         for (auto& part : pc.parts) if (part[0] == 0) t.qclass = 0;
       }
@@ -332,6 +338,7 @@ int Builder::run(std::string* err) {
     int32_t k = (int32_t)d->k_col[c];
     if (k == 0) continue;
     std::vector<SegSpec> segs{{kSegX, d->cl_start[c], (int32_t)size(c), nullptr, d->col_basis[c], false, 0}};
+    cur_cl_ = c;
     emit_group(kUpLeaf, 0, k, segs, &xhat_[c], 0, nullptr, true);
   }
   // ---- forward, inner clusters bottom-up: x^_p = sum_c F_c^T x^_c (h2.py:201-205)
@@ -348,6 +355,7 @@ int Builder::run(std::string* err) {
         if (!xhat_[ch].exists()) continue;
         segs.push_back({kSegCoef, 0, (int32_t)d->k_col[ch], &xhat_[ch], d->col_transfer[ch], false, 0});
       }
+      cur_cl_ = p;
       emit_group(kUpNode, height_[p], k, segs, &xhat_[p], 0, nullptr, true);
     }
   }
@@ -371,6 +379,7 @@ int Builder::run(std::string* err) {
         int64_t ncol = size(s);
         segs.push_back({kSegX, d->cl_start[s], (int32_t)ncol, nullptr, d->nr_data[b] + br.second * ncol, true, ncol});
       }
+      cur_cl_ = l;
       emit_group(kNear, 0, (int32_t)size(l), segs, &nearv_[l], 0, nullptr, true, 2);
     }
   }
@@ -398,6 +407,7 @@ int Builder::run(std::string* err) {
       }
       if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
       const bool transfer = t != 0 && yhat_[parent_[t]].exists();
+      cur_cl_ = t;
       emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 2 : 1, transfer);
     }
   }
@@ -407,6 +417,7 @@ int Builder::run(std::string* err) {
     int32_t k = (int32_t)d->k_row[l];
     if (k > 0 && yhat_[l].exists())
       segs.push_back({kSegCoef, 0, k, &yhat_[l], d->row_basis[l], true, k});
+    cur_cl_ = l;
     emit_group(kFinal, 0, (int32_t)size(l), segs, nullptr, d->cl_start[l], &nearv_[l], false);
   }
   // Entries never read by the product (e.g. row bases of an operator
@@ -416,105 +427,212 @@ int Builder::run(std::string* err) {
     return H2B_EINVAL;
   }
 
-  // ---- queue order: up-leaf, [near chunk, chain stage]*, near chunk, final
   const int32_t T = (int32_t)tasks_.size();
-  std::vector<int32_t> up_leaf, nearq, finalq;
-  std::vector<std::vector<int32_t>> stages;
-  int32_t max_h = 0, max_d = 0;
-  for (auto& t : tasks_) {
-    if (t.kind == kUpNode) max_h = std::max(max_h, t.stage);
-    if (t.kind == kDown) max_d = std::max(max_d, t.stage);
+  P.rank_lo.assign(1, 0);
+  P.rank_hi.assign(1, d->n);
+  if (opt_.world_size <= 1) {
+    std::vector<int32_t> all(T);
+    std::iota(all.begin(), all.end(), 0);
+    P.ph.resize(1);
+    P.local_bytes = P.stream_bytes;
+    return finalize(&P.ph[0], all, std::vector<char>(T, 1), err);
   }
-  std::vector<std::vector<int32_t>> upn(max_h + 1), dn(max_d + 1);
-  for (int32_t i = 0; i < T; ++i) {
-    auto& t = tasks_[i];
-    switch (t.kind) {
-      case kUpLeaf: up_leaf.push_back(i); break;
-      case kUpNode: upn[t.stage].push_back(i); break;
-      case kDown: dn[t.stage].push_back(i); break;
-      case kNear: nearq.push_back(i); break;
-      default: finalq.push_back(i); break;
-    }
-  }
-  for (auto& v : upn) if (!v.empty()) stages.push_back(v);
-  for (auto& v : dn) if (!v.empty()) stages.push_back(v);
-  std::vector<int32_t> q;
-  q.reserve(T);
-  q.insert(q.end(), up_leaf.begin(), up_leaf.end());
-  const size_t S = stages.size();
-  if (opt_.interleave) {
-    size_t taken = 0;
-    for (size_t s = 0; s <= S; ++s) {
-      size_t upto = (nearq.size() * (s + 1)) / (S + 1);
-      q.insert(q.end(), nearq.begin() + taken, nearq.begin() + upto);
-      taken = upto;
-      if (s < S) q.insert(q.end(), stages[s].begin(), stages[s].end());
-    }
-  } else {
-    for (auto& v : stages) q.insert(q.end(), v.begin(), v.end());
-    q.insert(q.end(), nearq.begin(), nearq.end());
-  }
-  q.insert(q.end(), finalq.begin(), finalq.end());
-  std::vector<int32_t> pos(T);
-  for (int32_t i = 0; i < T; ++i) pos[q[i]] = i;
 
-  P.t_data.resize(T); P.t_out.resize(T); P.t_bias.resize(T);
-  P.t_m.resize(T); P.t_ld.resize(T); P.t_ncols.resize(T); P.t_kind.resize(T);
-  P.t_bias_nslots.resize(T); P.t_bias_stride.resize(T); P.t_qclass.resize(T);
-  P.t_seg0.assign(T + 1, 0); P.t_dep0.assign(T + 1, 0);
+  // ---- multi-GPU: byte-balanced contiguous leaf ranges (tree order is a
+  // geometric bisection order, so ranges are compact), DESIGN.md §7
+  const int32_t W = opt_.world_size, R = opt_.rank;
+  std::vector<double> leaf_w(nc, 0.0);
+  for (auto& t : tasks_) leaf_w[t.cl] += 8.0 * t.m * t.ncols;
+  double total = 0.0;
+  for (int32_t l : leaves_) total += leaf_w[l] + 1.0;
+  P.rank_lo.assign(W, 0);
+  P.rank_hi.assign(W, 0);
+  {
+    double acc = 0.0;
+    int32_t r = 0;
+    P.rank_lo[0] = 0;
+    for (size_t i = 0; i < leaves_.size(); ++i) {
+      const int32_t l = leaves_[i];
+      acc += leaf_w[l] + 1.0;
+      const size_t left = leaves_.size() - i - 1;
+      if (r < W - 1 && (acc >= total * (r + 1) / W || left <= (size_t)(W - 1 - r))) {
+        P.rank_hi[r] = d->cl_end[l];
+        ++r;
+        P.rank_lo[r] = d->cl_end[l];
+      }
+    }
+    for (; r < W; ++r) {
+      if (r > 0 && P.rank_lo[r] == 0) P.rank_lo[r] = d->n;
+      P.rank_hi[r] = d->n;
+    }
+  }
+  const int64_t lo = P.rank_lo[R], hi = P.rank_hi[R];
+  auto owner = [&](int32_t c) -> int32_t {
+    for (int32_t r = 0; r < W; ++r)
+      if (d->cl_start[c] >= P.rank_lo[r] && d->cl_end[c] <= P.rank_hi[r]) return r;
+    return -1;  // spans several ranks
+  };
+  // selection and phase of every task on this rank
+  std::vector<char> sel(T, 0), in0(T, 0), in1(T, 0);
   for (int32_t i = 0; i < T; ++i) {
-    const TaskTmp& t = tasks_[q[i]];
-    P.t_data[i] = t.data; P.t_out[i] = t.out; P.t_bias[i] = t.bias;
-    P.t_m[i] = t.m; P.t_ld[i] = t.ld; P.t_ncols[i] = t.ncols; P.t_kind[i] = t.kind;
-    P.t_bias_nslots[i] = t.bias_nslots; P.t_bias_stride[i] = t.bias_stride;
-    P.t_qclass[i] = t.qclass;
+    const TaskTmp& t = tasks_[i];
+    const int32_t o = owner(t.cl);
+    if (t.kind == kUpLeaf || t.kind == kUpNode) {
+      if (o == R) { sel[i] = 1; in0[i] = 1; }
+      else if (o < 0) { sel[i] = 1; in1[i] = 1; }
+    } else if (t.kind == kDown) {
+      if (d->cl_start[t.cl] < hi && d->cl_end[t.cl] > lo) { sel[i] = 1; in1[i] = 1; }
+    } else if (o == R) {
+      sel[i] = 1; in1[i] = 1;
+    }
+  }
+  // coefficient layout: the x^ vectors of owned clusters move into
+  // per-rank exchange regions of equal size at the start of the workspace
+  {
+    struct Blk { int64_t old_off, size, new_off; };
+    std::vector<Blk> blks;
+    std::vector<int64_t> region(W, 0);
+    std::vector<int32_t> blk_owner;
+    for (int32_t c = 0; c < nc; ++c) {
+      const Vec& v = xhat_[c];
+      if (!v.exists()) continue;
+      const int32_t o = owner(c);
+      blks.push_back({v.off, (int64_t)v.len * v.nslots, 0});
+      blk_owner.push_back(o);
+      if (o >= 0) region[o] += (int64_t)v.len * v.nslots;
+    }
+    int64_t rsz = 0;
+    for (int32_t r = 0; r < W; ++r) rsz = std::max(rsz, region[r]);
+    std::vector<int64_t> fill(W);
+    for (int32_t r = 0; r < W; ++r) fill[r] = (int64_t)r * rsz;
+    // everything else keeps its order after the regions
+    std::vector<char> moved(P.coef_len, 0);
+    for (size_t b2 = 0; b2 < blks.size(); ++b2)
+      if (blk_owner[b2] >= 0) {
+        blks[b2].new_off = fill[blk_owner[b2]];
+        fill[blk_owner[b2]] += blks[b2].size;
+        std::fill(moved.begin() + blks[b2].old_off, moved.begin() + blks[b2].old_off + blks[b2].size, 1);
+      }
+    // map for the rest: compact the unmoved doubles after the regions
+    std::vector<int64_t> rest(P.coef_len + 1, 0);
+    int64_t nxt = (int64_t)W * rsz;
+    for (int64_t o = 0; o < P.coef_len; ++o) {
+      rest[o] = nxt;
+      if (!moved[o]) ++nxt;
+    }
+    std::vector<int64_t> newpos(P.coef_len, 0);
+    for (int64_t o = 0; o < P.coef_len; ++o) newpos[o] = rest[o];
+    for (size_t b2 = 0; b2 < blks.size(); ++b2)
+      if (blk_owner[b2] >= 0)
+        for (int64_t k = 0; k < blks[b2].size; ++k) newpos[blks[b2].old_off + k] = blks[b2].new_off + k;
+    auto map = [&](int64_t o) -> int64_t { return o < P.coef_len ? newpos[o] : o; };
+    for (auto& t : tasks_) {
+      if (t.kind != kFinal) t.out = map(t.out);
+      if (t.bias >= 0) t.bias = map(t.bias);
+    }
+    for (size_t k = 0; k < s_src_.size(); ++k)
+      if (s_kind_[k] == kSegCoef) s_src_[k] = map(s_src_[k]);
+    P.coef_len = nxt;
+    P.exch_off = 0;
+    P.exch_count = rsz;
+  }
+  P.ph.resize(2);
+  std::vector<int32_t> ids0, ids1;
+  P.local_bytes = 0;
+  for (int32_t i = 0; i < T; ++i) {
+    if (in0[i]) ids0.push_back(i);
+    if (in1[i]) ids1.push_back(i);
+    if (sel[i]) P.local_bytes += 8 * (int64_t)tasks_[i].m * tasks_[i].ncols;
+  }
+  // a phase-1 dependency on a phase-1 item of another rank would be a
+  // missing exchange: check the selection is closed
+  for (int32_t i : ids1)
+    for (int32_t dp : tasks_[i].deps)
+      if (!in1[dp] && !(tasks_[dp].kind == kUpLeaf || tasks_[dp].kind == kUpNode)) {
+        *err = "internal: rank plan is missing a dependency";
+        return H2B_EINVAL;
+      }
+  rc = finalize(&P.ph[0], ids0, in0, err);
+  if (rc != H2B_OK) return rc;
+  return finalize(&P.ph[1], ids1, in1, err);
+}
+
+int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char>& in_phase, std::string* err) {
+  // queue order: up-leaf, upward levels, downward levels, near field, finals
+  // (only the dependency order matters: the kernel schedules dynamically)
+  std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
+    auto key = [&](const TaskTmp& t) {
+      switch (t.kind) {
+        case kUpLeaf: return 0;
+        case kUpNode: return 1 + t.stage;
+        case kDown: return 1000 + t.stage;
+        case kNear: return 2000;
+        default: return 3000;
+      }
+    };
+    return key(tasks_[a]) < key(tasks_[b]);
+  });
+  const int32_t T = (int32_t)ids.size();
+  std::vector<int32_t> pos(tasks_.size(), -1);
+  for (int32_t i = 0; i < T; ++i) pos[ids[i]] = i;
+
+  F->t_data.resize(T); F->t_out.resize(T); F->t_bias.resize(T);
+  F->t_m.resize(T); F->t_ld.resize(T); F->t_ncols.resize(T); F->t_kind.resize(T);
+  F->t_bias_nslots.resize(T); F->t_bias_stride.resize(T); F->t_qclass.resize(T);
+  F->t_seg0.assign(T + 1, 0); F->t_dep0.assign(T + 1, 0);
+  for (int32_t i = 0; i < T; ++i) {
+    const TaskTmp& t = tasks_[ids[i]];
+    F->t_data[i] = t.data; F->t_out[i] = t.out; F->t_bias[i] = t.bias;
+    F->t_m[i] = t.m; F->t_ld[i] = t.ld; F->t_ncols[i] = t.ncols; F->t_kind[i] = t.kind;
+    F->t_bias_nslots[i] = t.bias_nslots; F->t_bias_stride[i] = t.bias_stride;
+    F->t_qclass[i] = (int8_t)t.qclass;
     for (int32_t si : t.seg_idx) {
-      P.s_src.push_back(s_src_[si]); P.s_ncols.push_back(s_ncols_[si]); P.s_kind.push_back(s_kind_[si]);
-      P.s_nslots.push_back(s_nslots_[si]); P.s_stride.push_back(s_stride_[si]);
+      F->s_src.push_back(s_src_[si]); F->s_ncols.push_back(s_ncols_[si]); F->s_kind.push_back(s_kind_[si]);
+      F->s_nslots.push_back(s_nslots_[si]); F->s_stride.push_back(s_stride_[si]);
     }
     for (int32_t dp : t.deps) {
-      int32_t qd = pos[dp];
-      if (qd >= i) { *err = "internal: dependency not earlier in the queue"; return H2B_EINVAL; }
-      P.deps.push_back(qd);
+      if (!in_phase[dp]) continue;  // produced before this phase
+      const int32_t qd = pos[dp];
+      if (qd < 0 || qd >= i) { *err = "internal: dependency not earlier in the queue"; return H2B_EINVAL; }
+      F->deps.push_back(qd);
     }
-    P.t_seg0[i + 1] = (int32_t)P.s_ncols.size();
-    P.t_dep0[i + 1] = (int32_t)P.deps.size();
-    P.tasks_by_kind[t.kind] += 1;
+    F->t_seg0[i + 1] = (int32_t)F->s_ncols.size();
+    F->t_dep0[i + 1] = (int32_t)F->deps.size();
+    F->tasks_by_kind[t.kind] += 1;
   }
   // successor lists for the completion-driven scheduler
-  P.succ0.assign(T + 1, 0);
-  for (int32_t dp : P.deps) P.succ0[dp + 1] += 1;
-  for (int32_t i = 0; i < T; ++i) P.succ0[i + 1] += P.succ0[i];
-  P.succ.assign(P.deps.size(), 0);
+  F->succ0.assign(T + 1, 0);
+  for (int32_t dp : F->deps) F->succ0[dp + 1] += 1;
+  for (int32_t i = 0; i < T; ++i) F->succ0[i + 1] += F->succ0[i];
+  F->succ.assign(F->deps.size(), 0);
   {
-    std::vector<int32_t> fill(P.succ0.begin(), P.succ0.end() - 1);
+    std::vector<int32_t> fill(F->succ0.begin(), F->succ0.end() - 1);
     for (int32_t i = 0; i < T; ++i)
-      for (int32_t k = P.t_dep0[i]; k < P.t_dep0[i + 1]; ++k) P.succ[fill[P.deps[k]]++] = i;
+      for (int32_t k = F->t_dep0[i]; k < F->t_dep0[i + 1]; ++k) F->succ[fill[F->deps[k]]++] = i;
   }
   // initially ready items: class 0 first (up-leaf: they start the far-field
-  // chain), then class 1 (the near field) longest first, so that heavy rows
+  // chain), then the rest (the near field) longest first, so that heavy rows
   // start early and the end of the launch is made of short items
   for (int32_t i = 0; i < T; ++i)
-    if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] == 0) P.ready0.push_back(i);
-  P.n_ready0_hi = (int32_t)P.ready0.size();
+    if (F->t_dep0[i + 1] == F->t_dep0[i] && F->t_qclass[i] == 0) F->ready0.push_back(i);
+  F->n_ready0_hi = (int32_t)F->ready0.size();
   {
-    std::vector<int32_t> lo;
+    std::vector<int32_t> rest;
     for (int32_t i = 0; i < T; ++i)
-      if (P.t_dep0[i + 1] == P.t_dep0[i] && P.t_qclass[i] != 0) lo.push_back(i);  // near field
-    std::stable_sort(lo.begin(), lo.end(), [&](int32_t a, int32_t b) {
-      return (int64_t)P.t_m[a] * P.t_ncols[a] > (int64_t)P.t_m[b] * P.t_ncols[b];
+      if (F->t_dep0[i + 1] == F->t_dep0[i] && F->t_qclass[i] != 0) rest.push_back(i);
+    std::stable_sort(rest.begin(), rest.end(), [&](int32_t a, int32_t b) {
+      return (int64_t)F->t_m[a] * F->t_ncols[a] > (int64_t)F->t_m[b] * F->t_ncols[b];
     });
-    P.ready0.insert(P.ready0.end(), lo.begin(), lo.end());
+    F->ready0.insert(F->ready0.end(), rest.begin(), rest.end());
   }
-  P.local_bytes = P.stream_bytes;
   return H2B_OK;
 }
 
 }  // namespace
 
 int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string* err) {
-  if (opt.world_size > 1) {
-    *err = "multi-GPU plans are built per rank by the partitioner (not yet available)";
+  if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= std::max(1, opt.world_size)) {
+    *err = "rank must be in [0, world_size)";
     return H2B_EINVAL;
   }
   if (opt.task_bytes < 8 || opt.far_task_bytes < 8) { *err = "task_bytes must be >= 8"; return H2B_EINVAL; }

@@ -38,17 +38,14 @@ constexpr int kMaxRows = 64;  // rows per work item (lanes own rows l, l+32)
 constexpr int kMaxSegs = 32;  // source segments per work item (one per lane)
 constexpr int kMaxNearPieces = 32;  // near-field items per leaf row at most
 
-struct Plan {
-  int64_t n = 0;
-  std::vector<int64_t> perm;
-  std::vector<double> mat;  // packed matrix pool
-  int64_t coef_len = 0;     // doubles per right-hand side
-  int64_t stream_bytes = 0; // == H2Matrix.storage_bytes()
-
+// One launch of the persistent kernel: a work-item queue (queue order, all
+// dependencies earlier) with its scheduling metadata.
+struct Phase {
   // tasks (queue order)
   std::vector<int64_t> t_data, t_out, t_bias;
   std::vector<int32_t> t_m, t_ld, t_ncols, t_kind, t_seg0, t_dep0;
   std::vector<int32_t> t_bias_nslots, t_bias_stride;
+  std::vector<int8_t> t_qclass;     // 0: far-field chain, 1: inner coupling, 2: leaf coupling / near
   // segments
   std::vector<int64_t> s_src;
   std::vector<int32_t> s_ncols, s_kind, s_nslots, s_stride;
@@ -59,15 +56,32 @@ struct Plan {
   std::vector<int32_t> succ0, succ;
   std::vector<int32_t> ready0;
   int32_t n_ready0_hi = 0;          // ready0[0:n_ready0_hi) are class 0
-  std::vector<int8_t> t_qclass;     // 0: critical chain, 1: slack (near field, leaf coupling)
-
   int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
-  int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
-  int32_t rank = 0, world_size = 1;
-  int64_t local_bytes = 0;
 
   int64_t ntasks() const { return (int64_t)t_m.size(); }
   int64_t nsegs() const { return (int64_t)s_ncols.size(); }
+};
+
+// The execution plan of one operator on one rank.  Single GPU: one phase.
+// world_size > 1: phase 0 computes the upward coefficients
+// x^ of the clusters this rank owns into its exchange region of the
+// coefficient workspace, the regions are all-gathered (every rank's region
+// has exch_count doubles, rank r's at exch_off + r * exch_count), and phase 1
+// runs the rest of this rank's rows: the clusters spanning several ranks
+// (replicated), the downward pass, the near field and the finals of its
+// leaves.
+struct Plan {
+  int64_t n = 0;
+  std::vector<int64_t> perm;
+  std::vector<double> mat;  // packed matrix pool
+  int64_t coef_len = 0;     // doubles per right-hand side
+  int64_t stream_bytes = 0; // == H2Matrix.storage_bytes()
+  int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
+  int32_t rank = 0, world_size = 1;
+  int64_t local_bytes = 0;  // matrix bytes streamed by this rank
+  std::vector<Phase> ph;
+  int64_t exch_off = 0, exch_count = 0;
+  std::vector<int64_t> rank_lo, rank_hi;  // tree-position range of each rank's leaves
 };
 
 struct PlanOptions {

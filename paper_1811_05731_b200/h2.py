@@ -31,7 +31,15 @@ from . import _native as nat
 from .cluster import ClusterTree
 
 __all__ = ["H2Matrix", "h2_matvec", "h2_matmat", "DeviceOperator", "device_operator",
-           "describe", "plan_view", "install_into_reference", "rank_arrays"]
+           "describe", "plan_view", "install_into_reference", "rank_arrays", "nccl_unique_id"]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, every rank passes it to
+    ``DeviceOperator(op, rank=r, world_size=W, nccl_unique_id=...)``)."""
+    buf = C.create_string_buffer(128)
+    nat.check(nat.lib().h2b_nccl_unique_id(buf), "h2b_nccl_unique_id")
+    return buf.raw
 
 
 @dataclass(eq=False)
@@ -180,7 +188,7 @@ def describe(op) -> _DescHolder:
 
 
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, l2_prefetch=0,
-             rank=0, world_size=1) -> nat.Options:
+             rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
     o.far_task_bytes = int(far_task_bytes)
@@ -190,47 +198,69 @@ def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max
     o.l2_prefetch = int(l2_prefetch)
     o.rank = int(rank)
     o.world_size = int(world_size)
+    if nccl_unique_id is not None:
+        buf = C.create_string_buffer(bytes(nccl_unique_id), 128)
+        o._keep_id = buf
+        o.nccl_unique_id = C.cast(buf, C.c_void_p)
     return o
+
+
+def _grab_view(v) -> dict:
+    T, S, D = v.ntasks, v.nsegs, v.ndeps
+
+    def grab(ptr, count, dtype):
+        if count == 0:
+            return np.zeros(0, dtype)
+        return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
+
+    return {
+        "coef_len": int(v.coef_len),
+        "t_data": grab(v.t_data, T, np.int64), "t_out": grab(v.t_out, T, np.int64),
+        "t_bias": grab(v.t_bias, T, np.int64), "t_m": grab(v.t_m, T, np.int32),
+        "t_ld": grab(v.t_ld, T, np.int32), "t_ncols": grab(v.t_ncols, T, np.int32),
+        "t_kind": grab(v.t_kind, T, np.int32), "t_seg0": grab(v.t_seg0, T + 1, np.int32),
+        "t_dep0": grab(v.t_dep0, T + 1, np.int32),
+        "t_bias_nslots": grab(v.t_bias_nslots, T, np.int32),
+        "t_bias_stride": grab(v.t_bias_stride, T, np.int32),
+        "s_src": grab(v.s_src, S, np.int64), "s_ncols": grab(v.s_ncols, S, np.int32),
+        "s_kind": grab(v.s_kind, S, np.int32), "s_nslots": grab(v.s_nslots, S, np.int32),
+        "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
+    }
 
 
 def plan_view(op, **options) -> dict:
     """Host-only execution plan (no GPU needed), returned as numpy copies:
     the arrays the kernel consumes plus stats.  Used by the CPU tests, which
-    execute the plan with a numpy interpreter (oracle/flat_matvec.py)."""
+    execute the plan with a numpy interpreter (oracle/flat_matvec.py).
+    The top-level arrays are phase 0; ``phases`` lists every phase (two for
+    a multi-GPU rank plan)."""
     h = describe(op)
     lib = nat.lib()
     handle = C.c_void_p()
     nat.check(lib.h2b_plan_create(C.byref(h.desc), C.byref(_options(**options)), C.byref(handle)),
               "h2b_plan_create")
     try:
-        v = nat.PlanView()
-        nat.check(lib.h2b_plan_view_get(handle, C.byref(v)))
         st = nat.Stats()
         nat.check(lib.h2b_plan_stats(handle, C.byref(st)))
-        T, S, D = v.ntasks, v.nsegs, v.ndeps
-
-        def grab(ptr, count, dtype):
-            if count == 0:
-                return np.zeros(0, dtype)
-            return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True)
-
-        out = {
-            "mat": grab(v.mat, v.mat_len, np.float64),
-            "coef_len": int(v.coef_len),
-            "t_data": grab(v.t_data, T, np.int64), "t_out": grab(v.t_out, T, np.int64),
-            "t_bias": grab(v.t_bias, T, np.int64), "t_m": grab(v.t_m, T, np.int32),
-            "t_ld": grab(v.t_ld, T, np.int32), "t_ncols": grab(v.t_ncols, T, np.int32),
-            "t_kind": grab(v.t_kind, T, np.int32), "t_seg0": grab(v.t_seg0, T + 1, np.int32),
-            "t_dep0": grab(v.t_dep0, T + 1, np.int32),
-            "t_bias_nslots": grab(v.t_bias_nslots, T, np.int32),
-            "t_bias_stride": grab(v.t_bias_stride, T, np.int32),
-            "s_src": grab(v.s_src, S, np.int64), "s_ncols": grab(v.s_ncols, S, np.int32),
-            "s_kind": grab(v.s_kind, S, np.int32), "s_nslots": grab(v.s_nslots, S, np.int32),
-            "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
-            "perm": np.ascontiguousarray(h.arrays["perm"]).copy(),
-            "n": int(op.n),
-            "stats": st.as_dict(),
-        }
+        phases = []
+        mat = None
+        for k in range(lib.h2b_plan_phases(handle)):
+            v = nat.PlanView()
+            nat.check(lib.h2b_plan_phase_view(handle, k, C.byref(v)))
+            if mat is None:
+                mat = (np.ctypeslib.as_array(v.mat, shape=(v.mat_len,)).copy() if v.mat_len
+                       else np.zeros(0))
+            phases.append(_grab_view(v))
+        world = max(1, int(options.get("world_size", 1)))
+        lohi = np.zeros(2 * world, np.int64)
+        exch = np.zeros(2, np.int64)
+        nat.check(lib.h2b_plan_partition(handle, nat.as_i64_ptr(lohi), nat.as_i64_ptr(exch)))
+        perm = np.ascontiguousarray(h.arrays["perm"]).copy()
+        for ph in phases:
+            ph.update(mat=mat, perm=perm, n=int(op.n))
+        out = dict(phases[0])
+        out.update(phases=phases, stats=st.as_dict(), rank_lo_hi=lohi.reshape(world, 2),
+                   exchange=(int(exch[0]), int(exch[1])))
         return out
     finally:
         lib.h2b_plan_destroy(handle)
@@ -244,8 +274,8 @@ class DeviceOperator:
         h = describe(op)
         self._lib = nat.lib()
         handle = C.c_void_p()
-        nat.check(self._lib.h2b_create(C.byref(h.desc), C.byref(_options(**options)), C.byref(handle)),
-                  "h2b_create")
+        opts = _options(**options)
+        nat.check(self._lib.h2b_create(C.byref(h.desc), C.byref(opts), C.byref(handle)), "h2b_create")
         self._h = handle
         self._lock = threading.Lock()
 
@@ -268,9 +298,28 @@ class DeviceOperator:
         return y
 
     def matvec_dev(self, x_ptr: int, y_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
-        """Device pointers (e.g. ``tensor.data_ptr()``); asynchronous on ``stream``."""
+        """Device pointers (e.g. ``tensor.data_ptr()``); asynchronous on ``stream``.
+        For a multi-GPU rank operator, y receives this rank's rows."""
         nat.check(self._lib.h2b_matvec_dev(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
                                            int(nrhs), C.c_void_p(stream)), "h2b_matvec_dev")
+
+    def matvec_phase(self, phase: int, x_ptr: int, y_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
+        """One phase of a multi-GPU rank product."""
+        nat.check(self._lib.h2b_matvec_phase(self._h, int(phase), C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                             int(nrhs), C.c_void_p(stream)), "h2b_matvec_phase")
+
+    def exchange_copy_from(self, other: "DeviceOperator", nrhs: int = 1, stream: int = 0) -> None:
+        """Copy ``other``'s own x^ exchange region into this operator (for
+        drivers that run the ranks' phases themselves)."""
+        nat.check(self._lib.h2b_exchange_copy(self._h, other._h, int(nrhs), C.c_void_p(stream)),
+                  "h2b_exchange_copy")
+
+    def exchange_region(self, nrhs: int = 1) -> tuple[int, int]:
+        """(device address, doubles per rank) of the x^ exchange regions."""
+        base = C.c_void_p()
+        cnt = np.zeros(1, np.int64)
+        nat.check(self._lib.h2b_exchange_region(self._h, int(nrhs), C.byref(base), nat.as_i64_ptr(cnt)))
+        return int(base.value or 0), int(cnt[0])
 
     def close(self) -> None:
         if getattr(self, "_h", None):
