@@ -305,8 +305,8 @@ def run_b200(args):
                                                            (info.get("build_seconds") or {}).items()},
                                          "work_items": st["ntasks"], "grid": st["grid"],
                                          "bytes_by_kind": st["bytes_by_kind"]}),
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                             "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"] * ws, "unit": "GB/s",
+                             "frac": achieved / (peaks["hbm_gbs"] * ws), "traffic": args.traffic,
                              "peak_kind": peak_kind, "aggregate_over_gpus": ws,
                              "algorithmic_bytes_per_launch": b_alg},
                 "cpu_baseline": cpu, "e2e": e2e,
