@@ -75,16 +75,24 @@ typedef struct h2b_desc {
   const double* const* nr_data; /* [nnear] N_b                              */
 } h2b_desc;
 
+/* sched_flags: run the near item a warp claimed ahead before the coupling
+   rows of inner clusters (default: inner coupling rows first). */
+#define H2B_SCHED_NEAR_FIRST 1
+/* sched_flags bits 8-15: warps per CTA that take near-field items (0: all) */
+#define H2B_SCHED_NEAR_WARPS(k) (((k) & 0xff) << 8)
+/* sched_flags bits 16-17: columns in flight per lane of a streamed item:
+   0 -> 8 (default), 1 -> 16, 2 -> 4 */
+#define H2B_SCHED_STREAM(s) (((s) & 3) << 16)
+
 /* Execution-plan knobs.  Zero-initialise for defaults. */
 typedef struct h2b_options {
   int64_t task_bytes;   /* max bytes per near-field work item (def. 65536)   */
   int64_t far_task_bytes; /* max bytes per far-field item (default 4096): each
                              is staged to shared memory by one TMA bulk copy */
-  int32_t warps_per_cta;/* persistent CTA width in warps (default 10, <= 16) */
+  int32_t warps_per_cta;/* persistent CTA width in warps (default 8, <= 16)  */
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
-  int32_t l2_prefetch;  /* 1: 1-D TMA L2 prefetch (cp.async.bulk.prefetch) of
-                           the work item claimed ahead; 0 (default): off     */
+  int32_t sched_flags;  /* H2B_SCHED_* bits; 0 = default scheduling          */
   /* Multi-GPU (one process per GPU).  world_size <= 1: whole operator. */
   int32_t rank;
   int32_t world_size;

@@ -41,7 +41,7 @@ class Desc(C.Structure):
 class Options(C.Structure):
     _fields_ = [
         ("task_bytes", C.c_int64), ("far_task_bytes", C.c_int64), ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
-        ("max_nrhs", C.c_int32), ("l2_prefetch", C.c_int32),
+        ("max_nrhs", C.c_int32), ("sched_flags", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
     ]
 

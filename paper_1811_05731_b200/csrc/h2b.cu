@@ -22,6 +22,7 @@
 // deterministic, no floating-point atomics.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -108,10 +109,12 @@ struct KParams {
   int32_t ntasks;
   int32_t nready0;
   int32_t nready0_hi;                   // ready0[0:nready0_hi) are class 0
-  int32_t prefetch;                     // 1: 1-D TMA L2 prefetch of the claimed-ahead item
+  int32_t flags;                        // kFlag* scheduling switches (h2b_options.sched_flags)
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
 };
 
+// scheduling switches
+constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ahead near item
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -147,6 +150,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Arrival count: releases this warp's outputs (after __syncwarp) and acquires
+// the other predecessors' (their arrivals precede ours in the counter's
+// modification order), so neither a separate fence before nor after is needed.
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -222,11 +233,12 @@ __device__ __forceinline__ double ldA(const double* q) {
 // One work item with NRHS right-hand sides.  A is the item's column-major
 // matrix: staged in shared memory by a TMA bulk copy that completes on `bar`
 // (SMEM), or streamed from global memory.
-template <int NRHS, bool SMEM>
+template <int NRHS, bool SMEM, int UC>
 __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
-                                         int lane, const double* A, uint64_t* bar, unsigned parity) {
+                                         int lane, const double* A, uint64_t* bar, unsigned parity,
+                                         unsigned long long& t_gath) {
   constexpr int kCols = kChunkBytes / (8 * NRHS);
-  constexpr int U = (NRHS == 1) ? 16 : 4;  // columns in flight per lane
+  constexpr int U = (NRHS == 1) ? UC : 4;  // columns in flight per lane
   const int m = T.m, ld = T.ld;
 
   // ---- segment table: one segment per lane, column offsets by warp scan
@@ -270,6 +282,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
       for (int j = lane; j < cc; j += 32) w.xs[j] = gather_one<NRHS>(p, w, col + j, 0, k);
       __syncwarp();
       if (SMEM && col == 0) mbar_wait(bar, parity);
+      if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
       const double* Ac = A + (int64_t)col * m;
       int c = g;
       for (; c + 7 * G < cc; c += 8 * G) {
@@ -347,6 +360,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
       }
       __syncwarp();
       if (SMEM && col == 0) mbar_wait(bar, parity);
+      if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u < np) {
@@ -439,6 +453,14 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   int pend = -1;             // near item claimed ahead (slack work, no priority cost)
   int cont = -1;             // continuation (all lanes)
+  // warps allowed to take near-field items (fewer loads in flight lower the
+  // memory latency the far-field chain sees)
+  const int near_lim = (p.flags >> 8) & 0xff;
+  // columns in flight per lane for streamed items: enough to cover the
+  // bandwidth-latency product, and no more (excess requests only queue)
+  const int u_sel = (p.flags >> 16) & 3;
+  const int stream_u = u_sel == 1 ? 16 : (u_sel >= 2 ? 4 : 8);
+  const bool near_ok = near_lim == 0 || wib < near_lim;
   for (;;) {
     int item = cont;
     if (lane == 0 && item < 0) {
@@ -493,11 +515,13 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           break;
         }
         // class-0 static items (up-leaf) before any slack work
-        if (!static_done && !static_lo && (item = take_static()) >= 0) {
+        if (!static_done && !static_lo && near_ok && (item = take_static()) >= 0) {
           if (!static_lo) break;
           pend = item;  // already class 1: keep it for after the slack queue
           item = -1;
         }
+        // coupling rows of inner clusters feed the downward chain level by level
+        if ((p.flags & kFlagSlackFirst) && owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
         // the near item claimed ahead comes before the slack queue: near
         // items are issued longest first, and a long one must not wait
         if (pend >= 0) {
@@ -508,7 +532,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         // coupling rows of inner clusters: the chain needs them level by level
         if (owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
         if (owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) break;
-        if (!static_done && (item = take_static()) >= 0) break;
+        if (!static_done && near_ok && (item = take_static()) >= 0) break;
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
         if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
@@ -524,51 +548,53 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     // claim the next near item ahead, so that the next decision costs no
     // atomic round trip (its result is read after this item)
     unsigned ahead = 0xffffffffu;
-    if (lane == 0 && item >= 0 && pend < 0 && static_lo && !static_done)
+    if (lane == 0 && item >= 0 && pend < 0 && static_lo && !static_done && near_ok)
       ahead = atomicAdd(&ctl->static_head, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
     unsigned long long t_start = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    // Far-field items (the latency-critical chain) are staged whole into
-    // shared memory by one TMA bulk copy, overlapping the source gather;
-    // near-field items stream from global memory with 16 columns in flight.
-    int off = -1;
-    if (lane == 0) {
-      const DTask* t = p.tasks + item;
-      const int kind = __ldg(&t->kind), m = __ldg(&t->m), ld = __ldg(&t->ld), nc = __ldg(&t->ncols);
-      if (kind != h2b::kNear && ld == m && nc > 0) {
-        const double* g0 = p.mat + __ldg(&t->data);
-        const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-        const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)m * nc) + 15) & ~(uintptr_t)15;
-        if (a1 - a0 <= (uintptr_t)kStageBytes) {
-          bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
-          off = (int)(((uintptr_t)g0 - a0) >> 3);
-        }
-      }
-    }
-    off = __shfl_sync(0xffffffffu, off, 0);
+    // descriptor, inline segments and successor range in one round trip
     const DTask T = p.tasks[item];
     DSeg sin{0, 0, 0, 0, 0};
     if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
-    // successor list, fetched now so that its latency hides under the item
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
-    int2 sd_first = make_int2(-1, 0);
+    // Far-field items (the latency-critical chain) are staged whole into
+    // shared memory by one TMA bulk copy, overlapping the source gather;
+    // near-field items stream from global memory with 16 columns in flight.
+    unsigned long long t_desc = 0, t_gath = 0;
+    if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_desc) : "r"(T.kind) : "memory");
+    int off = -1;
+    if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
+      const double* g0 = p.mat + T.data;
+      const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+      const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
+      if (a1 - a0 <= (uintptr_t)kStageBytes) {
+        if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
+        off = (int)(((uintptr_t)g0 - a0) >> 3);
+      }
+    }
+    // successor list (two entries per lane), fetched now so that its latency
+    // hides under the item
+    int2 sd_first = make_int2(-1, 0), sd_second = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
+    if (s0 + 32 + lane < s1) sd_second = __ldg(p.succ + s0 + 32 + lane);
     if (off >= 0) {
-      run_item<NRHS, true>(p, T, sin, w, lane, w.abuf + off, bar, phase);
+      run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
       phase ^= 1u;
+    } else if (stream_u == 4) {
+      run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+    } else if (stream_u == 8) {
+      run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     } else {
-      run_item<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase);
+      run_item<NRHS, false, 16>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
     // the first one itself next and pushes the others.
     __syncwarp();
-    unsigned long long t_run = 0, t_fence = 0;
+    unsigned long long t_run = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_run));
-    fence_acq_rel();
-    if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fence));
     cont = -1;
     for (int k0 = s0; k0 < s1; k0 += 128) {
       // arrival counts of up to 4 x 32 successors in flight at once
@@ -579,9 +605,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
         dd[u] = -1;
         qq[u] = 0;
         if (k < s1) {
-          const int2 sd = (k0 == s0 && u == 0) ? sd_first : __ldg(p.succ + k);
+          const int2 sd = (k0 == s0 && u == 0) ? sd_first
+                          : (k0 == s0 && u == 1) ? sd_second : __ldg(p.succ + k);
           const unsigned ndep = (unsigned)sd.y & 0xffffffu;
-          if (atomicAdd(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
+          if (atom_add_acq_rel(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
           qq[u] = sd.y >> 24;
         }
       }
@@ -615,7 +642,6 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
           cnt[q] += __popc(mask[u][q]);
         }
       if (cnt[0] + cnt[1] + cnt[2] == 0) continue;
-      fence_acq_rel();  // acquire side of the other predecessors' releases
       unsigned base = 0;
       if (lane < kQueues && cnt[lane] > 0) base = atomicAdd(&ctl->tail[lane].v, cnt[lane]);
       unsigned b[kQueues];
@@ -648,12 +674,10 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
       tr[2] = (smid << 32) | (unsigned)(blockIdx.x * nw + wib);
       tr[3] = (unsigned long long)(cont >= 0 ? cont + 1 : 0);
       tr[4] = t_run;
-      tr[5] = t_fence;
+      tr[5] = t_desc;
+      tr[6] = t_gath;
     }
-    if (cont >= 0) {
-      fence_acq_rel();  // acquire side of the other predecessors' releases
-      if (lane == 0) atomicAdd(&ctl->dyn_started, 1u);
-    }
+    if (cont >= 0 && lane == 0) atomicAdd(&ctl->dyn_started, 1u);
     __syncwarp();
   }
   if (lane == 0) {
@@ -707,7 +731,7 @@ struct h2b_op {
   double* d_coef = nullptr;
   int64_t* d_perm = nullptr;
   double* d_xp = nullptr;  // x in tree order
-  int prefetch = 0;
+  int flags = 0;
   std::vector<PhaseDev> ph;
   // multi-GPU
   int rank = 0, world = 1;
@@ -813,7 +837,7 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   p.perm = op->d_perm;
   p.xp = op->d_xp;
   p.y = y;
-  p.prefetch = op->prefetch;
+  p.flags = op->flags;
   const int gi = nrhs_index(NRHS);
   const size_t smem = (size_t)op->wpc * sizeof(WarpSmem);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
@@ -975,7 +999,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
-  op->prefetch = (o && o->l2_prefetch > 0) ? 1 : 0;
+  op->flags = ((o && (o->sched_flags & H2B_SCHED_NEAR_FIRST)) ? 0 : kFlagSlackFirst) |
+              (o ? (o->sched_flags & 0x3ff00) : 0);
   op->rank = P.rank;
   op->world = P.world_size;
   op->exch_off = P.exch_off;

@@ -187,7 +187,7 @@ def describe(op) -> _DescHolder:
     return _DescHolder(op)
 
 
-def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, l2_prefetch=0,
+def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
              rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
@@ -195,7 +195,7 @@ def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max
     o.warps_per_cta = int(warps_per_cta)
     o.ctas_per_sm = int(ctas_per_sm)
     o.max_nrhs = int(max_nrhs)
-    o.l2_prefetch = int(l2_prefetch)
+    o.sched_flags = int(sched_flags)
     o.rank = int(rank)
     o.world_size = int(world_size)
     if nccl_unique_id is not None:

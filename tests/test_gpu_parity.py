@@ -52,7 +52,7 @@ def test_far_and_near_fields_separately(golden):
     assert rel(h2.h2_matvec(near, x), ex["y_near"][:, 0]) <= TOL, name
 
 
-@pytest.mark.parametrize("opts", [dict(task_bytes=512), dict(task_bytes=4096, l2_prefetch=1),
+@pytest.mark.parametrize("opts", [dict(task_bytes=512), dict(task_bytes=4096, sched_flags=1),
                                   dict(warps_per_cta=4, ctas_per_sm=1)])
 def test_plan_variants(opts):
     op, ex = load_golden("config1_sphere4")

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
     ap.add_argument("--grid", default='{"task_bytes":[16384,32768,65536],"interleave":[0,-1]}')
+    ap.add_argument("--flush", action="store_true", help="flush L2 before each timed step")
     ap.add_argument("--ablate", default="", help="comma list of: far (near=[]), near (coupling=[])")
     a = ap.parse_args()
     import torch
@@ -40,6 +41,8 @@ def main():
     x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
     y = torch.empty_like(x)
     s = torch.cuda.current_stream()
+    from bench import DeviceTimer
+    timer = DeviceTimer(s, flush=a.flush)
     ref = None
     for (name, opx), vals in itertools.product(ops.items(), itertools.product(*[grid[k] for k in keys])):
         opts = dict(zip(keys, vals))
@@ -47,13 +50,7 @@ def main():
         st = dev.stats()
         for _ in range(5):
             dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.steps):
-            dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.steps
+        ms = timer.run(lambda: dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream), a.steps)
         yy = y.cpu().numpy()
         if ref is None or name != "full":
             ref = yy if name == "full" or ref is None else ref

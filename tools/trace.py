@@ -41,6 +41,8 @@ def main():
         op = dataclasses.replace(op, near=[])
     elif a.ablate == "near":
         op = dataclasses.replace(op, coupling=[])
+    elif a.ablate == "chain":  # bases and transfers only: the bare tree chain
+        op = dataclasses.replace(op, near=[], coupling=[])
     opts = json.loads(a.opts)
     plan = plan_view(op, **opts)
     dev = DeviceOperator(op, **opts)
@@ -66,16 +68,19 @@ def main():
     end -= t0
     kind = plan["t_kind"]
     dur = end - start
-    t_run = tr[:, 4].astype(np.int64) - t0 - start
-    t_fence = tr[:, 5].astype(np.int64) - tr[:, 4].astype(np.int64)
-    t_succ = tr[:, 1].astype(np.int64) - tr[:, 5].astype(np.int64)
+    # stages: descriptor fetch, gather (+ staged matrix), compute, successors
+    ts = tr[:, 0].astype(np.int64)
+    td, tg, tr_ = (tr[:, j].astype(np.int64) for j in (5, 6, 4))
+    tg = np.where(tg > 0, tg, td)
+    t_desc, t_gath, t_comp = td - ts, tg - td, tr_ - tg
+    t_succ = tr[:, 1].astype(np.int64) - tr_
     nbytes = 8 * plan["t_m"].astype(np.int64) * plan["t_ncols"]
     print(f"items {T}, span {end.max() / 1e3:.1f} us, bytes {nbytes.sum() / 1e6:.1f} MB")
     for k in range(5):
         sel = kind == k
         if sel.any():
             print(f"  {KINDS[k]:8s} n={sel.sum():6d} dur mean {dur[sel].mean() / 1e3:6.2f} us "
-                  f"(run {t_run[sel].mean() / 1e3:5.2f} fence {t_fence[sel].mean() / 1e3:5.2f} succ {t_succ[sel].mean() / 1e3:5.2f})  "
+                  f"(desc {t_desc[sel].mean() / 1e3:5.2f} gath {t_gath[sel].mean() / 1e3:5.2f} comp {t_comp[sel].mean() / 1e3:5.2f} succ {t_succ[sel].mean() / 1e3:5.2f})  "
                   f"p90 {np.percentile(dur[sel], 90) / 1e3:6.2f}  start [{start[sel].min() / 1e3:7.1f}, "
                   f"{start[sel].max() / 1e3:7.1f}]  end max {end[sel].max() / 1e3:7.1f} us  "
                   f"MB {nbytes[sel].sum() / 1e6:7.1f}")
@@ -96,7 +101,7 @@ def main():
         gap = (start[it] - end[pred]) / 1e3 if pred is not None else start[it] / 1e3
         print(f"  {KINDS[kind[it]]:8s} m={plan['t_m'][it]:3d} ncols={plan['t_ncols'][it]:4d} "
               f"ndeps={dep0[it + 1] - dep0[it]:3d} start {start[it] / 1e3:7.1f} dur {dur[it] / 1e3:5.2f} "
-              f"[run {t_run[it] / 1e3:5.2f} fence {t_fence[it] / 1e3:5.2f} succ {t_succ[it] / 1e3:5.2f}] "
+              f"[desc {t_desc[it] / 1e3:5.2f} gath {t_gath[it] / 1e3:5.2f} comp {t_comp[it] / 1e3:5.2f} succ {t_succ[it] / 1e3:5.2f}] "
               f"gap {gap:5.2f} us sm={int(tr[it, 2]) >> 32} cont={int(tr[it, 3]) > 0}")
     # warps busy over time
     bins = np.linspace(0, end.max(), 21)
