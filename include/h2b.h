@@ -93,6 +93,8 @@ typedef struct h2b_options {
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
   int32_t sched_flags;  /* H2B_SCHED_* bits; 0 = default scheduling          */
+  int32_t band_depth;   /* tree levels of the far-field chain one warp runs
+                           back to back (fused runs); 0 = default (1 = none) */
   /* Multi-GPU (one process per GPU).  world_size <= 1: whole operator. */
   int32_t rank;
   int32_t world_size;
@@ -141,6 +143,8 @@ typedef struct h2b_plan_view {
   const int32_t* s_nslots;  /* [nsegs] slots summed (coef)                  */
   const int32_t* s_stride;  /* [nsegs] slot stride (coef)                   */
   const int32_t* deps;      /* [ndeps] task indices, all < dependent        */
+  const int32_t* t_mlen;    /* [ntasks] fused run length at its first item,
+                               0 for the run's other items (1: unfused)     */
 } h2b_plan_view;
 
 int h2b_abi_version(void);

@@ -18,13 +18,13 @@ import numpy as np
 __all__ = ["run_plan", "run_phase", "run_ranks", "check_plan_invariants"]
 
 
-def run_plan(plan: dict, x: np.ndarray) -> np.ndarray:
-    """Single-phase plan: y = M x."""
+def run_plan(plan: dict, x: np.ndarray, rng=None) -> np.ndarray:
+    """Single-phase plan: y = M x (``rng``: random dependency-respecting order)."""
     x = np.asarray(x, dtype=np.float64)
     nrhs = 1 if x.ndim == 1 else x.shape[1]
     coef = np.full((max(1, plan["coef_len"]), nrhs), np.nan)
     Y = np.full((plan["n"], nrhs), np.nan)
-    run_phase(plan, x, coef, Y)
+    run_phase(plan, x, coef, Y, rng=rng)
     return Y[:, 0].copy() if x.ndim == 1 else Y
 
 
@@ -55,15 +55,23 @@ def run_ranks(rank_plans: list, x: np.ndarray) -> np.ndarray:
     return Y[:, 0].copy() if x.ndim == 1 else Y
 
 
-def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray) -> None:
+def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray, rng=None) -> None:
+    """Execute one phase.  Scheduled units are fused runs (t_mlen > 0 at
+    their first item: items t .. t+L-1 run back to back, like one warp of
+    the kernel).  In queue order by default; with ``rng`` in a random
+    dependency-respecting order, as the dynamic scheduler may — inputs a
+    unit does not declare would then read the NaN-initialised workspace."""
     nrhs = coef.shape[1]
     X = np.asarray(x, dtype=np.float64).reshape(plan["n"], nrhs)
     mat, perm = plan["mat"], plan["perm"]
-    done = np.zeros(len(plan["t_m"]), bool)
+    T = len(plan["t_m"])
+    mlen = plan.get("t_mlen")
+    if mlen is None:
+        mlen = np.ones(T, np.int32)
+    done = np.zeros(T, bool)
     t_seg0, t_dep0 = plan["t_seg0"], plan["t_dep0"]
-    for t in range(len(plan["t_m"])):
-        deps = plan["deps"][t_dep0[t]:t_dep0[t + 1]]
-        assert np.all(deps < t) and np.all(done[deps]), "dependency order violated"
+
+    def execute(t):
         m, ld, nc = int(plan["t_m"][t]), int(plan["t_ld"][t]), int(plan["t_ncols"][t])
         src = []
         for s in range(t_seg0[t], t_seg0[t + 1]):
@@ -93,6 +101,34 @@ def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray) -> Non
         else:
             coef[o:o + m] = acc
         done[t] = True
+
+    def run_unit(t):
+        deps = plan["deps"][t_dep0[t]:t_dep0[t + 1]]
+        assert np.all(deps < t) and np.all(done[deps]), "dependency order violated"
+        for j in range(int(mlen[t])):
+            assert j == 0 or (mlen[t + j] == 0 and t_dep0[t + j] == t_dep0[t + j + 1])
+            execute(t + j)
+
+    units = [t for t in range(T) if mlen[t] > 0]
+    assert sum(int(mlen[t]) for t in units) == T, "fused runs must tile the queue"
+    if rng is None:
+        for t in units:
+            run_unit(t)
+        return
+    remaining = {t: int(t_dep0[t + 1] - t_dep0[t]) for t in units}
+    succ = {t: [] for t in units}
+    for t in units:
+        for d in plan["deps"][t_dep0[t]:t_dep0[t + 1]]:
+            succ[int(d)].append(t)
+    ready = [t for t in units if remaining[t] == 0]
+    while ready:
+        t = ready.pop(int(rng.integers(len(ready))))
+        run_unit(t)
+        for s2 in succ[t]:
+            remaining[s2] -= 1
+            if remaining[s2] == 0:
+                ready.append(s2)
+    assert all(done), "some units never became ready"
 
 
 def check_plan_invariants(plan: dict) -> None:

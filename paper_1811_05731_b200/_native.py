@@ -41,7 +41,7 @@ class Desc(C.Structure):
 class Options(C.Structure):
     _fields_ = [
         ("task_bytes", C.c_int64), ("far_task_bytes", C.c_int64), ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
-        ("max_nrhs", C.c_int32), ("sched_flags", C.c_int32),
+        ("max_nrhs", C.c_int32), ("sched_flags", C.c_int32), ("band_depth", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
     ]
 
@@ -71,7 +71,7 @@ class PlanView(C.Structure):
         ("t_m", _p32), ("t_ld", _p32), ("t_ncols", _p32), ("t_kind", _p32),
         ("t_seg0", _p32), ("t_dep0", _p32), ("t_bias_nslots", _p32), ("t_bias_stride", _p32),
         ("s_src", _p64), ("s_ncols", _p32), ("s_kind", _p32), ("s_nslots", _p32),
-        ("s_stride", _p32), ("deps", _p32),
+        ("s_stride", _p32), ("deps", _p32), ("t_mlen", _p32),
     ]
 
 

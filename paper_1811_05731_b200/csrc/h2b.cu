@@ -56,7 +56,9 @@ struct __align__(16) DTask {
   int64_t out;    // coef offset (slot) or tree position (final)
   int64_t bias;   // coef offset or -1
   int32_t m, ld, ncols, kind;
-  int32_t seg0, seg1, dep0, dep1;
+  int32_t seg0, seg1;
+  int32_t mlen;   // fused run length (first item of a run), 0 for its other items
+  int32_t pad_;
   int32_t bias_nslots, bias_stride;
 };
 static_assert(sizeof(DTask) == 64, "DTask layout");
@@ -107,6 +109,7 @@ struct KParams {
   unsigned* ready_flag;                 // per slot: epoch+1 once the id is written
   Ctl* ctl;
   int32_t ntasks;
+  int32_t nnodes;                       // scheduled units (fused runs count once)
   int32_t nready0;
   int32_t nready0_hi;                   // ready0[0:nready0_hi) are class 0
   int32_t flags;                        // kFlag* scheduling switches (h2b_options.sched_flags)
@@ -164,6 +167,10 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 
 // ---- 1-D TMA (cp.async.bulk) staging into shared memory, mbarrier completion
 __device__ __forceinline__ uint32_t smem_u32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
+// L2 prefetch of [a, a + bytes) (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* a, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -447,7 +454,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   //  2. a static item (up-leaf first, then the near field).
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
-  const unsigned n_dynamic = (unsigned)(p.ntasks - p.nready0);
+  const unsigned n_dynamic = (unsigned)(p.nnodes - p.nready0);
   bool static_done = false;  // lane-0 state below
   bool static_lo = false;    // static claims have reached the class-1 (near) part
   int owed = -1;             // claimed dynamic slot whose push is still in flight
@@ -555,39 +562,57 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     unsigned long long t_start = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     // descriptor, inline segments and successor range in one round trip
-    const DTask T = p.tasks[item];
+    DTask T = p.tasks[item];
     DSeg sin{0, 0, 0, 0, 0};
     if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
-    // Far-field items (the latency-critical chain) are staged whole into
-    // shared memory by one TMA bulk copy, overlapping the source gather;
-    // near-field items stream from global memory with 16 columns in flight.
     unsigned long long t_desc = 0, t_gath = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_desc) : "r"(T.kind) : "memory");
-    int off = -1;
-    if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
-      const double* g0 = p.mat + T.data;
+    const int mlen = T.mlen;
+    // a fused run: start the matrices of its later items towards L2 now
+    if (mlen > 1 && lane > 0 && lane < mlen) {
+      const DTask* tj = p.tasks + item + lane;
+      const double* g0 = p.mat + __ldg(&tj->data);
       const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-      const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
-      if (a1 - a0 <= (uintptr_t)kStageBytes) {
-        if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
-        off = (int)(((uintptr_t)g0 - a0) >> 3);
-      }
+      const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)(__ldg(&tj->ncols) - 1) * __ldg(&tj->ld) + __ldg(&tj->m)) + 15) &
+                           ~(uintptr_t)15;
+      if (a1 > a0) prefetch_l2((const void*)a0, (unsigned)(a1 - a0));
     }
     // successor list (two entries per lane), fetched now so that its latency
     // hides under the item
     int2 sd_first = make_int2(-1, 0), sd_second = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (s0 + 32 + lane < s1) sd_second = __ldg(p.succ + s0 + 32 + lane);
-    if (off >= 0) {
-      run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
-      phase ^= 1u;
-    } else if (stream_u == 4) {
-      run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
-    } else if (stream_u == 8) {
-      run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
-    } else {
-      run_item<NRHS, false, 16>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+    for (int j = 0;;) {
+      // Far-field items (the latency-critical chain) are staged whole into
+      // shared memory by one TMA bulk copy, overlapping the source gather;
+      // near-field items stream from global memory.
+      int off = -1;
+      if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
+        const double* g0 = p.mat + T.data;
+        const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+        const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
+        if (a1 - a0 <= (uintptr_t)kStageBytes) {
+          if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
+          off = (int)(((uintptr_t)g0 - a0) >> 3);
+        }
+      }
+      if (off >= 0) {
+        run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
+        phase ^= 1u;
+      } else if (stream_u == 4) {
+        run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+      } else if (stream_u == 8) {
+        run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+      } else {
+        run_item<NRHS, false, 16>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+      }
+      if (++j >= mlen) break;
+      // next item of the fused run: its inputs from this warp's earlier items
+      // are ordered by the warp barrier (same-warp global writes, then .cg reads)
+      __syncwarp();
+      T = p.tasks[item + j];
+      if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)(item + j) * kInlineSegs + lane];
     }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
@@ -705,6 +730,7 @@ int set_error(int code, const std::string& msg) { return fail(code, msg); }
 // One kernel launch worth of device state (a Phase of the plan).
 struct PhaseDev {
   int64_t ntasks = 0;
+  int64_t nnodes = 0;
   DTask* d_tasks = nullptr;
   DSeg* d_segs = nullptr;
   DSeg* d_seg_inline = nullptr;
@@ -741,6 +767,7 @@ struct h2b_op {
   double* d_x = nullptr;
   double* d_y = nullptr;
   size_t xy_cap = 0;
+  cudaStream_t hstream = nullptr;
   std::mutex mu;
   h2b_stats stats{};
 };
@@ -763,6 +790,7 @@ h2b::PlanOptions to_plan_options(const h2b_options* o) {
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
     if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
+    if (o->band_depth > 0) po.band_depth = o->band_depth;
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
   }
@@ -832,6 +860,7 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   p.ctl = F.d_ctl;
   p.trace = F.d_trace;
   p.ntasks = (int32_t)F.ntasks;
+  p.nnodes = (int32_t)F.nnodes;
   p.mat = op->d_mat;
   p.coef = op->d_coef;
   p.perm = op->d_perm;
@@ -909,12 +938,14 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_xp);
+  if (op->hstream) cudaStreamDestroy(op->hstream);
   delete op;
 }
 
 int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   int rc;
   F->ntasks = P.ntasks();
+  F->nnodes = P.nnodes;
   std::vector<DTask> tasks(P.ntasks());
   for (int64_t i = 0; i < P.ntasks(); ++i) {
     DTask& t = tasks[i];
@@ -927,8 +958,8 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
     t.kind = P.t_kind[i];
     t.seg0 = P.t_seg0[i];
     t.seg1 = P.t_seg0[i + 1];
-    t.dep0 = P.t_dep0[i];
-    t.dep1 = P.t_dep0[i + 1];
+    t.mlen = P.t_mlen[i];
+    t.pad_ = 0;
     t.bias_nslots = P.t_bias_nslots[i];
     t.bias_stride = P.t_bias_stride[i];
   }
@@ -1075,6 +1106,7 @@ void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
   v->t_kind = F.t_kind.data();
   v->t_seg0 = F.t_seg0.data();
   v->t_dep0 = F.t_dep0.data();
+  v->t_mlen = F.t_mlen.data();
   v->t_bias_nslots = F.t_bias_nslots.data();
   v->t_bias_stride = F.t_bias_stride.data();
   v->s_src = F.s_src.data();
@@ -1200,17 +1232,22 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
     H2B_CUDA(cudaMalloc(&op->d_y, bytes));
     op->xy_cap = bytes;
   }
-  H2B_CUDA(cudaMemcpy(op->d_x, x_host, bytes, cudaMemcpyHostToDevice));
-  if (op->world > 1) H2B_CUDA(cudaMemset(op->d_y, 0, bytes));
-  int rc = matvec_dev_impl(op, op->d_x, op->d_y, nrhs, nullptr);
+  // one stream: copy in, product, copy out, then a single synchronisation
+  // (a blocking stream: ordered with the legacy default stream, like before)
+  if (!op->hstream) H2B_CUDA(cudaStreamCreate(&op->hstream));
+  cudaStream_t st = op->hstream;
+  H2B_CUDA(cudaMemcpyAsync(op->d_x, x_host, bytes, cudaMemcpyHostToDevice, st));
+  if (op->world > 1) H2B_CUDA(cudaMemsetAsync(op->d_y, 0, bytes, st));
+  int rc = matvec_dev_impl(op, op->d_x, op->d_y, nrhs, st);
   if (rc != H2B_OK) return rc;
   // multi-GPU: every rank wrote its own rows, the others are zero; one sum
   // assembles the full y everywhere (exact: one nonzero term per entry)
   if (op->world > 1) {
     if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
-    H2B_NCCL(ncclAllReduce(op->d_y, op->d_y, (size_t)n * std::max(1, nrhs), ncclDouble, ncclSum, op->comm, nullptr));
+    H2B_NCCL(ncclAllReduce(op->d_y, op->d_y, (size_t)n * std::max(1, nrhs), ncclDouble, ncclSum, op->comm, st));
   }
-  H2B_CUDA(cudaMemcpy(y_host, op->d_y, bytes, cudaMemcpyDeviceToHost));
+  H2B_CUDA(cudaMemcpyAsync(y_host, op->d_y, bytes, cudaMemcpyDeviceToHost, st));
+  H2B_CUDA(cudaStreamSynchronize(st));
   return H2B_OK;
 }
 

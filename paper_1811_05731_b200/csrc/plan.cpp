@@ -11,6 +11,9 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <functional>
+#include <queue>
+#include <unordered_map>
 #include <array>
 #include <cstring>
 #include <numeric>
@@ -560,66 +563,176 @@ int Builder::run(std::string* err) {
 int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char>& in_phase, std::string* err) {
   // queue order: up-leaf, upward levels, downward levels, near field, finals
   // (only the dependency order matters: the kernel schedules dynamically)
-  std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
-    auto key = [&](const TaskTmp& t) {
-      switch (t.kind) {
-        case kUpLeaf: return 0;
-        case kUpNode: return 1 + t.stage;
-        case kDown: return 1000 + t.stage;
-        case kNear: return 2000;
-        default: return 3000;
-      }
-    };
-    return key(tasks_[a]) < key(tasks_[b]);
-  });
+  auto key = [&](int32_t i) {
+    const TaskTmp& t = tasks_[i];
+    switch (t.kind) {
+      case kUpLeaf: return 0;
+      case kUpNode: return 1 + t.stage;
+      case kDown: return 1000 + t.stage;
+      case kNear: return 2000;
+      default: return 3000;
+    }
+  };
+  std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) { return key(a) < key(b); });
   const int32_t T = (int32_t)ids.size();
-  std::vector<int32_t> pos(tasks_.size(), -1);
-  for (int32_t i = 0; i < T; ++i) pos[ids[i]] = i;
+
+  // ---- fused runs of the far-field chain.  The upward items of the clusters
+  // of one band (a cluster whose depth is a multiple of D and its
+  // descendants down to D-1 levels below) run on one warp, deepest first;
+  // so do the transfer pieces of the downward pass, shallowest first.  A
+  // chain of depth L then costs ~L/D scheduling links instead of L.  Both
+  // sets are convex (no path leaves the run and comes back), so a run waits
+  // only for its external inputs.
+  const int D = std::max(1, opt_.band_depth);
+  std::vector<std::vector<int32_t>> runs;  // members (provisional ids) in run order
+  std::vector<int32_t> run_of(tasks_.size(), -1);
+  {
+    std::vector<int64_t> run_key_tab;
+    std::unordered_map<int64_t, int32_t> by_key;
+    for (int32_t i : ids) {
+      const TaskTmp& t = tasks_[i];
+      int dir = -1;
+      if (D > 1) {
+        if (t.kind == kUpLeaf || t.kind == kUpNode) dir = 0;
+        else if (t.kind == kDown && t.qclass == 0) dir = 1;
+      }
+      int32_t r;
+      if (dir < 0) {
+        r = (int32_t)runs.size();
+        runs.emplace_back();
+      } else {
+        int32_t b = t.cl;
+        while (depth_[b] % D != 0) b = parent_[b];
+        const int64_t k = 2 * (int64_t)b + dir;
+        auto it = by_key.find(k);
+        if (it == by_key.end()) {
+          r = (int32_t)runs.size();
+          by_key.emplace(k, r);
+          runs.emplace_back();
+        } else {
+          r = it->second;
+        }
+      }
+      runs[r].push_back(i);
+      run_of[i] = r;
+    }
+    for (auto& R : runs) {
+      if (R.size() < 2) continue;
+      const bool up = tasks_[R[0]].kind == kUpLeaf || tasks_[R[0]].kind == kUpNode;
+      std::stable_sort(R.begin(), R.end(), [&](int32_t a, int32_t b) {
+        return up ? depth_[tasks_[a].cl] > depth_[tasks_[b].cl] : depth_[tasks_[a].cl] < depth_[tasks_[b].cl];
+      });
+    }
+  }
+  // run graph: external dependencies (within this phase), deduplicated
+  const int32_t NR = (int32_t)runs.size();
+  std::vector<std::vector<int32_t>> rdeps(NR);
+  for (int32_t r = 0; r < NR; ++r) {
+    auto& dv = rdeps[r];
+    for (int32_t i : runs[r])
+      for (int32_t dp : tasks_[i].deps) {
+        if (!in_phase[dp]) continue;  // produced before this phase
+        const int32_t q = run_of[dp];
+        if (q < 0) { *err = "internal: dependency outside the phase"; return H2B_EINVAL; }
+        if (q != r) dv.push_back(q);
+      }
+    std::sort(dv.begin(), dv.end());
+    dv.erase(std::unique(dv.begin(), dv.end()), dv.end());
+    // internal dependencies must point backwards in run order
+    std::vector<int32_t> seen;
+    for (int32_t i : runs[r]) {
+      for (int32_t dp : tasks_[i].deps)
+        if (in_phase[dp] && run_of[dp] == r && std::find(seen.begin(), seen.end(), dp) == seen.end()) {
+          *err = "internal: fused run out of dependency order";
+          return H2B_EINVAL;
+        }
+      seen.push_back(i);
+    }
+  }
+  // topological order of the runs (Kahn), by the queue key of their first item
+  std::vector<int32_t> order;
+  {
+    std::vector<int32_t> indeg(NR, 0);
+    std::vector<std::vector<int32_t>> rsucc(NR);
+    for (int32_t r = 0; r < NR; ++r)
+      for (int32_t q : rdeps[r]) { rsucc[q].push_back(r); ++indeg[r]; }
+    std::vector<int32_t> firstpos(NR);
+    {
+      std::vector<int32_t> qpos(tasks_.size(), 0);
+      for (int32_t k = 0; k < T; ++k) qpos[ids[k]] = k;
+      for (int32_t r = 0; r < NR; ++r) {
+        int32_t mn = INT32_MAX;
+        for (int32_t i : runs[r]) mn = std::min(mn, qpos[i]);
+        firstpos[r] = mn;
+      }
+    }
+    using E = std::pair<int32_t, int32_t>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+    for (int32_t r = 0; r < NR; ++r) if (indeg[r] == 0) pq.push({firstpos[r], r});
+    while (!pq.empty()) {
+      const int32_t r = pq.top().second;
+      pq.pop();
+      order.push_back(r);
+      for (int32_t q : rsucc[r]) if (--indeg[q] == 0) pq.push({firstpos[q], q});
+    }
+    if ((int32_t)order.size() != NR) { *err = "internal: cycle among fused runs"; return H2B_EINVAL; }
+  }
+  std::vector<int32_t> lead(NR);  // queue position of each run's first item
+  {
+    int32_t k = 0;
+    for (int32_t r : order) { lead[r] = k; k += (int32_t)runs[r].size(); }
+  }
 
   F->t_data.resize(T); F->t_out.resize(T); F->t_bias.resize(T);
   F->t_m.resize(T); F->t_ld.resize(T); F->t_ncols.resize(T); F->t_kind.resize(T);
   F->t_bias_nslots.resize(T); F->t_bias_stride.resize(T); F->t_qclass.resize(T);
+  F->t_mlen.assign(T, 0);
   F->t_seg0.assign(T + 1, 0); F->t_dep0.assign(T + 1, 0);
-  for (int32_t i = 0; i < T; ++i) {
-    const TaskTmp& t = tasks_[ids[i]];
-    F->t_data[i] = t.data; F->t_out[i] = t.out; F->t_bias[i] = t.bias;
-    F->t_m[i] = t.m; F->t_ld[i] = t.ld; F->t_ncols[i] = t.ncols; F->t_kind[i] = t.kind;
-    F->t_bias_nslots[i] = t.bias_nslots; F->t_bias_stride[i] = t.bias_stride;
-    F->t_qclass[i] = (int8_t)t.qclass;
-    for (int32_t si : t.seg_idx) {
-      F->s_src.push_back(s_src_[si]); F->s_ncols.push_back(s_ncols_[si]); F->s_kind.push_back(s_kind_[si]);
-      F->s_nslots.push_back(s_nslots_[si]); F->s_stride.push_back(s_stride_[si]);
+  F->nnodes = NR;
+  int32_t i = 0;
+  for (int32_t r : order) {
+    for (size_t j = 0; j < runs[r].size(); ++j, ++i) {
+      const TaskTmp& t = tasks_[runs[r][j]];
+      F->t_data[i] = t.data; F->t_out[i] = t.out; F->t_bias[i] = t.bias;
+      F->t_m[i] = t.m; F->t_ld[i] = t.ld; F->t_ncols[i] = t.ncols; F->t_kind[i] = t.kind;
+      F->t_bias_nslots[i] = t.bias_nslots; F->t_bias_stride[i] = t.bias_stride;
+      F->t_qclass[i] = (int8_t)tasks_[runs[r][0]].qclass;
+      for (int32_t si : t.seg_idx) {
+        F->s_src.push_back(s_src_[si]); F->s_ncols.push_back(s_ncols_[si]); F->s_kind.push_back(s_kind_[si]);
+        F->s_nslots.push_back(s_nslots_[si]); F->s_stride.push_back(s_stride_[si]);
+      }
+      if (j == 0) {
+        F->t_mlen[i] = (int32_t)runs[r].size();
+        for (int32_t q : rdeps[r]) {
+          if (lead[q] >= i) { *err = "internal: dependency not earlier in the queue"; return H2B_EINVAL; }
+          F->deps.push_back(lead[q]);
+        }
+      }
+      F->t_seg0[i + 1] = (int32_t)F->s_ncols.size();
+      F->t_dep0[i + 1] = (int32_t)F->deps.size();
+      F->tasks_by_kind[t.kind] += 1;
     }
-    for (int32_t dp : t.deps) {
-      if (!in_phase[dp]) continue;  // produced before this phase
-      const int32_t qd = pos[dp];
-      if (qd < 0 || qd >= i) { *err = "internal: dependency not earlier in the queue"; return H2B_EINVAL; }
-      F->deps.push_back(qd);
-    }
-    F->t_seg0[i + 1] = (int32_t)F->s_ncols.size();
-    F->t_dep0[i + 1] = (int32_t)F->deps.size();
-    F->tasks_by_kind[t.kind] += 1;
   }
   // successor lists for the completion-driven scheduler
   F->succ0.assign(T + 1, 0);
   for (int32_t dp : F->deps) F->succ0[dp + 1] += 1;
-  for (int32_t i = 0; i < T; ++i) F->succ0[i + 1] += F->succ0[i];
+  for (int32_t k = 0; k < T; ++k) F->succ0[k + 1] += F->succ0[k];
   F->succ.assign(F->deps.size(), 0);
   {
     std::vector<int32_t> fill(F->succ0.begin(), F->succ0.end() - 1);
-    for (int32_t i = 0; i < T; ++i)
-      for (int32_t k = F->t_dep0[i]; k < F->t_dep0[i + 1]; ++k) F->succ[fill[F->deps[k]]++] = i;
+    for (int32_t k = 0; k < T; ++k)
+      for (int32_t e = F->t_dep0[k]; e < F->t_dep0[k + 1]; ++e) F->succ[fill[F->deps[e]]++] = k;
   }
-  // initially ready items: class 0 first (up-leaf: they start the far-field
+  // initially ready runs: class 0 first (up-leaf: they start the far-field
   // chain), then the rest (the near field) longest first, so that heavy rows
   // start early and the end of the launch is made of short items
-  for (int32_t i = 0; i < T; ++i)
-    if (F->t_dep0[i + 1] == F->t_dep0[i] && F->t_qclass[i] == 0) F->ready0.push_back(i);
+  for (int32_t k = 0; k < T; ++k)
+    if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] == 0) F->ready0.push_back(k);
   F->n_ready0_hi = (int32_t)F->ready0.size();
   {
     std::vector<int32_t> rest;
-    for (int32_t i = 0; i < T; ++i)
-      if (F->t_dep0[i + 1] == F->t_dep0[i] && F->t_qclass[i] != 0) rest.push_back(i);
+    for (int32_t k = 0; k < T; ++k)
+      if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] != 0) rest.push_back(k);
     std::stable_sort(rest.begin(), rest.end(), [&](int32_t a, int32_t b) {
       return (int64_t)F->t_m[a] * F->t_ncols[a] > (int64_t)F->t_m[b] * F->t_ncols[b];
     });

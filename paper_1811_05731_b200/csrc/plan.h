@@ -46,6 +46,12 @@ struct Phase {
   std::vector<int32_t> t_m, t_ld, t_ncols, t_kind, t_seg0, t_dep0;
   std::vector<int32_t> t_bias_nslots, t_bias_stride;
   std::vector<int8_t> t_qclass;     // 0: far-field chain, 1: inner coupling, 2: leaf coupling / near
+  // Fused runs: item i with t_mlen[i] = L > 0 is scheduled as
+  // one unit that runs items i .. i+L-1 in order on one warp; its deps and
+  // successors are the run's external ones.  t_mlen = 0 marks the members
+  // after the first (never scheduled on their own, no deps of their own).
+  std::vector<int32_t> t_mlen;
+  int64_t nnodes = 0;               // scheduled units (items with t_mlen > 0)
   // segments
   std::vector<int64_t> s_src;
   std::vector<int32_t> s_ncols, s_kind, s_nslots, s_stride;
@@ -87,6 +93,7 @@ struct Plan {
 struct PlanOptions {
   int64_t task_bytes = 65536;     // near-field items (and leaf coupling rows)
   int64_t far_task_bytes = 4096;  // up-leaf, up-node and down items
+  int32_t band_depth = 1;         // tree levels fused into one run of the far-field chain (1: none)
   bool interleave = true;
   int32_t rank = 0;
   int32_t world_size = 1;

@@ -188,7 +188,7 @@ def describe(op) -> _DescHolder:
 
 
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
-             rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
+             band_depth=0, rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
     o.far_task_bytes = int(far_task_bytes)
@@ -196,6 +196,7 @@ def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max
     o.ctas_per_sm = int(ctas_per_sm)
     o.max_nrhs = int(max_nrhs)
     o.sched_flags = int(sched_flags)
+    o.band_depth = int(band_depth)
     o.rank = int(rank)
     o.world_size = int(world_size)
     if nccl_unique_id is not None:
@@ -225,6 +226,7 @@ def _grab_view(v) -> dict:
         "s_src": grab(v.s_src, S, np.int64), "s_ncols": grab(v.s_ncols, S, np.int32),
         "s_kind": grab(v.s_kind, S, np.int32), "s_nslots": grab(v.s_nslots, S, np.int32),
         "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
+        "t_mlen": grab(v.t_mlen, T, np.int32),
     }
 
 
@@ -266,6 +268,15 @@ def plan_view(op, **options) -> dict:
         lib.h2b_plan_destroy(handle)
 
 
+def _pinned_empty(shape) -> np.ndarray:
+    """A fresh float64 host array in page-locked memory, so the product's
+    device-to-host copy is one DMA.  The memory comes from torch's caching
+    host allocator (no cudaHostAlloc per call) and returns to it when the
+    array is released."""
+    import torch
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
 class DeviceOperator:
     """An H² operator resident on the current CUDA device (``h2b_op``)."""
 
@@ -291,7 +302,7 @@ class DeviceOperator:
         """Host arrays in/out: (n,) or (n, nrhs) with nrhs in {1,2,4,8,16}."""
         x = np.ascontiguousarray(x, dtype=np.float64)
         nrhs = 1 if x.ndim == 1 else x.shape[1]
-        y = np.empty_like(x)
+        y = _pinned_empty(x.shape)
         with self._lock:
             nat.check(self._lib.h2b_matvec(self._h, nat.as_d_ptr(x), nat.as_d_ptr(y),
                                            self.n, nrhs), "h2b_matvec")

@@ -61,9 +61,13 @@ def main():
     T = plan["t_m"].size
     tr = np.zeros((T, 8), np.uint64)
     nat.check(lib.h2b_trace_read(dev._h, tr.ctypes.data, T))
+    # one record per scheduled unit (the first item of a fused run)
+    unit = tr[:, 1] > 0
     start = tr[:, 0].astype(np.int64)
     end = tr[:, 1].astype(np.int64)
-    t0 = start.min()
+    t0 = start[unit].min()
+    start[~unit] = t0
+    end[~unit] = t0
     start -= t0
     end -= t0
     kind = plan["t_kind"]
@@ -76,8 +80,11 @@ def main():
     t_succ = tr[:, 1].astype(np.int64) - tr_
     nbytes = 8 * plan["t_m"].astype(np.int64) * plan["t_ncols"]
     print(f"items {T}, span {end.max() / 1e3:.1f} us, bytes {nbytes.sum() / 1e6:.1f} MB")
+    mlen = plan.get("t_mlen", np.ones(T, np.int32))
+    print(f"units {int(unit.sum())}, fused runs {int((mlen > 1).sum())} (mean length "
+          f"{mlen[mlen > 1].mean() if (mlen > 1).any() else 0:.1f})")
     for k in range(5):
-        sel = kind == k
+        sel = (kind == k) & unit
         if sel.any():
             print(f"  {KINDS[k]:8s} n={sel.sum():6d} dur mean {dur[sel].mean() / 1e3:6.2f} us "
                   f"(desc {t_desc[sel].mean() / 1e3:5.2f} gath {t_gath[sel].mean() / 1e3:5.2f} comp {t_comp[sel].mean() / 1e3:5.2f} succ {t_succ[sel].mean() / 1e3:5.2f})  "
@@ -99,7 +106,7 @@ def main():
     print(f"critical path: {len(path)} items")
     for it, pred in path[::-1]:
         gap = (start[it] - end[pred]) / 1e3 if pred is not None else start[it] / 1e3
-        print(f"  {KINDS[kind[it]]:8s} m={plan['t_m'][it]:3d} ncols={plan['t_ncols'][it]:4d} "
+        print(f"  {KINDS[kind[it]]:8s} L={mlen[it]:2d} m={plan['t_m'][it]:3d} ncols={plan['t_ncols'][it]:4d} "
               f"ndeps={dep0[it + 1] - dep0[it]:3d} start {start[it] / 1e3:7.1f} dur {dur[it] / 1e3:5.2f} "
               f"[desc {t_desc[it] / 1e3:5.2f} gath {t_gath[it] / 1e3:5.2f} comp {t_comp[it] / 1e3:5.2f} succ {t_succ[it] / 1e3:5.2f}] "
               f"gap {gap:5.2f} us sm={int(tr[it, 2]) >> 32} cont={int(tr[it, 3]) > 0}")
