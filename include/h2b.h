@@ -81,7 +81,7 @@ typedef struct h2b_desc {
 /* sched_flags bits 8-15: warps per CTA that take near-field items (0: all) */
 #define H2B_SCHED_NEAR_WARPS(k) (((k) & 0xff) << 8)
 /* sched_flags bits 16-17: columns in flight per lane of a streamed item:
-   0 -> 8 (default), 1 -> 16, 2 -> 4 */
+   0 -> 8 (default), 2 -> 4 */
 #define H2B_SCHED_STREAM(s) (((s) & 3) << 16)
 
 /* Execution-plan knobs.  Zero-initialise for defaults. */
@@ -93,8 +93,9 @@ typedef struct h2b_options {
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
   int32_t sched_flags;  /* H2B_SCHED_* bits; 0 = default scheduling          */
-  int32_t band_depth;   /* tree levels of the far-field chain one warp runs
-                           back to back (fused runs); 0 = default (1 = none) */
+  int32_t band_depth;   /* plans only (h2b_plan_create): group D tree levels
+                           of the far-field chain into fused runs; 0/1 = none.
+                           h2b_create rejects D > 1 (measured slower)       */
   /* Multi-GPU (one process per GPU).  world_size <= 1: whole operator. */
   int32_t rank;
   int32_t world_size;

@@ -16,7 +16,8 @@ import numpy as np
 __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
            "KIND_NAMES", "H2BError"]
 
-LIB_PATH = Path(__file__).resolve().parent / "libh2b.so"
+# H2B_LIB: an alternative build of the library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
 H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV = 0, -1, -2, -3, -4, -5
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")

@@ -28,6 +28,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <nccl.h>
@@ -57,8 +58,7 @@ struct __align__(16) DTask {
   int64_t bias;   // coef offset or -1
   int32_t m, ld, ncols, kind;
   int32_t seg0, seg1;
-  int32_t mlen;   // fused run length (first item of a run), 0 for its other items
-  int32_t pad_;
+  int32_t pad0_, pad1_;
   int32_t bias_nslots, bias_stride;
 };
 static_assert(sizeof(DTask) == 64, "DTask layout");
@@ -167,10 +167,6 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 
 // ---- 1-D TMA (cp.async.bulk) staging into shared memory, mbarrier completion
 __device__ __forceinline__ uint32_t smem_u32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
-// L2 prefetch of [a, a + bytes) (16-byte aligned, multiple of 16)
-__device__ __forceinline__ void prefetch_l2(const void* a, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -231,6 +227,111 @@ __device__ __forceinline__ double gather_one(const KParams& p, const WarpSmem& w
   return v;
 }
 
+__device__ __forceinline__ void add_to(double& a, double b) { a += b; }
+__device__ __forceinline__ void add_to(double2& a, double2 b) {
+  a.x += b.x;
+  a.y += b.y;
+}
+
+// Gather the sources of item columns [col, col + cc) (all NRHS values of
+// each) into the warp's staging buffer xs, through the segment table.
+// VW consecutive values (same column, consecutive right-hand sides: they
+// are contiguous in x and in the coefficient slots) per load and UG loads
+// per lane in flight: the first (or only) slot of each is one predicated
+// load -- x through the read-only path (L1 hits across items on the same
+// SM), coefficient slots from L2 -- and split producers' further partial
+// slots are added afterwards in slot order (eight loads in flight), so
+// every value is slot0 + slot1 + ... in a fixed order.
+template <int NRHS>
+__device__ __forceinline__ double gather_one(const KParams& p, const WarpSmem& w, int c, int r, int& k);
+
+template <int NRHS>
+__device__ __forceinline__ void gather_chunk(const KParams& p, WarpSmem& w, int lane, int col, int cc) {
+  if constexpr (NRHS == 1) {
+    // single vector: one value per load, the matrix stream already in flight
+    int k = 0;
+    for (int j = lane; j < cc; j += 32) w.xs[j] = gather_one<1>(p, w, col + j, 0, k);
+    return;
+  }
+  constexpr int VW = NRHS >= 2 ? 2 : 1;
+  constexpr int UG = NRHS >= 16 ? 8 : 4;
+  using V = typename std::conditional<VW == 2, double2, double>::type;
+  const int total = cc * NRHS / VW;
+  int k = 0;  // segment cursor (columns increase along a lane)
+  for (int j0 = lane; j0 < total; j0 += 32 * UG) {
+    V v[UG];
+    const V* q[UG];
+    int ns[UG];
+    bool isx[UG];
+    int64_t st[UG];
+#pragma unroll
+    for (int u = 0; u < UG; ++u) {
+      const int j = (j0 + 32 * u) * VW;
+      const int c = col + j / NRHS, r = j % NRHS;
+      ns[u] = 0;
+      isx[u] = false;
+      q[u] = reinterpret_cast<const V*>(p.coef);
+      st[u] = 0;
+      if (j < total * VW) {
+        while (w.seg_off[k + 1] <= c) ++k;
+        const int64_t e = (w.seg_src[k] + (c - w.seg_off[k])) * NRHS + r;
+        isx[u] = w.seg_kind[k] == h2b::kSegX;
+        q[u] = reinterpret_cast<const V*>((isx[u] ? p.xp : p.coef) + e);
+        ns[u] = isx[u] ? 1 : w.seg_nslots[k];
+        st[u] = (int64_t)w.seg_stride[k] * NRHS / VW;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UG; ++u) {
+      if (ns[u] == 0) v[u] = V{};
+      else v[u] = isx[u] ? __ldg(q[u]) : __ldcg(q[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UG; ++u) {
+      int s = 1;
+      for (; s + 8 <= ns[u]; s += 8) {
+        V t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = __ldcg(q[u] + (int64_t)(s + i) * st[u]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) add_to(v[u], t[i]);
+      }
+      for (; s < ns[u]; ++s) add_to(v[u], __ldcg(q[u] + (int64_t)s * st[u]));
+    }
+    V* xs = reinterpret_cast<V*>(w.xs);
+#pragma unroll
+    for (int u = 0; u < UG; ++u)
+      if (j0 + 32 * u < total) xs[j0 + 32 * u] = v[u];
+  }
+}
+
+// The item's segment table into the warp's shared memory: one segment per
+// lane, column offsets by warp scan.
+__device__ __forceinline__ void load_segtable(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                              int lane) {
+  const int nseg = T.seg1 - T.seg0;  // <= kMaxSegs (planner)
+  int nc = 0;
+  if (lane < nseg) {
+    // items with few segments carry them inline (fetched with the task)
+    const DSeg S = nseg <= kInlineSegs ? sin : p.segs[T.seg0 + lane];
+    nc = S.ncols;
+    w.seg_src[lane] = S.src;
+    w.seg_kind[lane] = S.kind;
+    w.seg_nslots[lane] = S.nslots;
+    w.seg_stride[lane] = S.stride;
+  }
+  int incl = nc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane < nseg) w.seg_off[lane] = incl - nc;
+  if (lane == nseg - 1 || (nseg == 0 && lane == 0)) w.seg_off[nseg] = incl;
+  if (lane == 0 && nseg < h2b::kMaxSegs) w.seg_off[h2b::kMaxSegs] = 0x7fffffff;
+  __syncwarp();
+}
+
 template <bool SMEM>
 __device__ __forceinline__ double ldA(const double* q) {
   if constexpr (SMEM) return *q;
@@ -248,30 +349,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
   constexpr int U = (NRHS == 1) ? UC : 4;  // columns in flight per lane
   const int m = T.m, ld = T.ld;
 
-  // ---- segment table: one segment per lane, column offsets by warp scan
-  {
-    const int nseg = T.seg1 - T.seg0;  // <= kMaxSegs (planner)
-    int nc = 0;
-    if (lane < nseg) {
-      // items with few segments carry them inline (fetched with the task)
-      const DSeg S = nseg <= kInlineSegs ? sin : p.segs[T.seg0 + lane];
-      nc = S.ncols;
-      w.seg_src[lane] = S.src;
-      w.seg_kind[lane] = S.kind;
-      w.seg_nslots[lane] = S.nslots;
-      w.seg_stride[lane] = S.stride;
-    }
-    int incl = nc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane < nseg) w.seg_off[lane] = incl - nc;
-    if (lane == nseg - 1 || (nseg == 0 && lane == 0)) w.seg_off[nseg] = incl;
-    if (lane == 0 && nseg < h2b::kMaxSegs) w.seg_off[h2b::kMaxSegs] = 0x7fffffff;
-    __syncwarp();
-  }
+  load_segtable(p, T, sin, w, lane);
 
   const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
   double acc0[NRHS], acc1[NRHS];
@@ -285,8 +363,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
     const bool v0 = g < G;
     for (int col = 0; col < T.ncols; col += kCols) {
       const int cc = min(kCols, T.ncols - col);
-      int k = 0;
-      for (int j = lane; j < cc; j += 32) w.xs[j] = gather_one<NRHS>(p, w, col + j, 0, k);
+      gather_chunk<NRHS>(p, w, lane, col, cc);
       __syncwarp();
       if (SMEM && col == 0) mbar_wait(bar, parity);
       if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
@@ -360,11 +437,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
         a0[u] = (u < np && v0) ? ld_stream(Ac + (int64_t)u * ld + lane) : 0.0;
         a1[u] = (u < np && v1) ? ld_stream(Ac + (int64_t)u * ld + lane + 32) : 0.0;
       }
-      int k = 0;
-      for (int j = lane; j < cc * NRHS; j += 32) {
-        const int c = j / NRHS, r = j - c * NRHS;
-        w.xs[j] = gather_one<NRHS>(p, w, col + c, r, k);
-      }
+      gather_chunk<NRHS>(p, w, lane, col, cc);
       __syncwarp();
       if (SMEM && col == 0) mbar_wait(bar, parity);
       if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
@@ -431,8 +504,121 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
   }
 }
 
+
+// D(16x8) += A(16x4, row) B(4x8, col) in fp64 on the tensor cores (DMMA).
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// One work item with NRHS = 8 or 16 right-hand sides on the FP64 tensor
+// cores: Y(m x NRHS) = A(m x ncols) X(ncols x NRHS) as 16 x 8 x 4 DMMA tiles.
+// Lane (g = lane/4, t = lane%4) holds A rows g and g+8 of column t of each
+// 16-row tile (eight consecutive doubles per column and tile: coalesced),
+// X row t / column g of each 8-column tile from the gathered sources in
+// shared memory, and accumulator rows g, g+8 / columns 2t, 2t+1.
+template <int NRHS, bool SMEM>
+__device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                             int lane, const double* A, uint64_t* bar, unsigned parity,
+                                             unsigned long long& t_gath) {
+  static_assert(NRHS == 8 || NRHS == 16, "DMMA path: 8 or 16 right-hand sides");
+  constexpr int kCols = kChunkBytes / (8 * NRHS);
+  constexpr int NT = NRHS / 8;  // 8-column tiles
+  constexpr int MT = 4;         // 16-row tiles (m <= 64)
+  const int m = T.m, ld = T.ld;
+  const int mtiles = (m + 15) >> 4;
+  const int g = lane >> 2, t = lane & 3;
+  load_segtable(p, T, sin, w, lane);
+
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  for (int col = 0; col < T.ncols; col += kCols) {
+    const int cc = min(kCols, T.ncols - col);
+    const double* Ac = A + (int64_t)col * ld;
+    // A fragments of the first k-step: streamed ones are issued before the
+    // gather, staged ones read once the bulk copy has landed
+    double a[MT][2];
+    auto load_a0 = [&]() {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = 16 * i + g;
+        const bool ok = i < mtiles && t < cc;
+        a[i][0] = (ok && r < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r) : 0.0;
+        a[i][1] = (ok && r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r + 8) : 0.0;
+      }
+    };
+    if (!SMEM) load_a0();
+    gather_chunk<NRHS>(p, w, lane, col, cc);
+    for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) w.xs[j] = 0.0;  // k padding
+    __syncwarp();
+    if (SMEM && col == 0) mbar_wait(bar, parity);
+    if (SMEM) load_a0();
+    if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
+    for (int c = 0; c < cc; c += 4) {
+      // next k-step's A fragments in flight while this one multiplies
+      double an[MT][2];
+      const int cn = c + 4 + t;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = 16 * i + g;
+        const bool ok = i < mtiles && cn < cc;
+        an[i][0] = (ok && r < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r) : 0.0;
+        an[i][1] = (ok && r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r + 8) : 0.0;
+      }
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = w.xs[(c + t) * NRHS + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (i < mtiles)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        a[i][0] = an[i][0];
+        a[i][1] = an[i][1];
+      }
+    }
+    __syncwarp();
+  }
+
+  // bias slots, then the output rows this lane holds
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    if (i >= mtiles) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 16 * i + g + 8 * h;
+      if (r >= m) continue;
+      double2 v[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) v[j] = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
+      if (T.bias >= 0)
+        for (int s = 0; s < T.bias_nslots; ++s) {
+          const double* bp = p.coef + (T.bias + (int64_t)s * T.bias_stride + r) * NRHS + 2 * t;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const double2 q = __ldcg(reinterpret_cast<const double2*>(bp + 8 * j));
+            v[j].x += q.x;
+            v[j].y += q.y;
+          }
+        }
+      double* dst = T.kind == h2b::kFinal ? p.y + __ldg(p.perm + T.out + r) * NRHS : p.coef + (T.out + r) * NRHS;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) *reinterpret_cast<double2*>(dst + 8 * j + 2 * t) = v[j];
+    }
+  }
+}
+
 template <int NRHS>
-__global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
+__global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -466,7 +652,7 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
   // columns in flight per lane for streamed items: enough to cover the
   // bandwidth-latency product, and no more (excess requests only queue)
   const int u_sel = (p.flags >> 16) & 3;
-  const int stream_u = u_sel == 1 ? 16 : (u_sel >= 2 ? 4 : 8);
+  const int stream_u = u_sel >= 2 ? 4 : 8;
   const bool near_ok = near_lim == 0 || wib < near_lim;
   for (;;) {
     int item = cont;
@@ -562,57 +748,44 @@ __global__ void __launch_bounds__(256, 2) h2b_dataflow_kernel(KParams p) {
     unsigned long long t_start = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     // descriptor, inline segments and successor range in one round trip
-    DTask T = p.tasks[item];
+    const DTask T = p.tasks[item];
     DSeg sin{0, 0, 0, 0, 0};
     if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
     unsigned long long t_desc = 0, t_gath = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_desc) : "r"(T.kind) : "memory");
-    const int mlen = T.mlen;
-    // a fused run: start the matrices of its later items towards L2 now
-    if (mlen > 1 && lane > 0 && lane < mlen) {
-      const DTask* tj = p.tasks + item + lane;
-      const double* g0 = p.mat + __ldg(&tj->data);
-      const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-      const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)(__ldg(&tj->ncols) - 1) * __ldg(&tj->ld) + __ldg(&tj->m)) + 15) &
-                           ~(uintptr_t)15;
-      if (a1 > a0) prefetch_l2((const void*)a0, (unsigned)(a1 - a0));
-    }
     // successor list (two entries per lane), fetched now so that its latency
     // hides under the item
     int2 sd_first = make_int2(-1, 0), sd_second = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (s0 + 32 + lane < s1) sd_second = __ldg(p.succ + s0 + 32 + lane);
-    for (int j = 0;;) {
-      // Far-field items (the latency-critical chain) are staged whole into
-      // shared memory by one TMA bulk copy, overlapping the source gather;
-      // near-field items stream from global memory.
-      int off = -1;
-      if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
-        const double* g0 = p.mat + T.data;
-        const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
-        const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
-        if (a1 - a0 <= (uintptr_t)kStageBytes) {
-          if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
-          off = (int)(((uintptr_t)g0 - a0) >> 3);
-        }
+    // Far-field items (the latency-critical chain) are staged whole into
+    // shared memory by one TMA bulk copy, overlapping the source gather;
+    // near-field items stream from global memory.
+    int off = -1;
+    if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
+      const double* g0 = p.mat + T.data;
+      const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+      const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
+      if (a1 - a0 <= (uintptr_t)kStageBytes) {
+        if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
+        off = (int)(((uintptr_t)g0 - a0) >> 3);
       }
+    }
+    if constexpr (NRHS >= 8) {
       if (off >= 0) {
-        run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
+        run_item_mma<NRHS, true>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
         phase ^= 1u;
-      } else if (stream_u == 4) {
-        run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
-      } else if (stream_u == 8) {
-        run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       } else {
-        run_item<NRHS, false, 16>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+        run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       }
-      if (++j >= mlen) break;
-      // next item of the fused run: its inputs from this warp's earlier items
-      // are ordered by the warp barrier (same-warp global writes, then .cg reads)
-      __syncwarp();
-      T = p.tasks[item + j];
-      if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)(item + j) * kInlineSegs + lane];
+    } else if (off >= 0) {
+      run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
+      phase ^= 1u;
+    } else if (stream_u == 4) {
+      run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+    } else {
+      run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     }
     // publish: outputs visible GPU-wide, then count this item into each
     // successor.  Of the successors whose count this warp completes, it runs
@@ -958,8 +1131,7 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
     t.kind = P.t_kind[i];
     t.seg0 = P.t_seg0[i];
     t.seg1 = P.t_seg0[i + 1];
-    t.mlen = P.t_mlen[i];
-    t.pad_ = 0;
+    t.pad0_ = t.pad1_ = 0;
     t.bias_nslots = P.t_bias_nslots[i];
     t.bias_stride = P.t_bias_stride[i];
   }
@@ -1018,8 +1190,12 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   std::string err;
   int rc = h2b::build_plan(d, to_plan_options(o), &P, &err);
   if (rc != H2B_OK) return fail(rc, err);
-  for (const auto& F : P.ph)
+  for (const auto& F : P.ph) {
     if (F.ntasks() >= INT32_MAX / kQueues) return fail(H2B_EINVAL, "too many work items");
+    if (F.nnodes != F.ntasks())
+      return fail(H2B_EINVAL, "band_depth > 1 (fused runs) is a planning option only: the kernel runs "
+                              "single items (fused runs measured slower on B200, DESIGN.md)");
+  }
 
   std::unique_ptr<h2b_op, void (*)(h2b_op*)> op(new h2b_op(), free_op);
   H2B_CUDA(cudaGetDevice(&op->device));

@@ -64,7 +64,7 @@ def test_plan_variants(opts):
         dev.close()
 
 
-@pytest.mark.parametrize("nrhs", [2, 4, 16])
+@pytest.mark.parametrize("nrhs", [2, 4, 8, 16])
 def test_multi_rhs(nrhs):
     op, ex = load_golden("config1_sphere4")
     X = np.tile(ex["X"], (1, 4))[:, :nrhs]
@@ -83,10 +83,11 @@ def test_random_structures(seed):
     for _ in range(2):
         x = rng.standard_normal(op.n)
         assert rel(h2.h2_matvec(op, x), h2_matvec_ref(op, x)) <= TOL
-    X = rng.standard_normal((op.n, 4))
-    Y = h2.h2_matmat(op, X)
-    for i in range(4):
-        assert rel(Y[:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+    for nrhs in (4, 8, 16):  # CUDA-core path and the DMMA path (8, 16)
+        X = rng.standard_normal((op.n, nrhs))
+        Y = h2.h2_matmat(op, X)
+        for i in range(nrhs):
+            assert rel(Y[:, i], h2_matvec_ref(op, X[:, i])) <= TOL
 
 
 def test_zero_linearity_determinism():
