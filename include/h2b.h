@@ -48,6 +48,7 @@ extern "C" {
 #define H2B_ENCCL (-3)
 #define H2B_ENOMEM (-4)
 #define H2B_ENODEV (-5)
+#define H2B_EIO (-6)     /* corrupt or incompatible operator file (OperatorIOError) */
 
 /* One H2Matrix, as the reference holds it (h2.py:23-42, cluster.py:13-59).
  * Host arrays; they are only read during h2b_create / h2b_plan_create and may
@@ -180,6 +181,23 @@ int h2b_exchange_copy(h2b_op* dst, const h2b_op* src, int nrhs, void* stream);
 int64_t h2b_stream_bytes(const h2b_op* op);
 int h2b_stats_get(const h2b_op* op, h2b_stats* out);
 void h2b_destroy(h2b_op* op);
+
+/* ---- Operator files: the reference's "H2MS" v1 format (persist.py:22-199)
+ * and its CRC-64/XZ (persist.py:24-38; check value 0x995DC9BBDF1939FA for
+ * "123456789").  Errors: H2B_EIO with the reference's OperatorIOError texts. */
+uint64_t h2b_crc64(const void* data, uint64_t len);  /* all host cores above 8 MiB */
+typedef struct h2b_h2ms h2b_h2ms;
+/* Read, verify (checksum first, like load_h2) and parse a file; expected_n < 0
+ * skips the node-count check.  The operator stays in host memory until
+ * h2b_h2ms_close. */
+int h2b_h2ms_open(const char* path, int64_t expected_n, h2b_h2ms** out);
+/* Descriptor view of an opened file (pointers into it): pass to h2b_create. */
+int h2b_h2ms_desc(const h2b_h2ms* f, h2b_desc* out);
+/* Cluster boxes [nclusters*6] (lo xyz, hi xyz) and leaf flags [nclusters]. */
+int h2b_h2ms_tree(const h2b_h2ms* f, double* bbox, uint8_t* leaf);
+void h2b_h2ms_close(h2b_h2ms* f);
+/* save_h2 (persist.py:117-135): the same bytes the reference writes. */
+int h2b_h2ms_write(const h2b_desc* d, const double* bbox, const char* path);
 
 /* Diagnostics: per-work-item timeline of the next products, 8 words per item
  * ({start, end, (smid << 32) | warp, continuation+1, compute done, fence

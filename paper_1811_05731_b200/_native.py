@@ -19,7 +19,7 @@ __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
 # H2B_LIB: an alternative build of the library (A/B timing of kernel variants)
 LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
-H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV = 0, -1, -2, -3, -4, -5
+H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO = 0, -1, -2, -3, -4, -5, -6
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")
 
 _p64 = C.POINTER(C.c_int64)
@@ -108,6 +108,16 @@ def _load():
     lib.h2b_matvec_phase.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.h2b_exchange_region.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), _p64]
     lib.h2b_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.h2b_crc64.argtypes = [C.c_void_p, C.c_uint64]
+    lib.h2b_crc64.restype = C.c_uint64
+    lib.h2b_h2ms_open.argtypes = [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]
+    lib.h2b_h2ms_desc.argtypes = [C.c_void_p, C.POINTER(Desc)]
+    lib.h2b_h2ms_tree.argtypes = [C.c_void_p, _pd, C.POINTER(C.c_uint8)]
+    lib.h2b_h2ms_close.argtypes = [C.c_void_p]
+    lib.h2b_h2ms_close.restype = None
+    lib.h2b_h2ms_write.argtypes = [C.POINTER(Desc), _pd, C.c_char_p]
+    for name in ("h2b_h2ms_open", "h2b_h2ms_desc", "h2b_h2ms_tree", "h2b_h2ms_write"):
+        getattr(lib, name).restype = C.c_int
     for name in ("h2b_plan_create", "h2b_plan_view_get", "h2b_plan_stats", "h2b_create",
                  "h2b_matvec_dev", "h2b_matvec", "h2b_stats_get", "h2b_nccl_unique_id",
                  "h2b_plan_phases", "h2b_plan_phase_view", "h2b_plan_partition", "h2b_matvec_phase",
@@ -132,6 +142,9 @@ def check(rc: int, what: str = "h2b") -> None:
     msg = lib().h2b_last_error().decode(errors="replace")
     if rc == H2B_EINVAL:
         raise ValueError(msg)
+    if rc == H2B_EIO:
+        from .persist import OperatorIOError
+        raise OperatorIOError(msg)
     raise H2BError(f"{what} failed ({rc}): {msg}")
 
 

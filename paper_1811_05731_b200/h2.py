@@ -281,14 +281,24 @@ class DeviceOperator:
     """An H² operator resident on the current CUDA device (``h2b_op``)."""
 
     def __init__(self, op, **options):
-        self.n = int(op.n)
         h = describe(op)
+        self._create(h.desc, options)
+
+    def _create(self, desc, options) -> None:
+        self.n = int(desc.n)
         self._lib = nat.lib()
         handle = C.c_void_p()
         opts = _options(**options)
-        nat.check(self._lib.h2b_create(C.byref(h.desc), C.byref(opts), C.byref(handle)), "h2b_create")
+        nat.check(self._lib.h2b_create(C.byref(desc), C.byref(opts), C.byref(handle)), "h2b_create")
         self._h = handle
         self._lock = threading.Lock()
+
+    @classmethod
+    def from_desc(cls, desc, **options) -> "DeviceOperator":
+        """From a filled ``h2b_desc`` (e.g. an opened H2MS file's)."""
+        self = cls.__new__(cls)
+        self._create(desc, options)
+        return self
 
     def stats(self) -> dict:
         st = nat.Stats()
