@@ -1,0 +1,225 @@
+"""Batched HCA on the GPU: the admissible blocks of a large operator.
+
+The same algorithm as ``hbuild._hca_prepare`` / ``truncate_lowrank``
+(hca.py:38-105, lowrank.py:125-164): per admissible block (t, s), tensor
+Chebyshev grids of both cluster boxes, a fully pivoted cross of the Green's
+function matrix between them (stop when the residual's Frobenius norm drops
+below eps, or the pivot below eps * |S| / size), the interpolation factor
+A = G(x_t, eta_s[sigma]) cross^{-1}, the panel rows B at the pivots (the
+collocation kernel), and the QR/SVD truncation of A B^T.  Here thousands of
+blocks advance together: the crosses as one masked rank-1 update per step on
+a (blocks x 125 x 125) tensor, the solves and truncations as batched
+cuSOLVER calls grouped by cross rank, padded with zero rows.
+
+Results agree with the numpy path to rounding: the residual norms are summed
+in a different order and cuSOLVER factorises differently, so a pivot decision
+or kept rank can differ right at a threshold.  The small operators of the
+parity tests therefore use the numpy path (bit-identical to the reference);
+this one builds the large BASELINE workloads (configs 3-5), whose parity is
+checked product-for-product against the oracle on the very operator built.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = ["hca_gpu"]
+
+_FOUR_PI = 4.0 * math.pi
+_COND_LIMIT = 1e12
+
+
+def _cheb_grid(torch, lo, hi, nodes):
+    """Tensor Chebyshev grids of boxes [lo, hi] (B x 3 each): (B, o^3, 3),
+    ordered like numpy.meshgrid(indexing="ij") (hbuild.chebyshev_points)."""
+    o = nodes.shape[0]
+    ax = 0.5 * (lo + hi)[:, :, None] + 0.5 * (hi - lo)[:, :, None] * nodes  # (B, 3, o)
+    B = lo.shape[0]
+    X = ax[:, 0, :, None, None].expand(B, o, o, o)
+    Y = ax[:, 1, None, :, None].expand(B, o, o, o)
+    Z = ax[:, 2, None, None, :].expand(B, o, o, o)
+    return torch.stack([X, Y, Z], dim=-1).reshape(B, o ** 3, 3)
+
+
+def _green(torch, x, y):
+    """-1 / (4 pi |x - y|) between point sets x (B, m, 3) and y (B, n, 3)."""
+    d = x[:, :, None, :] - y[:, None, :, :]
+    r = torch.sqrt(d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1] + d[..., 2] * d[..., 2])
+    return -1.0 / (_FOUR_PI * r)
+
+
+def _aca_full_batched(torch, S, eps):
+    """Fully pivoted cross of every matrix in S (B, n, n) at once: the pivot
+    rows/columns and the rank of each (lowrank.py:125-150)."""
+    B, n, _ = S.shape
+    res = S.clone()
+    flat = res.view(B, n * n)
+    norm0 = torch.linalg.vector_norm(flat, dim=1)
+    floor = eps * norm0 / math.sqrt(n * n)
+    tau = torch.zeros(B, n, dtype=torch.long, device=S.device)
+    sigma = torch.zeros_like(tau)
+    rank = torch.zeros(B, dtype=torch.long, device=S.device)
+    done = norm0 == 0.0
+    ar = torch.arange(B, device=S.device)
+    for _ in range(n):
+        idx = flat.abs().argmax(dim=1)
+        piv = flat[ar, idx]
+        active = (~done) & (piv.abs() > floor)
+        done = done | ~active
+        if not bool(active.any()):
+            break
+        i, j = idx // n, idx % n
+        tau[ar, rank.clamp(max=n - 1)] = torch.where(active, i, tau[ar, rank.clamp(max=n - 1)])
+        sigma[ar, rank.clamp(max=n - 1)] = torch.where(active, j, sigma[ar, rank.clamp(max=n - 1)])
+        rank = rank + active.long()
+        safe = torch.where(active, piv, torch.ones_like(piv))
+        col = res[ar, :, j] / safe[:, None]
+        row = res[ar, i, :]
+        res -= (col * active[:, None].to(col.dtype))[:, :, None] * row[:, None, :]
+        nrm = torch.linalg.vector_norm(flat, dim=1)
+        done = done | (active & (nrm <= eps * norm0))
+    return tau, sigma, rank
+
+
+def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, batch=4096, device="cuda"):
+    """Low-rank factors (A, B) of the admissible blocks (bt[i], bs[i]).
+
+    Returns a list with, per block, ("ok", A, B) with A (|t| x k), B (|s| x k)
+    truncated numpy arrays, ("zero", None, None) for a zero cross, or
+    ("fallback", None, None) for an ill-conditioned cross (the caller runs
+    the partially pivoted ACA on the block, as hca.py:90-93 does)."""
+    import torch
+    dev = torch.device(device)
+    f64 = torch.float64
+    nb = int(bt.size)
+    out = [None] * nb
+    nodes = torch.from_numpy(np.cos((2.0 * np.arange(order) + 1.0) * np.pi / (2.0 * order))).to(dev)
+    lo_d = torch.from_numpy(np.ascontiguousarray(lo, np.float64)).to(dev)
+    hi_d = torch.from_numpy(np.ascontiguousarray(hi, np.float64)).to(dev)
+    coords_d = torch.from_numpy(np.ascontiguousarray(coords, np.float64)).to(dev)
+    perm_d = torch.from_numpy(np.ascontiguousarray(perm, np.int64)).to(dev)
+    start_d = torch.from_numpy(np.ascontiguousarray(start, np.int64)).to(dev)
+    size = (end - start).astype(np.int64)
+    n3 = order ** 3
+
+    # ---- 1. crosses, in batches of blocks
+    tau_all = np.zeros((nb, n3), np.int64)
+    sig_all = np.zeros((nb, n3), np.int64)
+    rank_all = np.zeros(nb, np.int64)
+    for b0 in range(0, nb, batch):
+        sl = slice(b0, min(nb, b0 + batch))
+        t = torch.from_numpy(bt[sl]).to(dev)
+        s = torch.from_numpy(bs[sl]).to(dev)
+        et = _cheb_grid(torch, lo_d[t], hi_d[t], nodes)
+        es = _cheb_grid(torch, lo_d[s], hi_d[s], nodes)
+        S = _green(torch, et, es)
+        if not bool(torch.isfinite(S).all()):
+            raise ValueError("Green's function is singular at coincident points")
+        tau, sig, rk = _aca_full_batched(torch, S, eps)
+        tau_all[sl] = tau.cpu().numpy()
+        sig_all[sl] = sig.cpu().numpy()
+        rank_all[sl] = rk.cpu().numpy()
+        del S, et, es
+    for i in np.flatnonzero(rank_all == 0):
+        out[i] = ("zero", None, None)
+
+    # ---- 2. per cross rank k: condition check, A by one batched solve,
+    # pivot points for the panel rows of B
+    ok_ids, pts_list, a_parts = [], [], {}
+    for k in np.unique(rank_all[rank_all > 0]):
+        k = int(k)
+        ids = np.flatnonzero(rank_all == k)
+        ids = ids[np.argsort(size[bt[ids]], kind="stable")]   # similar |t| per chunk
+        per = max(1, int(2e8 // max(1, 8 * k * int(size[bt[ids]].max()))))
+        for c0 in range(0, ids.size, per):
+            cid = ids[c0:c0 + per]
+            t = torch.from_numpy(bt[cid]).to(dev)
+            s = torch.from_numpy(bs[cid]).to(dev)
+            tau = torch.from_numpy(tau_all[cid, :k]).to(dev)
+            sig = torch.from_numpy(sig_all[cid, :k]).to(dev)
+            et = _cheb_grid(torch, lo_d[t], hi_d[t], nodes)
+            es = _cheb_grid(torch, lo_d[s], hi_d[s], nodes)
+            pt = torch.gather(et, 1, tau[:, :, None].expand(-1, -1, 3))     # eta_t[tau]
+            ps = torch.gather(es, 1, sig[:, :, None].expand(-1, -1, 3))     # eta_s[sigma]
+            cross = _green(torch, pt, ps)                                    # (B, k, k)
+            sv = torch.linalg.svdvals(cross)
+            cond = sv[:, 0] / sv[:, -1]
+            bad = ~(cond <= _COND_LIMIT)
+            # rows of t: coordinates of the cluster's nodes, padded far away
+            M = int(size[bt[cid]].max())
+            r = torch.arange(M, device=dev)
+            st = start_d[t]
+            valid = r[None, :] < torch.from_numpy(size[bt[cid]]).to(dev)[:, None]
+            pos = torch.where(valid, st[:, None] + r[None, :], st[:, None])
+            x = coords_d[perm_d[pos]]
+            x = torch.where(valid[:, :, None], x, torch.full_like(x, 1e6))
+            g = _green(torch, x, ps)                                          # (B, M, k)
+            safe = torch.where(bad[:, None, None], torch.eye(k, dtype=f64, device=dev).expand_as(cross), cross)
+            a = torch.linalg.solve(safe.transpose(1, 2), g.transpose(1, 2)).transpose(1, 2)  # a cross = g
+            a = a * valid[:, :, None]
+            bad_h = bad.cpu().numpy()
+            a_h = a.cpu().numpy()
+            pt_h = pt.cpu().numpy()
+            for q, bi in enumerate(cid):
+                if bad_h[q]:
+                    out[bi] = ("fallback", None, None)
+                    continue
+                ok_ids.append(int(bi))
+                a_parts[int(bi)] = a_h[q, :size[bt[bi]]]
+                pts_list.append(pt_h[q])
+    if not ok_ids:
+        return out
+
+    # ---- 3. B = panel rows at the pivots (bem.py:207-219), one kernel batch
+    ok = np.array(ok_ids, np.int64)
+    kk = rank_all[ok]
+    s_cl = bs[ok]
+    ncol = size[s_cl]
+    job_cnt = np.repeat(ncol, kk)
+    pts = np.concatenate(pts_list)
+    job_cb = np.repeat(start[s_cl], kk)
+    job_off = np.zeros(job_cnt.size + 1, np.int64)
+    np.cumsum(job_cnt, out=job_off[1:])
+    bflat = evaluator.rows(pts, job_cb, job_cnt.astype(np.int32), np.full(job_cnt.size, -1, np.int64),
+                           job_off[:-1], perm, int(job_off[-1]))
+    blk_off = np.zeros(ok.size + 1, np.int64)
+    np.cumsum(kk * ncol, out=blk_off[1:])
+
+    # ---- 4. truncation A B^T -> (Q_a U S, Q_b V) with s > eps * s0, batched per k
+    for k in np.unique(kk):
+        k = int(k)
+        sel = np.flatnonzero(kk == k)
+        sel = sel[np.argsort(size[bt[ok[sel]]] + size[s_cl[sel]], kind="stable")]
+        Mt_all, Ms_all = size[bt[ok[sel]]], ncol[sel]
+        per = max(1, int(2e8 // max(1, 8 * k * int(max(Mt_all.max(), Ms_all.max())))))
+        for c0 in range(0, sel.size, per):
+            qs = sel[c0:c0 + per]
+            Mt, Ms = int(size[bt[ok[qs]]].max()), int(ncol[qs].max())
+            A = np.zeros((qs.size, Mt, k))
+            Bm = np.zeros((qs.size, Ms, k))
+            for j, q in enumerate(qs):
+                a = a_parts[int(ok[q])]
+                A[j, :a.shape[0]] = a
+                m = int(ncol[q])
+                Bm[j, :m] = bflat[blk_off[q]: blk_off[q + 1]].reshape(k, m).T
+            Ad = torch.from_numpy(A).to(dev)
+            Bd = torch.from_numpy(Bm).to(dev)
+            qa, ra = torch.linalg.qr(Ad)
+            qb, rb = torch.linalg.qr(Bd)
+            u, sv, vh = torch.linalg.svd(ra @ rb.transpose(1, 2))
+            keep = (sv > eps * sv[:, :1]).sum(dim=1)
+            keep = torch.where(sv[:, 0] == 0.0, torch.zeros_like(keep), keep)
+            # (clusters smaller than the cross rank: reduced QR factors are
+            # min(|t|, k) wide, like numpy's)
+            mask = (torch.arange(sv.shape[1], device=dev)[None, :] < keep[:, None]).to(f64)
+            a2 = qa @ (u * (sv * mask)[:, None, :])
+            b2 = qb @ (vh.transpose(1, 2) * mask[:, None, :])
+            a2h, b2h, kh = a2.cpu().numpy(), b2.cpu().numpy(), keep.cpu().numpy()
+            for j, q in enumerate(qs):
+                kq = int(kh[j])
+                mt, ms = int(size[bt[ok[q]]]), int(ncol[q])
+                out[int(ok[q])] = ("ok", np.ascontiguousarray(a2h[j, :mt, :kq]),
+                                   np.ascontiguousarray(b2h[j, :ms, :kq]))
+    return out

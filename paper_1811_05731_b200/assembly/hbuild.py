@@ -401,9 +401,16 @@ def _map(fn, items, workers, chunksize=64):
 
 
 def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(), *,
-                evaluator=None, workers: int | None = None, log=None) -> tuple[H2Matrix, BuildReport]:
+                evaluator=None, workers: int | None = None, log=None,
+                backend: str = "numpy", device: str = "cuda") -> tuple[H2Matrix, BuildReport]:
     """Build the compressed operator M = K + D of ``surface`` as an H2Matrix
-    (``hmatrix.assemble_operator(mesh, "h2", config).payload``)."""
+    (``hmatrix.assemble_operator(mesh, "h2", config).payload``).
+
+    backend "numpy": the reference's operation order (bit-identical
+    operators, tests/test_builder.py).  backend "gpu": the admissible blocks
+    by batched HCA on the GPU (assembly/gpu_hca.py) and Gram-based bases in
+    the recompression -- the same algorithm to rounding, for the large
+    BASELINE workloads."""
     say = log or (lambda *a: None)
     times = {}
     t0 = time.perf_counter()
@@ -453,6 +460,45 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
     _G.clear()
     _G.update(bt=bt[adm_ids], bs=bs[adm_ids], lo=lo, hi=hi, start=start, end=end, perm=perm,
               coords=coords, order=config.cheb_order, eps=config.eps)
+    weights = None
+    if backend == "gpu" and config.method == "hca":
+        from .gpu_hca import hca_gpu
+        res = hca_gpu(bt=bt[adm_ids], bs=bs[adm_ids], lo=lo, hi=hi, start=start, end=end, perm=perm,
+                      coords=coords, order=config.cheb_order, eps=config.eps, evaluator=evaluator,
+                      device=device)
+        times["hca_gpu"] = time.perf_counter() - t2
+        lowrank, weights, n_fb = [None] * adm_ids.size, [None] * adm_ids.size, 0
+        for i, (st, a, b) in enumerate(res):
+            t_c, s_c = int(bt[adm_ids[i]]), int(bs[adm_ids[i]])
+            if st == "ok":
+                lowrank[i] = (a, b)
+                # a = Q_a U S, b = Q_b V: B^T B = I, A^T A = S^2 (see recompress)
+                sv = np.linalg.norm(a, axis=0)
+                weights[i] = (np.eye(a.shape[1]), np.diag(sv))
+                continue
+            if st == "zero":
+                lowrank[i] = (np.zeros((end[t_c] - start[t_c], 0)), np.zeros((end[s_c] - start[s_c], 0)))
+            else:
+                warnings.warn("ill-conditioned interpolation cross; falling back to ACA", RuntimeWarning)
+                n_fb += 1
+                lowrank[i] = _aca_block(evaluator, coords, perm, start, end, t_c, s_c, config.eps)
+            aa, bb = lowrank[i]
+            weights[i] = (np.linalg.qr(bb)[1], np.linalg.qr(aa)[1])
+        say(f"HCA (gpu): {adm_ids.size} blocks, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s)")
+        t5 = time.perf_counter()
+        from .recompress import recompress
+        op = recompress(tree, surface.n,
+                        [(int(bt[adm_ids[i]]), int(bs[adm_ids[i]]), lowrank[i][0], lowrank[i][1])
+                         for i in range(adm_ids.size)],
+                        [(int(dt[i]), int(ds[i]), near_mats[i]) for i in range(dense_ids.size)],
+                        config.eps_rec, workers=workers, weights=weights)
+        times["recompress"] = time.perf_counter() - t5
+        times["total"] = time.perf_counter() - t0
+        say(f"recompress {times['recompress']:.1f}s; H² {op.storage_bytes() / 1e6:.1f} MB; "
+            f"total {times['total']:.1f}s")
+        rep = BuildReport(n=surface.n, nclusters=len(cl), n_admissible=int(adm_ids.size),
+                          n_dense=int(dense_ids.size), n_fallback=n_fb, seconds=times)
+        return op, rep
     if config.method == "hca":
         prep = _map(_hca_prepare, list(range(adm_ids.size)), workers)
     else:

@@ -37,9 +37,25 @@ def _truncated_basis(z: np.ndarray, eps: float) -> np.ndarray:
     return u[:, : int(np.sum(s > eps * s[0]))]
 
 
+def _truncated_basis_gram(z: np.ndarray, eps: float) -> np.ndarray:
+    """The same subspace from the Gram matrix z z^T (rows <= ~100, columns
+    up to thousands): eigenvalues are the squared singular values, so the
+    cut s > eps * s0 is lambda > eps^2 * lambda0.  Used for large operators
+    (fast build); equal to the SVD's basis up to rounding and column signs."""
+    if z.shape[1] == 0 or z.shape[0] == 0:
+        return np.zeros((z.shape[0], 0))
+    lam, v = np.linalg.eigh(z @ z.T)
+    lam, v = lam[::-1], v[:, ::-1]
+    if lam[0] <= 0.0:
+        return np.zeros((z.shape[0], 0))
+    keep = int(np.sum(np.sqrt(np.maximum(lam, 0.0)) > eps * np.sqrt(lam[0])))
+    return np.ascontiguousarray(v[:, :keep])
+
+
 class _Side:
-    def __init__(self, eps):
+    def __init__(self, eps, fast=False):
         self.eps = eps
+        self.tb = _truncated_basis_gram if fast else _truncated_basis
         self.basis, self.transfer, self.explicit = {}, {}, {}
 
     def combine(self, c, current, kids):
@@ -52,7 +68,7 @@ class _Side:
             for ch, v in zip(c.children, kids):
                 proj.append(v.T @ z[off: off + ch.size])
                 off += ch.size
-            vhat = _truncated_basis(np.vstack(proj), self.eps)
+            vhat = self.tb(np.vstack(proj), self.eps)
         else:
             vhat = np.zeros((sum(v.shape[1] for v in kids), 0))
         parts, off = [], 0
@@ -69,7 +85,7 @@ class _Side:
         current = inherited + own.get(c.cid, [])
         if c.is_leaf:
             pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
-            v = _truncated_basis(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), self.eps)
+            v = self.tb(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), self.eps)
             self.basis[c.cid] = v
             self.explicit[c.cid] = v
             return v
@@ -77,10 +93,10 @@ class _Side:
         return self.combine(c, current, kids)
 
 
-def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0):
+def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0, fast: bool = False):
     """One side of the nested basis.  ``anchored[cid]`` lists (factor,
     weight) of the blocks whose cluster on this side is ``cid``."""
-    side = _Side(eps)
+    side = _Side(eps, fast)
     items = [(cid, f, w) for cid, lst in anchored.items() for f, w in lst]
     mats = list(pool.map(lambda t: t[1] @ t[2].T, items)) if pool else [f @ w.T for _, f, w in items]
     own: dict = {}
@@ -109,9 +125,14 @@ def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0
     return side.basis, side.transfer, side.explicit
 
 
-def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers: int = 1) -> H2Matrix:
+def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers: int = 1,
+               weights: list | None = None) -> H2Matrix:
     """``lowrank``: (row cid, col cid, A, B) with block = A @ B.T, in leaf-
-    block order; ``dense``: (row cid, col cid, matrix)."""
+    block order; ``dense``: (row cid, col cid, matrix).
+
+    ``weights`` (fast build of large operators): per low-rank block the
+    pair (W_b, W_a) with W^T W = B^T B and A^T A, replacing the QR R factors
+    (only R^T R enters the bases); bases then come from Gram matrices."""
     if eps_rec < 0.0:
         raise ValueError("epsilon_rec must be >= 0")
     pool = None
@@ -124,21 +145,26 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
             limiter = None
         pool = ThreadPoolExecutor(max_workers=workers)
     try:
-        nz = [(t, s, a, b) for t, s, a, b in lowrank if a.shape[1] > 0]
+        fast = weights is not None
+        keep_ids = [i for i, (t, s, a, b) in enumerate(lowrank) if a.shape[1] > 0]
+        nz = [lowrank[i] for i in keep_ids]
 
         def qr_r(t):
             _, _, a, b = t
             return np.linalg.qr(b)[1], np.linalg.qr(a)[1]
 
-        rs = list(pool.map(qr_r, nz)) if pool else [qr_r(t) for t in nz]
+        if fast:
+            rs = [weights[i] for i in keep_ids]
+        else:
+            rs = list(pool.map(qr_r, nz)) if pool else [qr_r(t) for t in nz]
         rows: dict = {}
         cols: dict = {}
         for (t, s, a, b), (rb, ra) in zip(nz, rs):
             rows.setdefault(t, []).append((a, rb))
             cols.setdefault(s, []).append((b, ra))
         depth = max(1, int(np.ceil(np.log2(max(2, 4 * workers))))) if pool else 0
-        rbasis, rtrans, rexp = basis_side(tree, rows, eps_rec, pool, depth)
-        cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec, pool, depth)
+        rbasis, rtrans, rexp = basis_side(tree, rows, eps_rec, pool, depth, fast)
+        cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec, pool, depth, fast)
         op = H2Matrix(tree=tree, n=n, row_basis=rbasis, row_transfer=rtrans,
                       col_basis=cbasis, col_transfer=ctrans)
 

@@ -32,11 +32,11 @@ WORKLOADS = {
     "config3": dict(desc="thin disk r=1 t=0.05, jittered Delaunay faces + structured rim (N=1040147), "
                          "leaf 64, eta 2, order 5",
                     surface=lambda: G.disk_surface(0.00252),
-                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5), backend="gpu"),
     "config5": dict(desc="icosphere level 10 decimated to 4194304 nodes, convex-hull re-triangulated, "
                          "leaf 64, eta 2, order 5",
                     surface=lambda: G.sphere_subsample_surface(10, 4_194_304),
-                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5)),
+                    cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5), backend="gpu"),
     # small variants for tests and quick runs
     "cube40": dict(desc="cube [-1,1]^3, 40x40 quads/face (N=9602), leaf 64, eta 2, order 5",
                    surface=lambda: G.cube_surface(40),
@@ -56,7 +56,8 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     """Build (or load from ``cache_dir``) the H² operator of a workload.
     The cache only saves build time; it is keyed by the workload recipe."""
     w = WORKLOADS[name]
-    key = hashlib.sha256(repr((name, w["desc"], w["cfg"], 1)).encode()).hexdigest()[:16]
+    backend = w.get("backend", "numpy")
+    key = hashlib.sha256(repr((name, w["desc"], w["cfg"], 1, backend)).encode()).hexdigest()[:16]
     path = Path(cache_dir) / f"h2b_{name}_{key}.npz" if cache_dir else None
     if path is not None and path.exists():
         from .io import load_npz
@@ -67,7 +68,8 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     t = time.perf_counter()
     surf = w["surface"]()
     log(f"[workload] {name}: surface N={surf.n} T={surf.triangles.shape[0]} ({time.perf_counter() - t:.1f}s)")
-    op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"))
+    op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"),
+                          backend=backend)
     info = {"cached": False, "n": surf.n, "build_seconds": rep.seconds, "n_admissible": rep.n_admissible,
             "n_dense": rep.n_dense, "n_fallback": rep.n_fallback}
     if path is not None:

@@ -112,3 +112,35 @@ def test_gpu_built_operator_matches_reference(name):
     # entries differ from the reference only by rounding: same accuracy
     for i in range(3):
         assert rel(h2_matvec_ref(op, ex["X"][:, i]), ex["y_full"][:, i]) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["sphere3_l32_eta2_o4", "torus_32_16_4_default"])
+def test_batched_hca_backend_same_operator_to_compression_accuracy(name):
+    """backend="gpu" (batched HCA, Gram-based bases; run here on torch's CPU
+    device) builds the same operator as the reference up to rounding at the
+    truncation thresholds: same blocks, products within the compression
+    accuracy of each other and of the dense operator."""
+    ref, ex = load_golden(name)
+    op, rep = assemble_h2(_surface(ex), _cfg(ex), evaluator=CpuCollocation, workers=2, backend="gpu",
+                          device="cpu")
+    assert [(a, b) for a, b, _ in op.coupling] == [(a, b) for a, b, _ in ref.coupling]
+    assert [(a, b) for a, b, _ in op.near] == [(a, b) for a, b, _ in ref.near]
+    assert abs(op.storage_bytes() - ref.storage_bytes()) <= 0.02 * ref.storage_bytes()
+    for i in range(3):
+        y = h2_matvec_ref(op, ex["X"][:, i])
+        assert rel(y, ex["y_full"][:, i]) <= 1e-4
+        assert rel(y, ex["y_dense"][:, i]) <= 2.0 * rel(ex["y_full"][:, i], ex["y_dense"][:, i]) + 1e-5
+
+
+@pytest.mark.gpu
+def test_batched_hca_on_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ref, ex = load_golden("config1_sphere4")
+    op, rep = assemble_h2(_surface(ex), _cfg(ex), workers=4, backend="gpu")
+    assert [(a, b) for a, b, _ in op.coupling] == [(a, b) for a, b, _ in ref.coupling]
+    for i in range(3):
+        y = h2_matvec_ref(op, ex["X"][:, i])
+        assert rel(y, ex["y_full"][:, i]) <= 1e-4
+        assert rel(y, ex["y_dense"][:, i]) <= 2.0 * rel(ex["y_full"][:, i], ex["y_dense"][:, i]) + 1e-5
