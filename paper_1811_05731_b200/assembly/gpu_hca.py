@@ -8,8 +8,10 @@ below eps, or the pivot below eps * |S| / size), the interpolation factor
 A = G(x_t, eta_s[sigma]) cross^{-1}, the panel rows B at the pivots (the
 collocation kernel), and the QR/SVD truncation of A B^T.  Here thousands of
 blocks advance together: the crosses as one masked rank-1 update per step on
-a (blocks x 125 x 125) tensor, the solves and truncations as batched
-cuSOLVER calls grouped by cross rank, padded with zero rows.
+a (blocks x 125 x 125) tensor, the solves as batched cuSOLVER calls grouped by
+cross rank (padded with zero rows), and the QR/SVD truncations as stacked
+LAPACK calls on the host threads (cuSOLVER's batched QR and its SVDs above
+32 x 32 run one matrix at a time).
 
 Results agree with the numpy path to rounding: the residual norms are summed
 in a different order and cuSOLVER factorises differently, so a pivot decision
@@ -29,6 +31,30 @@ __all__ = ["hca_gpu"]
 
 _FOUR_PI = 4.0 * math.pi
 _COND_LIMIT = 1e12
+
+
+def _host_pool_map(fn, items):
+    """fn over items on the host cores (numpy's stacked LAPACK loops release
+    the GIL), one BLAS thread each."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:
+        lim = None
+    try:
+        with ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1))) as ex:
+            return list(ex.map(fn, items))
+    finally:
+        if lim is not None:
+            lim.restore_original_limits()
+
+
+def _host_map(fn, stack, chunk=512):
+    """fn over a stacked array in chunks on the host cores, concatenated."""
+    parts = [stack[i:i + chunk] for i in range(0, stack.shape[0], chunk)]
+    return np.concatenate(_host_pool_map(fn, parts))
 
 
 def _cheb_grid(torch, lo, hi, nodes):
@@ -83,15 +109,26 @@ def _aca_full_batched(torch, S, eps):
     return tau, sigma, rank
 
 
-def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, batch=4096, device="cuda"):
+def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, batch=4096, device="cuda",
+            times=None):
     """Low-rank factors (A, B) of the admissible blocks (bt[i], bs[i]).
 
     Returns a list with, per block, ("ok", A, B) with A (|t| x k), B (|s| x k)
     truncated numpy arrays, ("zero", None, None) for a zero cross, or
     ("fallback", None, None) for an ill-conditioned cross (the caller runs
     the partially pivoted ACA on the block, as hca.py:90-93 does)."""
+    import time
     import torch
     dev = torch.device(device)
+    times = {} if times is None else times
+
+    def lap(name, t0):
+        if dev.type == "cuda":
+            torch.cuda.synchronize()
+        times[name] = times.get(name, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
+
+    t0 = time.perf_counter()
     f64 = torch.float64
     nb = int(bt.size)
     out = [None] * nb
@@ -124,6 +161,7 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
         del S, et, es
     for i in np.flatnonzero(rank_all == 0):
         out[i] = ("zero", None, None)
+    t0 = lap("cross", t0)
 
     # ---- 2. per cross rank k: condition check, A by one batched solve,
     # pivot points for the panel rows of B
@@ -144,7 +182,13 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
             pt = torch.gather(et, 1, tau[:, :, None].expand(-1, -1, 3))     # eta_t[tau]
             ps = torch.gather(es, 1, sig[:, :, None].expand(-1, -1, 3))     # eta_s[sigma]
             cross = _green(torch, pt, ps)                                    # (B, k, k)
-            sv = torch.linalg.svdvals(cross)
+            # cuSOLVER's batched SVD only covers k <= 32; larger crosses go
+            # through LAPACK on the host (stacked, GIL released)
+            if k <= 32:
+                sv = torch.linalg.svdvals(cross)
+            else:
+                sv = torch.from_numpy(_host_map(lambda m: np.linalg.svd(m, compute_uv=False),
+                                                cross.cpu().numpy())).to(dev)
             cond = sv[:, 0] / sv[:, -1]
             bad = ~(cond <= _COND_LIMIT)
             # rows of t: coordinates of the cluster's nodes, padded far away
@@ -169,6 +213,7 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
                 ok_ids.append(int(bi))
                 a_parts[int(bi)] = a_h[q, :size[bt[bi]]]
                 pts_list.append(pt_h[q])
+    t0 = lap("solve", t0)
     if not ok_ids:
         return out
 
@@ -186,16 +231,35 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
                            job_off[:-1], perm, int(job_off[-1]))
     blk_off = np.zeros(ok.size + 1, np.int64)
     np.cumsum(kk * ncol, out=blk_off[1:])
+    t0 = lap("rows", t0)
 
-    # ---- 4. truncation A B^T -> (Q_a U S, Q_b V) with s > eps * s0, batched per k
+    # ---- 4. truncation A B^T -> (Q_a U S, Q_b V) with s > eps * s0
+    # (truncate_lowrank), stacked per cross rank k: LAPACK on the host
+    # threads (cuSOLVER's batched QR/SVD are per-matrix loops at these sizes)
+    def trunc(args):
+        A, Bm = args
+        qa, ra = np.linalg.qr(A)
+        qb, rb = np.linalg.qr(Bm)
+        u, sv, vh = np.linalg.svd(ra @ np.swapaxes(rb, 1, 2))
+        keep = (sv > eps * sv[:, :1]).sum(axis=1)
+        keep[sv[:, 0] == 0.0] = 0
+        mask = np.arange(sv.shape[1])[None, :] < keep[:, None]
+        a2 = qa @ (u * (sv * mask)[:, None, :])
+        b2 = qb @ (np.swapaxes(vh, 1, 2) * mask[:, None, :])
+        return a2, b2, keep
+
+    jobs, metas = [], []
     for k in np.unique(kk):
         k = int(k)
         sel = np.flatnonzero(kk == k)
         sel = sel[np.argsort(size[bt[ok[sel]]] + size[s_cl[sel]], kind="stable")]
-        Mt_all, Ms_all = size[bt[ok[sel]]], ncol[sel]
-        per = max(1, int(2e8 // max(1, 8 * k * int(max(Mt_all.max(), Ms_all.max())))))
-        for c0 in range(0, sel.size, per):
-            qs = sel[c0:c0 + per]
+        rows = np.maximum(size[bt[ok[sel]]], ncol[sel])  # ascending
+        c0 = 0
+        while c0 < sel.size:
+            # at most 1024 blocks and ~64 MB of padded factors per job
+            cnt = int(min(1024, max(1, (64 << 20) // (16 * k * int(rows[min(sel.size, c0 + 1024) - 1])))))
+            qs = sel[c0:c0 + cnt]
+            c0 += cnt
             Mt, Ms = int(size[bt[ok[qs]]].max()), int(ncol[qs].max())
             A = np.zeros((qs.size, Mt, k))
             Bm = np.zeros((qs.size, Ms, k))
@@ -204,22 +268,13 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
                 A[j, :a.shape[0]] = a
                 m = int(ncol[q])
                 Bm[j, :m] = bflat[blk_off[q]: blk_off[q + 1]].reshape(k, m).T
-            Ad = torch.from_numpy(A).to(dev)
-            Bd = torch.from_numpy(Bm).to(dev)
-            qa, ra = torch.linalg.qr(Ad)
-            qb, rb = torch.linalg.qr(Bd)
-            u, sv, vh = torch.linalg.svd(ra @ rb.transpose(1, 2))
-            keep = (sv > eps * sv[:, :1]).sum(dim=1)
-            keep = torch.where(sv[:, 0] == 0.0, torch.zeros_like(keep), keep)
-            # (clusters smaller than the cross rank: reduced QR factors are
-            # min(|t|, k) wide, like numpy's)
-            mask = (torch.arange(sv.shape[1], device=dev)[None, :] < keep[:, None]).to(f64)
-            a2 = qa @ (u * (sv * mask)[:, None, :])
-            b2 = qb @ (vh.transpose(1, 2) * mask[:, None, :])
-            a2h, b2h, kh = a2.cpu().numpy(), b2.cpu().numpy(), keep.cpu().numpy()
-            for j, q in enumerate(qs):
-                kq = int(kh[j])
-                mt, ms = int(size[bt[ok[q]]]), int(ncol[q])
-                out[int(ok[q])] = ("ok", np.ascontiguousarray(a2h[j, :mt, :kq]),
-                                   np.ascontiguousarray(b2h[j, :ms, :kq]))
+            jobs.append((A, Bm))
+            metas.append(qs)
+    for qs, (a2h, b2h, kh) in zip(metas, _host_pool_map(trunc, jobs)):
+        for j, q in enumerate(qs):
+            kq = int(kh[j])
+            mt, ms = int(size[bt[ok[q]]]), int(ncol[q])
+            out[int(ok[q])] = ("ok", np.ascontiguousarray(a2h[j, :mt, :kq]),
+                               np.ascontiguousarray(b2h[j, :ms, :kq]))
+    lap("truncate", t0)
     return out

@@ -465,7 +465,7 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
         from .gpu_hca import hca_gpu
         res = hca_gpu(bt=bt[adm_ids], bs=bs[adm_ids], lo=lo, hi=hi, start=start, end=end, perm=perm,
                       coords=coords, order=config.cheb_order, eps=config.eps, evaluator=evaluator,
-                      device=device)
+                      device=device, times=times)
         times["hca_gpu"] = time.perf_counter() - t2
         lowrank, weights, n_fb = [None] * adm_ids.size, [None] * adm_ids.size, 0
         for i, (st, a, b) in enumerate(res):
@@ -484,7 +484,8 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
                 lowrank[i] = _aca_block(evaluator, coords, perm, start, end, t_c, s_c, config.eps)
             aa, bb = lowrank[i]
             weights[i] = (np.linalg.qr(bb)[1], np.linalg.qr(aa)[1])
-        say(f"HCA (gpu): {adm_ids.size} blocks, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s)")
+        say(f"HCA (gpu): {adm_ids.size} blocks, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s: "
+            + ", ".join(f"{k} {times[k]:.1f}s" for k in ("cross", "solve", "rows", "truncate") if k in times) + ")")
         t5 = time.perf_counter()
         from .recompress import recompress
         op = recompress(tree, surface.n,
