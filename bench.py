@@ -127,6 +127,20 @@ def _build(args, rank, ws, log):
     return build_workload(args.config, cache_dir=cache, log=log)
 
 
+def _traffic(args):
+    """DRAM bytes per launch of the dataflow kernel from the committed ncu
+    capture of this workload (profiles/r01_traffic.json), or --traffic."""
+    if args.traffic is not None:
+        return args.traffic
+    if args.nrhs != 1 or args.world > 1:
+        return None
+    try:
+        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        return t[args.config]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 L2_BYTES = 126 * 2**20
 
 
@@ -341,7 +355,7 @@ def run_b200(args):
                                          "work_items": st["ntasks"], "grid": st["grid"],
                                          "bytes_by_kind": st["bytes_by_kind"]}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"] * ws, "unit": "GB/s",
-                             "frac": achieved / (peaks["hbm_gbs"] * ws), "traffic": args.traffic,
+                             "frac": achieved / (peaks["hbm_gbs"] * ws), "traffic": _traffic(args),
                              "peak_kind": peak_kind, "aggregate_over_gpus": ws,
                              "algorithmic_bytes_per_launch": b_alg},
                 "cpu_baseline": cpu, "e2e": e2e,
