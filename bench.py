@@ -2,12 +2,14 @@
 """H² matvec benchmark (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config config2] [--nrhs 1]
+                    [--config config3] [--nrhs 1]
 
-A step is one H² product y = M x of the workload (default: BASELINE config 2,
-the 101 402-node cube, leaf 64, eta 2, order 5) with x already resident in
-HBM.  The operator is built on the box by the restated builder
-(paper_1811_05731_b200/assembly) before timing.  Rank 0 prints ONE JSON
+A step is one H² product y = M x of the workload (default: BASELINE config 3,
+the 1.04M-node thin disk, leaf 64, eta 2, order 5 -- the configuration the
+north star quotes its roofline target on) with x already resident in HBM.
+The operator is built on the box by the restated builder
+(paper_1811_05731_b200/assembly, GPU collocation and HCA; about 3 minutes
+for config 3) before timing and cached memory-mapped under --cache-dir.  Rank 0 prints ONE JSON
 line.  Under torchrun (N > 1) the product is sharded over the GPUs
 (byte-balanced leaf ranges, the upward coefficients
 all-gathered over NCCL between the two phases of every rank): a step is one
@@ -374,7 +376,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", default="config2")
+    ap.add_argument("--config", default="config3")
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--cache-dir", default=os.environ.get("H2B_CACHE", "/tmp/h2b_cache"))
     ap.add_argument("--profile", action="store_true", help="skip parity/e2e/CPU legs (for ncu)")

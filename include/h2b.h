@@ -84,6 +84,16 @@ typedef struct h2b_desc {
 /* sched_flags bits 16-17: columns in flight per lane of a streamed item:
    0 -> 8 (default), 2 -> 4 */
 #define H2B_SCHED_STREAM(s) (((s) & 3) << 16)
+/* sched_flags bits 20-23: serve the leaf coupling rows before the near item
+   a warp claimed ahead once it has run m near items in a row (15: always;
+   0: after it, the round-1 behaviour) */
+#define H2B_SCHED_LEAF_MIX(m) (((m) & 0xf) << 20)
+/* sched_flags bit 24: multi-RHS items stream through registers instead of
+   the per-warp TMA ring (A/B switch) */
+#define H2B_SCHED_NO_RING (1 << 24)
+/* sched_flags bits 26-29: the top k warps of each CTA take near-field items
+   before the up-leaf items and the coupling queues (0: none) */
+#define H2B_SCHED_NEAR_PRIO(k) (((k) & 0xf) << 26)
 
 /* Execution-plan knobs.  Zero-initialise for defaults. */
 typedef struct h2b_options {

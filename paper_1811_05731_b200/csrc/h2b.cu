@@ -83,8 +83,10 @@ struct Line {
 struct Ctl {
   Line head[kQueues];    // dynamic queue q: next slot to claim
   Line tail[kQueues];    // dynamic queue q: next slot to push
-  unsigned static_head;  // next initially-ready item to claim
+  unsigned static_head;  // next initially-ready up-leaf item to claim
   unsigned pad2[31];
+  unsigned near_head;    // next initially-ready near-field item to claim
+  unsigned pad5[31];
   unsigned dyn_started;  // dynamic items taken (queue or continuation)
   unsigned pad4[31];
   unsigned exited;       // warps that left the scheduler loop
@@ -118,6 +120,7 @@ struct KParams {
 
 // scheduling switches
 constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ahead near item
+constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -136,6 +139,16 @@ struct __align__(128) WarpSmem {
   int seg_nslots[h2b::kMaxSegs];
   int seg_stride[h2b::kMaxSegs];
 };
+
+// Per-warp TMA ring of the multi-RHS (NRHS >= 8) streamed items: two stages
+// of 8 KB (+ alignment slack) behind the WarpSmem array of the CTA.
+constexpr int kRingStageBytes = 8192;
+struct __align__(128) WarpRing {
+  double buf[2][(kRingStageBytes + 32) / 8];
+  uint64_t bar[2];
+};
+template <int NRHS>
+constexpr size_t ring_bytes_per_warp() { return NRHS >= 8 ? sizeof(WarpRing) : 0; }
 
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
@@ -505,6 +518,10 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
 }
 
 
+template <int NRHS>
+__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[4][NRHS / 8][4],
+                                             int lane);
+
 // D(16x8) += A(16x4, row) B(4x8, col) in fp64 on the tensor cores (DMMA).
 __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
@@ -589,7 +606,19 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
     __syncwarp();
   }
 
-  // bias slots, then the output rows this lane holds
+  mma_epilogue<NRHS>(p, T, acc, lane);
+}
+
+// Bias slots, then the output rows this lane holds (accumulator rows g, g+8
+// of each 16-row tile, columns 2t, 2t+1 of each 8-column tile).
+template <int NRHS>
+__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[4][NRHS / 8][4],
+                                             int lane) {
+  constexpr int NT = NRHS / 8;
+  constexpr int MT = 4;
+  const int m = T.m;
+  const int mtiles = (m + 15) >> 4;
+  const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     if (i >= mtiles) break;
@@ -617,6 +646,84 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
   }
 }
 
+// A streamed multi-RHS item (ld == m <= 64) on the DMMA tiles, its matrix
+// moved by TMA bulk copies through the warp's two-stage shared-memory ring:
+// chunk j + 2 is in flight while chunk j multiplies, so each warp keeps up
+// to 16 KB of the stream outstanding without holding it in registers (the
+// register-staged loop above keeps one 4-column k-step in flight, which
+// leaves HBM idle).  `rpar` holds the ring's mbarrier parities (bit s).
+template <int NRHS>
+__device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                                  WarpRing& R, unsigned& rpar, int lane,
+                                                  unsigned long long& t_gath) {
+  constexpr int kCols = kChunkBytes / (8 * NRHS);  // gathered-source capacity
+  constexpr int NT = NRHS / 8;
+  constexpr int MT = 4;
+  const int m = T.m;
+  const int mtiles = (m + 15) >> 4;
+  const int g = lane >> 2, t = lane & 3;
+  // columns per stage (>= 16), a whole number of 4-column k-steps so that
+  // the DMMA sums group columns exactly like the register-staged loop
+  const int cs = min(kCols, kRingStageBytes / (8 * m)) & ~3;
+  const int nch = (T.ncols + cs - 1) / cs;
+  const double* g0 = p.mat + T.data;
+  auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
+    const double* src = g0 + (int64_t)j * cs * m;
+    const int cc = min(cs, T.ncols - j * cs);
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
+    bulk_load(R.buf[j & 1], (const void*)a0, (unsigned)(a1 - a0), &R.bar[j & 1]);
+  };
+  if (lane == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  load_segtable(p, T, sin, w, lane);
+
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  for (int jc = 0; jc < nch; ++jc) {
+    const int col = jc * cs;
+    const int cc = min(cs, T.ncols - col);
+    gather_chunk<NRHS>(p, w, lane, col, cc);
+    for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) w.xs[j] = 0.0;  // k padding
+    __syncwarp();
+    const int s = jc & 1;
+    mbar_wait(&R.bar[s], (rpar >> s) & 1u);
+    rpar ^= 1u << s;
+    if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
+    const double* A = R.buf[s] + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    for (int c = 0; c < cc; c += 4) {
+      const bool okc = c + t < cc;
+      double a[MT][2];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = 16 * i + g;
+        const bool ok = okc && i < mtiles;
+        a[i][0] = (ok && r < m) ? A[(c + t) * m + r] : 0.0;
+        a[i][1] = (ok && r + 8 < m) ? A[(c + t) * m + r + 8] : 0.0;
+      }
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = w.xs[(c + t) * NRHS + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (i < mtiles)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+    }
+    __syncwarp();  // every lane is done with stage s and with xs
+    if (lane == 0 && jc + 2 < nch) issue(jc + 2);
+  }
+  mma_epilogue<NRHS>(p, T, acc, lane);
+}
+
 template <int NRHS>
 __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -628,6 +735,17 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   if (lane == 0) {
     mbar_init(bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // multi-RHS streaming ring (NRHS >= 8), behind the WarpSmem array
+  WarpRing* ring = nullptr;
+  unsigned rpar = 0;  // ring stage parities (all lanes)
+  if constexpr (NRHS >= 8) {
+    ring = reinterpret_cast<WarpRing*>(smem_raw + (size_t)nw * sizeof(WarpSmem)) + wib;
+    if (lane == 0) {
+      mbar_init(&ring->bar[0]);
+      mbar_init(&ring->bar[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
   __syncwarp();
   unsigned phase = 0;  // parity of the staging mbarrier (all lanes)
@@ -641,8 +759,12 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
   const unsigned n_dynamic = (unsigned)(p.nnodes - p.nready0);
-  bool static_done = false;  // lane-0 state below
-  bool static_lo = false;    // static claims have reached the class-1 (near) part
+  // lane-0 state below.  The initially-ready items are two static lists
+  // claimed through separate heads: up-leaf items ready0[0, nready0_hi) and
+  // the near field ready0[nready0_hi, nready0).
+  const unsigned n_up = (unsigned)p.nready0_hi, n_near = (unsigned)(p.nready0 - p.nready0_hi);
+  bool up_done = n_up == 0;
+  bool near_done = n_near == 0;
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   int pend = -1;             // near item claimed ahead (slack work, no priority cost)
   int cont = -1;             // continuation (all lanes)
@@ -654,6 +776,18 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   const int u_sel = (p.flags >> 16) & 3;
   const int stream_u = u_sel >= 2 ? 4 : 8;
   const bool near_ok = near_lim == 0 || wib < near_lim;
+  // leaf coupling rows (class 2) are served before the claimed-ahead near
+  // item once this warp has run `leaf_mix` near items in a row (15: always),
+  // so the gather-latency-bound downward rows overlap the near-field stream
+  // instead of forming a tail after it
+  const int leaf_mix = (p.flags >> 20) & 0xf;
+  const int leaf_thr = leaf_mix == 15 ? 0 : leaf_mix;
+  int near_run = 0;  // lane-0 state: near items run since the last class-2 item
+  // the top `near_prio` warps of each CTA stream near items from the start
+  // (after the chain queue only), so HBM is busy while the other warps work
+  // through the latency-bound upward pass and coupling rows
+  const int near_prio = (p.flags >> 26) & 0xf;
+  const bool nprio = near_prio > 0 && wib >= nw - near_prio;
   for (;;) {
     int item = cont;
     if (lane == 0 && item < 0) {
@@ -678,14 +812,21 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         owed = (int)abs;
         return -1;
       };
-      auto take_static = [&]() -> int {
+      auto take_up = [&]() -> int {
         const unsigned s = atomicAdd(&ctl->static_head, 1u);
-        if (s >= (unsigned)p.nready0) {
-          static_done = true;
+        if (s >= n_up) {
+          up_done = true;
           return -1;
         }
-        if (s >= (unsigned)p.nready0_hi) static_lo = true;
         return __ldg(p.ready0 + s);
+      };
+      auto take_near = [&]() -> int {
+        const unsigned s = atomicAdd(&ctl->near_head, 1u);
+        if (s >= n_near) {
+          near_done = true;
+          return -1;
+        }
+        return __ldg(p.ready0 + n_up + s);
       };
       unsigned backoff = 64;
       for (;;) {
@@ -707,25 +848,37 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         } else if (h[0] < t[0] && (item = claim(0)) >= 0) {
           break;
         }
-        // class-0 static items (up-leaf) before any slack work
-        if (!static_done && !static_lo && near_ok && (item = take_static()) >= 0) {
-          if (!static_lo) break;
-          pend = item;  // already class 1: keep it for after the slack queue
-          item = -1;
+        if (nprio) {
+          if (pend >= 0) {
+            item = pend;
+            pend = -1;
+            break;
+          }
+          if (!near_done && near_ok && (item = take_near()) >= 0) break;
         }
+        // class-0 static items (up-leaf) before any slack work
+        if (!up_done && near_ok && (item = take_up()) >= 0) break;
         // coupling rows of inner clusters feed the downward chain level by level
         if ((p.flags & kFlagSlackFirst) && owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
+        if (leaf_mix && near_run >= leaf_thr && owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) {
+          near_run = 0;
+          break;
+        }
         // the near item claimed ahead comes before the slack queue: near
         // items are issued longest first, and a long one must not wait
         if (pend >= 0) {
           item = pend;
           pend = -1;
+          ++near_run;
           break;
         }
         // coupling rows of inner clusters: the chain needs them level by level
         if (owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
         if (owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) break;
-        if (!static_done && near_ok && (item = take_static()) >= 0) break;
+        if (!near_done && near_ok && (item = take_near()) >= 0) {
+          ++near_run;
+          break;
+        }
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
         if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
@@ -741,8 +894,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     // claim the next near item ahead, so that the next decision costs no
     // atomic round trip (its result is read after this item)
     unsigned ahead = 0xffffffffu;
-    if (lane == 0 && item >= 0 && pend < 0 && static_lo && !static_done && near_ok)
-      ahead = atomicAdd(&ctl->static_head, 1u);
+    if (lane == 0 && item >= 0 && pend < 0 && (up_done || nprio) && !near_done && near_ok)
+      ahead = atomicAdd(&ctl->near_head, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item < 0) break;
     unsigned long long t_start = 0;
@@ -776,6 +929,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       if (off >= 0) {
         run_item_mma<NRHS, true>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
         phase ^= 1u;
+      } else if (T.ld == T.m && T.m <= 64 && T.ncols > 0 && !(p.flags & kFlagNoRing)) {
+        run_item_mma_ring<NRHS>(p, T, sin, w, *ring, rpar, lane, t_gath);
       } else {
         run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       }
@@ -858,8 +1013,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       }
     }
     if (lane == 0 && ahead != 0xffffffffu) {
-      if (ahead < (unsigned)p.nready0) pend = __ldg(p.ready0 + ahead);
-      else static_done = true;
+      if (ahead < n_near) pend = __ldg(p.ready0 + n_up + ahead);
+      else near_done = true;
     }
     if (p.trace && lane == 0) {
       unsigned long long t_end, smid;
@@ -886,6 +1041,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
 #pragma unroll
       for (int q = 0; q < kQueues; ++q) ctl->head[q].v = ctl->tail[q].v = 0;
       ctl->static_head = 0;
+      ctl->near_head = 0;
       ctl->dyn_started = 0;
       ctl->exited = 0;
       fence_acq_rel();
@@ -1001,7 +1157,7 @@ int nrhs_index(int nrhs) {
 
 template <int NRHS>
 int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
-  const size_t sm = (size_t)wpc * sizeof(WarpSmem);
+  const size_t sm = (size_t)wpc * (sizeof(WarpSmem) + ring_bytes_per_warp<NRHS>());
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -1041,7 +1197,7 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   p.y = y;
   p.flags = op->flags;
   const int gi = nrhs_index(NRHS);
-  const size_t smem = (size_t)op->wpc * sizeof(WarpSmem);
+  const size_t smem = (size_t)op->wpc * (sizeof(WarpSmem) + ring_bytes_per_warp<NRHS>());
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   if (k == 0) {
     const int64_t total = op->n * NRHS;
@@ -1207,7 +1363,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
   op->flags = ((o && (o->sched_flags & H2B_SCHED_NEAR_FIRST)) ? 0 : kFlagSlackFirst) |
-              (o ? (o->sched_flags & 0x3ff00) : 0);
+              (o ? (o->sched_flags & 0x3df3ff00) : 0);
   op->rank = P.rank;
   op->world = P.world_size;
   op->exch_off = P.exch_off;
@@ -1216,7 +1372,9 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   // +2 doubles: a 16-byte-rounded TMA copy of the last item may read past the end
   P.mat.push_back(0.0);
   P.mat.push_back(0.0);
-  if ((rc = upload(&op->d_mat, P.mat.data(), P.mat.size()))) return rc;
+  // the pool plus 32 bytes: bulk copies round a matrix's end up to 16 bytes
+  if ((rc = upload<double>(&op->d_mat, nullptr, P.mat.size() + 4))) return rc;
+  H2B_CUDA(cudaMemcpy(op->d_mat, P.mat.data(), sizeof(double) * P.mat.size(), cudaMemcpyHostToDevice));
   P.mat.resize(P.mat.size() - 2);
   op->ph.resize(P.ph.size());
   for (size_t k = 0; k < P.ph.size(); ++k)

@@ -187,6 +187,19 @@ def describe(op) -> _DescHolder:
     return _DescHolder(op)
 
 
+# h2b_options.sched_flags bits (include/h2b.h)
+SCHED_NEAR_FIRST = 1
+SCHED_NO_RING = 1 << 24
+
+
+def SCHED_LEAF_MIX(m: int) -> int:
+    return (int(m) & 0xF) << 20
+
+
+def SCHED_NEAR_PRIO(k: int) -> int:
+    return (int(k) & 0xF) << 26
+
+
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
              band_depth=0, rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
     o = nat.Options()

@@ -19,7 +19,7 @@ import numpy as np
 from .assembly import geometry as G
 from .assembly.hbuild import CompressionConfig, assemble_h2
 
-__all__ = ["WORKLOADS", "surface_for", "build_workload", "vector_for"]
+__all__ = ["WORKLOADS", "surface_for", "build_workload", "vector_for", "save_cached", "load_cached"]
 
 WORKLOADS = {
     "config1": dict(desc="unit icosphere level 4 (N=2562), leaf 32, eta 2, order 4",
@@ -58,11 +58,10 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     w = WORKLOADS[name]
     backend = w.get("backend", "numpy")
     key = hashlib.sha256(repr((name, w["desc"], w["cfg"], 1, backend)).encode()).hexdigest()[:16]
-    path = Path(cache_dir) / f"h2b_{name}_{key}.npz" if cache_dir else None
-    if path is not None and path.exists():
-        from .io import load_npz
+    path = Path(cache_dir) / f"h2b_{name}_{key}" if cache_dir else None
+    if path is not None and (path / "DONE").exists():
         t = time.perf_counter()
-        op, extra = load_npz(path)
+        op = load_cached(path)
         log(f"[workload] {name}: loaded cached operator {path} ({time.perf_counter() - t:.1f}s)")
         return op, {"cached": True, "n": op.n}
     t = time.perf_counter()
@@ -74,14 +73,28 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
             "n_dense": rep.n_dense, "n_fallback": rep.n_fallback}
     if path is not None:
         try:
-            os.makedirs(path.parent, exist_ok=True)
-            from .io import h2_to_arrays
-            tmp = path.with_suffix(".tmp.npz")
-            np.savez(tmp, **h2_to_arrays(op))
-            os.replace(tmp, path)
+            save_cached(op, path)
         except OSError:
             pass
     return op, info
+
+
+def save_cached(op, path: Path) -> None:
+    """One .npy file per flat array (io.h2_to_arrays), DONE written last."""
+    from .io import h2_to_arrays
+    os.makedirs(path, exist_ok=True)
+    for k, v in h2_to_arrays(op).items():
+        np.save(path / f"{k}.npy", v)
+    (path / "DONE").write_text("ok")
+
+
+def load_cached(path: Path):
+    """Memory-mapped: the operator's blocks are read-only views of the page
+    cache, so the ranks of a multi-GPU run on one host share one copy."""
+    from .io import h2_from_arrays
+    a = {f.stem: np.load(f, mmap_mode="r") for f in Path(path).glob("*.npy")}
+    a["n"] = np.asarray(a["n"])
+    return h2_from_arrays(a)
 
 
 def vector_for(name: str, n: int, nrhs: int = 1, seed: int = 1234) -> np.ndarray:

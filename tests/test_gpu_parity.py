@@ -53,7 +53,9 @@ def test_far_and_near_fields_separately(golden):
 
 
 @pytest.mark.parametrize("opts", [dict(task_bytes=512), dict(task_bytes=4096, sched_flags=1),
-                                  dict(warps_per_cta=4, ctas_per_sm=1)])
+                                  dict(warps_per_cta=4, ctas_per_sm=1),
+                                  dict(task_bytes=2048, sched_flags=(15 << 20) | (6 << 26)),
+                                  dict(sched_flags=(2 << 20) | (8 << 26))])
 def test_plan_variants(opts):
     op, ex = load_golden("config1_sphere4")
     dev = _gpu().DeviceOperator(op, **opts)
@@ -72,6 +74,28 @@ def test_multi_rhs(nrhs):
     Y = _gpu().h2_matmat(op, X)
     for i in range(nrhs):
         assert rel(Y[:, i], Yref[:, i]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["config1_sphere4", "prism_20_40_2_default"])
+@pytest.mark.parametrize("nrhs", [8, 16])
+def test_multi_rhs_ring_matches_register_path(name, nrhs):
+    """The TMA-ring streaming of the DMMA items (default) groups columns into
+    k-steps exactly like the register-staged loop (H2B_SCHED_NO_RING), so
+    the two give bit-identical products; both match the reference."""
+    op, ex = load_golden(name)
+    h2 = _gpu()
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((op.n, nrhs))
+    ys = []
+    for flags in (0, h2.SCHED_NO_RING):
+        dev = h2.DeviceOperator(op, sched_flags=flags)
+        try:
+            ys.append(dev.matvec(X))
+        finally:
+            dev.close()
+    assert np.array_equal(ys[0], ys[1])
+    for i in range(nrhs):
+        assert rel(ys[0][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
 
 
 @pytest.mark.parametrize("seed", range(3))

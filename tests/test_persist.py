@@ -178,3 +178,18 @@ def test_file_straight_to_device():
         assert dev.stream_bytes() == int(ex["storage_bytes"])
     finally:
         dev.close()
+
+
+def test_workload_cache_roundtrip_memory_mapped(tmp_path):
+    """bench.py's operator cache (one .npy per array, memory-mapped on load)
+    returns the same operator and the same product."""
+    from oracle.h2_matvec_ref import h2_matvec_ref
+    from paper_1811_05731_b200.workloads import load_cached, save_cached
+    op, ex = load_golden("torus_32_16_4_default")
+    save_cached(op, tmp_path / "op")
+    op2 = load_cached(tmp_path / "op")
+    assert op2.n == op.n and op2.storage_bytes() == op.storage_bytes()
+    assert isinstance(op2.near[0][2].base, np.memmap) or isinstance(op2.near[0][2], np.memmap) \
+        or op2.near[0][2].flags["OWNDATA"] is False
+    x = ex["X"][:, 0]
+    assert np.array_equal(h2_matvec_ref(op2, x), h2_matvec_ref(op, x))

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
     ap.add_argument("--grid", default='{"task_bytes":[16384,32768,65536],"interleave":[0,-1]}')
     ap.add_argument("--flush", action="store_true", help="flush L2 before each timed step")
+    ap.add_argument("--nrhs", default="1", help="comma list of right-hand-side counts")
     ap.add_argument("--ablate", default="", help="comma list of: far (near=[]), near (coupling=[])")
     a = ap.parse_args()
     import torch
@@ -38,25 +39,27 @@ def main():
         ops[ab] = dataclasses.replace(op, near=[]) if ab == "far" else dataclasses.replace(op, coupling=[])
     grid = json.loads(a.grid)
     keys = list(grid)
-    x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
-    y = torch.empty_like(x)
     s = torch.cuda.current_stream()
+    nrhs_list = [int(v) for v in a.nrhs.split(",")]
     from bench import DeviceTimer
     timer = DeviceTimer(s, flush=a.flush)
-    ref = None
-    for (name, opx), vals in itertools.product(ops.items(), itertools.product(*[grid[k] for k in keys])):
+    refs = {}
+    for (name, opx), nrhs, vals in itertools.product(ops.items(), nrhs_list,
+                                                     itertools.product(*[grid[k] for k in keys])):
         opts = dict(zip(keys, vals))
         dev = DeviceOperator(opx, **opts)
         st = dev.stats()
+        x = torch.from_numpy(np.ascontiguousarray(vector_for(a.config, op.n, nrhs))).cuda()
+        y = torch.empty_like(x)
         for _ in range(5):
-            dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
-        ms = timer.run(lambda: dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s.cuda_stream), a.steps)
+            dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, s.cuda_stream)
+        ms = timer.run(lambda: dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, s.cuda_stream), a.steps)
         yy = y.cpu().numpy()
-        if ref is None or name != "full":
-            ref = yy if name == "full" or ref is None else ref
-        err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref)) if name == "full" else None
-        gbs = (st["stream_bytes"] + 16 * op.n) / (ms * 1e-3) / 1e9
-        print(json.dumps({"op": name, "opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1), "items": st["ntasks"],
+        ref = refs.setdefault((name, nrhs), yy)
+        err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref))
+        gbs = (st["stream_bytes"] + 16 * op.n * nrhs) / (ms * 1e-3) / 1e9
+        print(json.dumps({"op": name, "nrhs": nrhs, "opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1),
+                          "ms_per_vector": round(ms / nrhs, 4), "items": st["ntasks"],
                           "grid": st["grid"], "rel_vs_first": err}), flush=True)
         dev.close()
 

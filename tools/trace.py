@@ -114,6 +114,21 @@ def main():
     bins = np.linspace(0, end.max(), 21)
     busy = [(np.minimum(end, b1) - np.maximum(start, b0)).clip(0).sum() / (b1 - b0) for b0, b1 in zip(bins, bins[1:])]
     print("avg busy warps per 5% of span:", " ".join(f"{b:.0f}" for b in busy))
+    # where each kind's bytes stream: MB per 5% of span (pro rata over each
+    # item's interval); down items split into transfer pieces (a down
+    # predecessor) and coupling pieces
+    dk = np.zeros(T, bool)
+    for it in np.nonzero(kind == 2)[0]:
+        d = deps[dep0[it]:dep0[it + 1]]
+        dk[it] = bool(d.size) and bool((kind[d] == 2).any())
+    groups = [("up", (kind <= 1)), ("down-xfer", (kind == 2) & dk), ("down-coupl", (kind == 2) & ~dk),
+              ("near", kind == 3), ("final", kind == 4)]
+    span = np.maximum(end - start, 1)
+    for name, sel in groups:
+        sel = sel & unit
+        row = [(nbytes[sel] * (np.minimum(end[sel], b1) - np.maximum(start[sel], b0)).clip(0) / span[sel]).sum() / 1e6
+               for b0, b1 in zip(bins, bins[1:])]
+        print(f"  MB/5% {name:10s}", " ".join(f"{r:6.0f}" for r in row))
     if a.save:
         np.savez_compressed(a.save, start=start, end=end, kind=kind, tr=tr)
 
