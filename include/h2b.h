@@ -79,6 +79,10 @@ typedef struct h2b_desc {
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */
 #define H2B_SCHED_NEAR_FIRST 1
+/* sched_flags bits 4-7: single-vector products give the top k warps of each
+   CTA a two-stage 8 KB TMA ring for streamed items (16 KB in flight each, no
+   registers); 0: register streaming only */
+#define H2B_SCHED_RING_WARPS(k) (((k) & 0xf) << 4)
 /* sched_flags bits 8-15: warps per CTA that take near-field items (0: all) */
 #define H2B_SCHED_NEAR_WARPS(k) (((k) & 0xff) << 8)
 /* sched_flags bits 16-17: columns in flight per lane of a streamed item:

@@ -115,6 +115,7 @@ struct KParams {
   int32_t nready0;
   int32_t nready0_hi;                   // ready0[0:nready0_hi) are class 0
   int32_t flags;                        // kFlag* scheduling switches (h2b_options.sched_flags)
+  int32_t ring_warps;                   // NRHS < 8: warps per CTA (the top ones) with a TMA ring
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
 };
 
@@ -129,7 +130,6 @@ constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+
 // gathered sources, the item's segment table, the small-item reduction
 // scratch and the staging mbarrier.
 struct __align__(128) WarpSmem {
-  double abuf[kStageBytes / 8];
   double xs[kChunkBytes / 8];
   unsigned long long bar;
   double red[32];
@@ -140,15 +140,22 @@ struct __align__(128) WarpSmem {
   int seg_stride[h2b::kMaxSegs];
 };
 
-// Per-warp TMA ring of the multi-RHS (NRHS >= 8) streamed items: two stages
-// of 8 KB (+ alignment slack) behind the WarpSmem array of the CTA.
+// Per-warp TMA ring of streamed items: two stages of 8 KB (+ alignment
+// slack).  Ring warps (all warps for NRHS >= 8, the top `ring_warps` of each
+// CTA otherwise) stream their items through it; a ring warp stages its
+// far-field items in buf[0].  Other warps have a kStageBytes staging buffer.
+// Dynamic shared memory: [WarpSmem x nw][staging of non-ring warps][rings].
 constexpr int kRingStageBytes = 8192;
 struct __align__(128) WarpRing {
   double buf[2][(kRingStageBytes + 32) / 8];
   uint64_t bar[2];
 };
-template <int NRHS>
-constexpr size_t ring_bytes_per_warp() { return NRHS >= 8 ? sizeof(WarpRing) : 0; }
+static_assert(sizeof(WarpRing) % 128 == 0 && kStageBytes % 128 == 0, "staging alignment");
+static_assert((kRingStageBytes + 32) >= kStageBytes, "a ring stage doubles as far-field staging");
+inline size_t smem_bytes(int nw, int ring_warps) {
+  return (size_t)nw * sizeof(WarpSmem) + (size_t)(nw - ring_warps) * kStageBytes +
+         (size_t)ring_warps * sizeof(WarpRing);
+}
 
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
@@ -351,6 +358,71 @@ __device__ __forceinline__ double ldA(const double* q) {
   else return ld_stream(q);
 }
 
+// Bias: partial slots of the output rows (lane, lane + 32), summed in slot
+// order (loads batched: heavy rows have hundreds of slots).
+template <int NRHS>
+__device__ __forceinline__ void add_bias(const KParams& p, const DTask& T, double (&acc0)[NRHS],
+                                         double (&acc1)[NRHS], int lane) {
+  const bool v0 = lane < T.m, v1 = lane + 32 < T.m;
+  if (T.bias >= 0) {
+    int s = 0;
+    constexpr int QB = NRHS == 1 ? 16 : (NRHS == 2 ? 4 : 1);
+    for (; s + QB <= T.bias_nslots; s += QB) {
+      double b0[QB][NRHS], b1[QB][NRHS];
+#pragma unroll
+      for (int q = 0; q < QB; ++q) {
+        const double* b = p.coef + (T.bias + (int64_t)(s + q) * T.bias_stride) * NRHS;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          b0[q][r] = v0 ? __ldcg(b + (int64_t)lane * NRHS + r) : 0.0;
+          b1[q][r] = v1 ? __ldcg(b + (int64_t)(lane + 32) * NRHS + r) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QB; ++q)
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          acc0[r] += b0[q][r];
+          acc1[r] += b1[q][r];
+        }
+    }
+    for (; s < T.bias_nslots; ++s) {
+      const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        if (v0) acc0[r] += __ldcg(b + (int64_t)lane * NRHS + r);
+        if (v1) acc1[r] += __ldcg(b + (int64_t)(lane + 32) * NRHS + r);
+      }
+    }
+  }
+}
+
+// Output rows (lane, lane + 32): a coefficient slot, or y in node order.
+template <int NRHS>
+__device__ __forceinline__ void store_rows(const KParams& p, const DTask& T, const double (&acc0)[NRHS],
+                                           const double (&acc1)[NRHS], int lane) {
+  const int m = T.m;
+  const bool w0 = lane < m, w1 = lane + 32 < m;
+  if (T.kind == h2b::kFinal) {
+    if (w0) {
+      const int64_t node = __ldg(p.perm + T.out + lane);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc0[r];
+    }
+    if (w1) {
+      const int64_t node = __ldg(p.perm + T.out + lane + 32);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc1[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      if (w0) p.coef[(T.out + lane) * NRHS + r] = acc0[r];
+      if (w1) p.coef[(T.out + lane + 32) * NRHS + r] = acc1[r];
+    }
+  }
+}
+
 // One work item with NRHS right-hand sides.  A is the item's column-major
 // matrix: staged in shared memory by a TMA bulk copy that completes on `bar`
 // (SMEM), or streamed from global memory.
@@ -406,39 +478,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
     acc0[0] = s;
   } else {
     const bool v0 = lane < m, v1 = lane + 32 < m;
-    // bias: near-field partial slots of a leaf, summed in slot order (loads
-    // batched four at a time: heavy rows have hundreds of slots)
-    if (T.bias >= 0) {
-      int s = 0;
-      constexpr int QB = NRHS == 1 ? 16 : (NRHS == 2 ? 4 : 1);
-      for (; s + QB <= T.bias_nslots; s += QB) {
-        double b0[QB][NRHS], b1[QB][NRHS];
-#pragma unroll
-        for (int q = 0; q < QB; ++q) {
-          const double* b = p.coef + (T.bias + (int64_t)(s + q) * T.bias_stride) * NRHS;
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            b0[q][r] = v0 ? __ldcg(b + (int64_t)lane * NRHS + r) : 0.0;
-            b1[q][r] = v1 ? __ldcg(b + (int64_t)(lane + 32) * NRHS + r) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < QB; ++q)
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            acc0[r] += b0[q][r];
-            acc1[r] += b1[q][r];
-          }
-      }
-      for (; s < T.bias_nslots; ++s) {
-        const double* b = p.coef + (T.bias + (int64_t)s * T.bias_stride) * NRHS;
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
-          if (v0) acc0[r] += __ldcg(b + (int64_t)lane * NRHS + r);
-          if (v1) acc1[r] += __ldcg(b + (int64_t)(lane + 32) * NRHS + r);
-        }
-      }
-    }
+    add_bias<NRHS>(p, T, acc0, acc1, lane);
     for (int col = 0; col < T.ncols; col += kCols) {
       const int cc = min(kCols, T.ncols - col);
       const double* Ac = A + (int64_t)col * ld;
@@ -496,25 +536,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
     }
   }
 
-  const bool w0 = lane < m, w1 = lane + 32 < m;
-  if (T.kind == h2b::kFinal) {
-    if (w0) {
-      const int64_t node = __ldg(p.perm + T.out + lane);
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc0[r];
-    }
-    if (w1) {
-      const int64_t node = __ldg(p.perm + T.out + lane + 32);
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc1[r];
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) {
-      if (w0) p.coef[(T.out + lane) * NRHS + r] = acc0[r];
-      if (w1) p.coef[(T.out + lane + 32) * NRHS + r] = acc1[r];
-    }
-  }
+  store_rows<NRHS>(p, T, acc0, acc1, lane);
 }
 
 
@@ -646,17 +668,65 @@ __device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, d
   }
 }
 
+// Sources of one multi-RHS chunk (<= 128 double2 values: 4 per lane),
+// split into issue (first slot of each value, loads left in flight in
+// registers) and commit (further partial slots in slot order, then the
+// store to shared memory), so a chunk's gather overlaps the previous
+// chunk's multiplication.  `k` is the lane's segment cursor (columns only
+// increase along a lane, across chunks too).
+template <int NRHS>
+struct GatherBatch {
+  double2 v[4];
+  const double2* q[4];
+  int ns[4];
+  int64_t st[4];
+};
+template <int NRHS>
+__device__ __forceinline__ void gather_issue(const KParams& p, const WarpSmem& w, int lane, int col, int cc,
+                                             GatherBatch<NRHS>& g, int& k) {
+  const int total = cc * NRHS / 2;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int jj = lane + 32 * u;
+    g.ns[u] = 0;
+    g.v[u] = make_double2(0.0, 0.0);
+    if (jj < total) {
+      const int j = 2 * jj;
+      const int c = col + j / NRHS, r = j % NRHS;
+      while (w.seg_off[k + 1] <= c) ++k;
+      const int64_t e = (w.seg_src[k] + (c - w.seg_off[k])) * NRHS + r;
+      const bool isx = w.seg_kind[k] == h2b::kSegX;
+      g.q[u] = reinterpret_cast<const double2*>((isx ? p.xp : p.coef) + e);
+      g.ns[u] = isx ? 1 : w.seg_nslots[k];
+      g.st[u] = (int64_t)w.seg_stride[k] * NRHS / 2;
+      if (g.ns[u] > 0) g.v[u] = isx ? __ldg(g.q[u]) : __ldcg(g.q[u]);
+    }
+  }
+}
+template <int NRHS>
+__device__ __forceinline__ void gather_commit(GatherBatch<NRHS>& g, int lane, int cc, double* xs) {
+  const int total = cc * NRHS / 2;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    for (int s = 1; s < g.ns[u]; ++s) add_to(g.v[u], __ldcg(g.q[u] + (int64_t)s * g.st[u]));
+    if (lane + 32 * u < total) reinterpret_cast<double2*>(xs)[lane + 32 * u] = g.v[u];
+  }
+  for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) xs[j] = 0.0;  // k padding
+}
+
 // A streamed multi-RHS item (ld == m <= 64) on the DMMA tiles, its matrix
 // moved by TMA bulk copies through the warp's two-stage shared-memory ring:
 // chunk j + 2 is in flight while chunk j multiplies, so each warp keeps up
 // to 16 KB of the stream outstanding without holding it in registers (the
 // register-staged loop above keeps one 4-column k-step in flight, which
-// leaves HBM idle).  `rpar` holds the ring's mbarrier parities (bit s).
+// leaves HBM idle).  The sources of chunk j + 1 are gathered into the other
+// half of the warp's source buffer while chunk j multiplies.  `rpar` holds
+// the ring's mbarrier parities (bit s).
 template <int NRHS>
 __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
                                                   WarpRing& R, unsigned& rpar, int lane,
                                                   unsigned long long& t_gath) {
-  constexpr int kCols = kChunkBytes / (8 * NRHS);  // gathered-source capacity
+  constexpr int kHalf = kChunkBytes / (16 * NRHS);  // columns per source half (16 or 32)
   constexpr int NT = NRHS / 8;
   constexpr int MT = 4;
   const int m = T.m;
@@ -664,7 +734,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   const int g = lane >> 2, t = lane & 3;
   // columns per stage (>= 16), a whole number of 4-column k-steps so that
   // the DMMA sums group columns exactly like the register-staged loop
-  const int cs = min(kCols, kRingStageBytes / (8 * m)) & ~3;
+  const int cs = min(kHalf, kRingStageBytes / (8 * m)) & ~3;
   const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
@@ -688,17 +758,23 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
+  GatherBatch<NRHS> gb;
+  int kseg = 0;
+  gather_issue<NRHS>(p, w, lane, 0, min(cs, T.ncols), gb, kseg);
+  gather_commit<NRHS>(gb, lane, min(cs, T.ncols), w.xs);
+  __syncwarp();
   for (int jc = 0; jc < nch; ++jc) {
     const int col = jc * cs;
     const int cc = min(cs, T.ncols - col);
-    gather_chunk<NRHS>(p, w, lane, col, cc);
-    for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) w.xs[j] = 0.0;  // k padding
-    __syncwarp();
+    const bool more = jc + 1 < nch;
+    const int cc1 = more ? min(cs, T.ncols - col - cs) : 0;
+    if (more) gather_issue<NRHS>(p, w, lane, col + cs, cc1, gb, kseg);
     const int s = jc & 1;
     mbar_wait(&R.bar[s], (rpar >> s) & 1u);
     rpar ^= 1u << s;
     if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
     const double* A = R.buf[s] + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* xs = w.xs + (jc & 1) * kHalf * NRHS;
     for (int c = 0; c < cc; c += 4) {
       const bool okc = c + t < cc;
       double a[MT][2];
@@ -711,17 +787,89 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
       }
       double b[NT];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = w.xs[(c + t) * NRHS + 8 * j + g];
+      for (int j = 0; j < NT; ++j) b[j] = xs[(c + t) * NRHS + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < MT; ++i)
         if (i < mtiles)
 #pragma unroll
           for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
     }
-    __syncwarp();  // every lane is done with stage s and with xs
+    __syncwarp();  // every lane is done with stage s and with this source half
     if (lane == 0 && jc + 2 < nch) issue(jc + 2);
+    if (more) {
+      gather_commit<NRHS>(gb, lane, cc1, w.xs + ((jc + 1) & 1) * kHalf * NRHS);
+      __syncwarp();
+    }
   }
   mma_epilogue<NRHS>(p, T, acc, lane);
+}
+
+
+// A streamed single-vector item (ld == m, 16 < m <= 64, ncols <= the gather
+// capacity) on a ring warp: its matrix moves through the warp's two-stage
+// TMA ring (16 KB in flight without registers), the sources are gathered
+// once, and every lane runs the same column-ordered FMA chain as run_item,
+// so a ring warp's result is bit-identical to a register-streaming warp's.
+__device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                               WarpRing& R, unsigned& rpar, int lane,
+                                               unsigned long long& t_gath) {
+  const int m = T.m;
+  const int cs = kRingStageBytes / (8 * m);  // columns per stage (>= 16)
+  const int nch = (T.ncols + cs - 1) / cs;
+  const double* g0 = p.mat + T.data;
+  auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
+    const double* src = g0 + (int64_t)j * cs * m;
+    const int cc = min(cs, T.ncols - j * cs);
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
+    bulk_load(R.buf[j & 1], (const void*)a0, (unsigned)(a1 - a0), &R.bar[j & 1]);
+  };
+  if (lane == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  load_segtable(p, T, sin, w, lane);
+  double acc0[1] = {0.0}, acc1[1] = {0.0};
+  add_bias<1>(p, T, acc0, acc1, lane);
+  gather_chunk<1>(p, w, lane, 0, T.ncols);
+  __syncwarp();
+  const bool v0 = lane < m, v1 = lane + 32 < m;
+  double s0 = acc0[0], s1 = acc1[0];
+  for (int jc = 0; jc < nch; ++jc) {
+    const int col = jc * cs;
+    const int cc = min(cs, T.ncols - col);
+    const int st = jc & 1;
+    mbar_wait(&R.bar[st], (rpar >> st) & 1u);
+    rpar ^= 1u << st;
+    if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
+    const double* A = R.buf[st] + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* xs = w.xs + col;
+    int c = 0;
+    for (; c + 8 <= cc; c += 8) {
+      double a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = v0 ? A[(c + u) * m + lane] : 0.0;
+        b[u] = v1 ? A[(c + u) * m + lane + 32] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s0 = fma(a[u], xs[c + u], s0);
+        s1 = fma(b[u], xs[c + u], s1);
+      }
+    }
+    for (; c < cc; ++c) {
+      const double a = v0 ? A[c * m + lane] : 0.0;
+      const double b = v1 ? A[c * m + lane + 32] : 0.0;
+      s0 = fma(a, xs[c], s0);
+      s1 = fma(b, xs[c], s1);
+    }
+    __syncwarp();  // every lane is done with stage st
+    if (lane == 0 && jc + 2 < nch) issue(jc + 2);
+  }
+  acc0[0] = s0;
+  acc1[0] = s1;
+  store_rows<1>(p, T, acc0, acc1, lane);
 }
 
 template <int NRHS>
@@ -736,15 +884,24 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     mbar_init(bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // multi-RHS streaming ring (NRHS >= 8), behind the WarpSmem array
+  // staging: a TMA ring (ring warps) or one far-field buffer
+  const int nring = NRHS >= 8 ? nw : p.ring_warps;
+  const int first_ring = nw - nring;
   WarpRing* ring = nullptr;
+  double* abuf;
   unsigned rpar = 0;  // ring stage parities (all lanes)
-  if constexpr (NRHS >= 8) {
-    ring = reinterpret_cast<WarpRing*>(smem_raw + (size_t)nw * sizeof(WarpSmem)) + wib;
-    if (lane == 0) {
-      mbar_init(&ring->bar[0]);
-      mbar_init(&ring->bar[1]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  {
+    unsigned char* st = smem_raw + (size_t)nw * sizeof(WarpSmem);
+    if (wib >= first_ring) {
+      ring = reinterpret_cast<WarpRing*>(st + (size_t)first_ring * kStageBytes) + (wib - first_ring);
+      abuf = ring->buf[0];
+      if (lane == 0) {
+        mbar_init(&ring->bar[0]);
+        mbar_init(&ring->bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+    } else {
+      abuf = reinterpret_cast<double*>(st + (size_t)wib * kStageBytes);
     }
   }
   __syncwarp();
@@ -921,22 +1078,25 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
       const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
       if (a1 - a0 <= (uintptr_t)kStageBytes) {
-        if (lane == 0) bulk_load(w.abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
+        if (lane == 0) bulk_load(abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
         off = (int)(((uintptr_t)g0 - a0) >> 3);
       }
     }
     if constexpr (NRHS >= 8) {
       if (off >= 0) {
-        run_item_mma<NRHS, true>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
+        run_item_mma<NRHS, true>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
         phase ^= 1u;
-      } else if (T.ld == T.m && T.m <= 64 && T.ncols > 0 && !(p.flags & kFlagNoRing)) {
+      } else if (T.ld == T.m && T.m <= 64 && T.ncols > 0 && !(p.flags & kFlagNoRing)) {  // all warps ring
         run_item_mma_ring<NRHS>(p, T, sin, w, *ring, rpar, lane, t_gath);
       } else {
         run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       }
     } else if (off >= 0) {
-      run_item<NRHS, true, 16>(p, T, sin, w, lane, w.abuf + off, bar, phase, t_gath);
+      run_item<NRHS, true, 16>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
       phase ^= 1u;
+    } else if (NRHS == 1 && ring != nullptr && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
+               T.ncols <= kChunkBytes / 8) {
+      run_item_ring1(p, T, sin, w, *ring, rpar, lane, t_gath);
     } else if (stream_u == 4) {
       run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     } else {
@@ -1087,6 +1247,7 @@ struct h2b_op {
   int64_t* d_perm = nullptr;
   double* d_xp = nullptr;  // x in tree order
   int flags = 0;
+  int ring_warps = 0;  // NRHS < 8: TMA-ring warps per CTA (sched_flags bits 4-7)
   std::vector<PhaseDev> ph;
   // multi-GPU
   int rank = 0, world = 1;
@@ -1156,8 +1317,8 @@ int nrhs_index(int nrhs) {
 }
 
 template <int NRHS>
-int occupancy_grid(int wpc, int ctas_per_sm, int* grid) {
-  const size_t sm = (size_t)wpc * (sizeof(WarpSmem) + ring_bytes_per_warp<NRHS>());
+int occupancy_grid(int wpc, int ring_warps, int ctas_per_sm, int* grid) {
+  const size_t sm = smem_bytes(wpc, NRHS >= 8 ? wpc : ring_warps);
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -1196,8 +1357,9 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   p.xp = op->d_xp;
   p.y = y;
   p.flags = op->flags;
+  p.ring_warps = op->ring_warps;
   const int gi = nrhs_index(NRHS);
-  const size_t smem = (size_t)op->wpc * (sizeof(WarpSmem) + ring_bytes_per_warp<NRHS>());
+  const size_t smem = smem_bytes(op->wpc, NRHS >= 8 ? op->wpc : op->ring_warps);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   if (k == 0) {
     const int64_t total = op->n * NRHS;
@@ -1364,6 +1526,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   const int cps = o ? o->ctas_per_sm : 0;
   op->flags = ((o && (o->sched_flags & H2B_SCHED_NEAR_FIRST)) ? 0 : kFlagSlackFirst) |
               (o ? (o->sched_flags & 0x3df3ff00) : 0);
+  op->ring_warps = o ? std::min((o->sched_flags >> 4) & 0xf, op->wpc) : 0;
   op->rank = P.rank;
   op->world = P.world_size;
   op->exch_off = P.exch_off;
@@ -1384,11 +1547,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
-  if ((rc = occupancy_grid<1>(op->wpc, cps, &op->grid[0]))) return rc;
-  if ((rc = occupancy_grid<2>(op->wpc, cps, &op->grid[1]))) return rc;
-  if ((rc = occupancy_grid<4>(op->wpc, cps, &op->grid[2]))) return rc;
-  if ((rc = occupancy_grid<8>(op->wpc, cps, &op->grid[3]))) return rc;
-  if ((rc = occupancy_grid<16>(op->wpc, cps, &op->grid[4]))) return rc;
+  if ((rc = occupancy_grid<1>(op->wpc, op->ring_warps, cps, &op->grid[0]))) return rc;
+  if ((rc = occupancy_grid<2>(op->wpc, op->ring_warps, cps, &op->grid[1]))) return rc;
+  if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, cps, &op->grid[2]))) return rc;
+  if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, cps, &op->grid[4]))) return rc;
   if (op->world > 1 && o && o->nccl_unique_id) {
     ncclUniqueId id;
     std::memcpy(&id, o->nccl_unique_id, sizeof(id));

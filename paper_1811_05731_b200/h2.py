@@ -196,6 +196,10 @@ def SCHED_LEAF_MIX(m: int) -> int:
     return (int(m) & 0xF) << 20
 
 
+def SCHED_RING_WARPS(k: int) -> int:
+    return (int(k) & 0xF) << 4
+
+
 def SCHED_NEAR_PRIO(k: int) -> int:
     return (int(k) & 0xF) << 26
 

@@ -55,7 +55,9 @@ def test_far_and_near_fields_separately(golden):
 @pytest.mark.parametrize("opts", [dict(task_bytes=512), dict(task_bytes=4096, sched_flags=1),
                                   dict(warps_per_cta=4, ctas_per_sm=1),
                                   dict(task_bytes=2048, sched_flags=(15 << 20) | (6 << 26)),
-                                  dict(sched_flags=(2 << 20) | (8 << 26))])
+                                  dict(sched_flags=(2 << 20) | (8 << 26)),
+                                  dict(sched_flags=(3 << 4) | (3 << 26)),
+                                  dict(task_bytes=8192, sched_flags=(8 << 4))])
 def test_plan_variants(opts):
     op, ex = load_golden("config1_sphere4")
     dev = _gpu().DeviceOperator(op, **opts)
@@ -96,6 +98,25 @@ def test_multi_rhs_ring_matches_register_path(name, nrhs):
     assert np.array_equal(ys[0], ys[1])
     for i in range(nrhs):
         assert rel(ys[0][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+
+
+@pytest.mark.parametrize("name", ["config1_sphere4", "prism_20_40_2_default", "torus_32_16_4_default"])
+def test_ring_warps_bit_identical(name):
+    """Single-vector items streamed through a warp's TMA ring run the same
+    column-ordered FMA chain as register-streamed ones: any mix of ring and
+    register warps gives the same bits."""
+    op, ex = load_golden(name)
+    h2 = _gpu()
+    x = ex["X"][:, 0]
+    ys = []
+    for flags in (0, h2.SCHED_RING_WARPS(3) | h2.SCHED_NEAR_PRIO(3), h2.SCHED_RING_WARPS(8)):
+        dev = h2.DeviceOperator(op, sched_flags=flags)
+        try:
+            ys.append(dev.matvec(x))
+        finally:
+            dev.close()
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+    assert rel(ys[0], ex["y_full"][:, 0]) <= TOL
 
 
 @pytest.mark.parametrize("seed", range(3))

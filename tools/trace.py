@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--ablate", default="")
     ap.add_argument("--opts", default="{}")
     ap.add_argument("--save", default="")
+    ap.add_argument("--nrhs", type=int, default=1)
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -49,14 +50,15 @@ def main():
     lib = nat.lib()
     lib.h2b_trace_enable.argtypes = [C.c_void_p, C.c_int]
     lib.h2b_trace_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
-    x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
+    nrhs = a.nrhs
+    x = torch.from_numpy(np.ascontiguousarray(vector_for(a.config, op.n, nrhs))).cuda()
     y = torch.empty_like(x)
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(5):
-        dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s)
+        dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, s)
     nat.check(lib.h2b_trace_enable(dev._h, 1))
     for _ in range(3):
-        dev.matvec_dev(x.data_ptr(), y.data_ptr(), 1, s)
+        dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, s)
     torch.cuda.synchronize()
     T = plan["t_m"].size
     tr = np.zeros((T, 8), np.uint64)
