@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define H2B_ABI_VERSION 1
+#define H2B_ABI_VERSION 2
 
 #define H2B_OK 0
 #define H2B_EINVAL (-1)
@@ -76,6 +76,14 @@ typedef struct h2b_desc {
   const double* const* nr_data; /* [nnear] N_b                              */
 } h2b_desc;
 
+/* sched_flags bit 3: take the flags literally.  Without it, an operator
+   whose matrix pool (this rank's) is at least H2B_STREAM_DEFAULT_BYTES gets
+   the streaming defaults for the fields left zero: every warp a ring warp
+   with 4 KB stages, 6 near-priority warps, leaf mix 2;
+   smaller operators, whose time is the far-field chain's latency, keep
+   plain scheduling. */
+#define H2B_SCHED_EXPLICIT 8
+#define H2B_STREAM_DEFAULT_BYTES (4LL << 30)
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */
 #define H2B_SCHED_NEAR_FIRST 1
@@ -83,6 +91,9 @@ typedef struct h2b_desc {
    CTA a two-stage 8 KB TMA ring for streamed items (16 KB in flight each, no
    registers); 0: register streaming only */
 #define H2B_SCHED_RING_WARPS(k) (((k) & 0xf) << 4)
+/* sched_flags bits 18-19: single-vector ring stage payload: 0 -> 8 KB,
+   1 -> 6 KB, 2 -> 4 KB (smaller stages fit more ring warps per CTA) */
+#define H2B_SCHED_RING_STAGE(s) (((s) & 3) << 18)
 /* sched_flags bits 8-15: warps per CTA that take near-field items (0: all) */
 #define H2B_SCHED_NEAR_WARPS(k) (((k) & 0xff) << 8)
 /* sched_flags bits 16-17: columns in flight per lane of a streamed item:
@@ -134,6 +145,8 @@ typedef struct h2b_stats {
   int32_t warps_per_cta;
   int32_t rank, world_size;
   int64_t local_bytes;      /* bytes this rank streams                     */
+  int32_t sched_flags;      /* effective scheduling (defaults applied)     */
+  int32_t ring_warps;       /* single-vector TMA-ring warps per CTA        */
 } h2b_stats;
 
 /* Plan arrays for host-side inspection (tests execute them with a numpy

@@ -19,6 +19,7 @@ __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
 # H2B_LIB: an alternative build of the library (A/B timing of kernel variants)
 LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
+ABI_VERSION = 2  # include/h2b.h H2B_ABI_VERSION
 H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO = 0, -1, -2, -3, -4, -5, -6
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")
 
@@ -54,6 +55,7 @@ class Stats(C.Structure):
         ("ndeps", C.c_int64), ("tasks_by_kind", C.c_int64 * 5), ("bytes_by_kind", C.c_int64 * 5),
         ("grid", C.c_int32), ("warps_per_cta", C.c_int32), ("rank", C.c_int32),
         ("world_size", C.c_int32), ("local_bytes", C.c_int64),
+        ("sched_flags", C.c_int32), ("ring_warps", C.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -87,6 +89,8 @@ def _load():
             "(there is no CPU fallback for the H² matvec)")
     lib = C.CDLL(os.fspath(LIB_PATH))
     lib.h2b_abi_version.restype = C.c_int
+    if lib.h2b_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{LIB_PATH} has ABI {lib.h2b_abi_version()}, this binding needs {ABI_VERSION}: rebuild it")
     lib.h2b_last_error.restype = C.c_char_p
     lib.h2b_plan_create.argtypes = [C.POINTER(Desc), C.POINTER(Options), C.POINTER(C.c_void_p)]
     lib.h2b_plan_view_get.argtypes = [C.c_void_p, C.POINTER(PlanView)]

@@ -116,6 +116,7 @@ struct KParams {
   int32_t nready0_hi;                   // ready0[0:nready0_hi) are class 0
   int32_t flags;                        // kFlag* scheduling switches (h2b_options.sched_flags)
   int32_t ring_warps;                   // NRHS < 8: warps per CTA (the top ones) with a TMA ring
+  int32_t ring_stage;                   // NRHS < 8: ring stage payload bytes (8192, 6144, 4096)
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
 };
 
@@ -145,16 +146,23 @@ struct __align__(128) WarpSmem {
 // CTA otherwise) stream their items through it; a ring warp stages its
 // far-field items in buf[0].  Other warps have a kStageBytes staging buffer.
 // Dynamic shared memory: [WarpSmem x nw][staging of non-ring warps][rings].
+// Stage payload: 8 KB (multi-RHS, and the single-vector default), or 6 / 4
+// KB for single-vector products (sched_flags bits 18-19), which lets more
+// warps of a CTA own a ring at two CTAs per SM.
 constexpr int kRingStageBytes = 8192;
-struct __align__(128) WarpRing {
-  double buf[2][(kRingStageBytes + 32) / 8];
-  uint64_t bar[2];
+struct WarpRing {  // view into dynamic shared memory (no dynamically indexed arrays)
+  double* base;     // stage 0; stage 1 follows at base + sdbl
+  uint64_t* bars;   // two mbarriers
+  int sdbl;         // stage stride in doubles
+  __device__ __forceinline__ double* buf(int j) const { return base + (j & 1) * sdbl; }
+  __device__ __forceinline__ uint64_t* bar(int j) const { return bars + (j & 1); }
 };
-static_assert(sizeof(WarpRing) % 128 == 0 && kStageBytes % 128 == 0, "staging alignment");
-static_assert((kRingStageBytes + 32) >= kStageBytes, "a ring stage doubles as far-field staging");
-inline size_t smem_bytes(int nw, int ring_warps) {
+__host__ __device__ constexpr int ring_bytes(int stage) { return ((2 * (stage + 32) + 16) + 127) / 128 * 128; }
+static_assert(kStageBytes % 128 == 0 && sizeof(WarpSmem) % 128 == 0, "staging alignment");
+static_assert(2 * (4096 + 32) >= kStageBytes, "a ring (both stages, contiguous) doubles as far-field staging");
+inline size_t smem_bytes(int nw, int ring_warps, int stage) {
   return (size_t)nw * sizeof(WarpSmem) + (size_t)(nw - ring_warps) * kStageBytes +
-         (size_t)ring_warps * sizeof(WarpRing);
+         (size_t)ring_warps * ring_bytes(stage);
 }
 
 __device__ __forceinline__ double ld_stream(const double* p) {
@@ -724,7 +732,7 @@ __device__ __forceinline__ void gather_commit(GatherBatch<NRHS>& g, int lane, in
 // the ring's mbarrier parities (bit s).
 template <int NRHS>
 __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
-                                                  WarpRing& R, unsigned& rpar, int lane,
+                                                  const WarpRing R, unsigned& rpar, int lane,
                                                   unsigned long long& t_gath) {
   constexpr int kHalf = kChunkBytes / (16 * NRHS);  // columns per source half (16 or 32)
   constexpr int NT = NRHS / 8;
@@ -734,7 +742,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   const int g = lane >> 2, t = lane & 3;
   // columns per stage (>= 16), a whole number of 4-column k-steps so that
   // the DMMA sums group columns exactly like the register-staged loop
-  const int cs = min(kHalf, kRingStageBytes / (8 * m)) & ~3;
+  const int cs = min(kHalf, kRingStageBytes / (8 * m)) & ~3;  // multi-RHS rings: 8 KB stages
   const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
@@ -742,7 +750,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     const int cc = min(cs, T.ncols - j * cs);
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
-    bulk_load(R.buf[j & 1], (const void*)a0, (unsigned)(a1 - a0), &R.bar[j & 1]);
+    bulk_load(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
   };
   if (lane == 0) {
     issue(0);
@@ -770,10 +778,10 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     const int cc1 = more ? min(cs, T.ncols - col - cs) : 0;
     if (more) gather_issue<NRHS>(p, w, lane, col + cs, cc1, gb, kseg);
     const int s = jc & 1;
-    mbar_wait(&R.bar[s], (rpar >> s) & 1u);
+    mbar_wait(R.bar(s), (rpar >> s) & 1u);
     rpar ^= 1u << s;
     if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
-    const double* A = R.buf[s] + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* A = R.buf(s) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
     const double* xs = w.xs + (jc & 1) * kHalf * NRHS;
     for (int c = 0; c < cc; c += 4) {
       const bool okc = c + t < cc;
@@ -811,10 +819,10 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
 // once, and every lane runs the same column-ordered FMA chain as run_item,
 // so a ring warp's result is bit-identical to a register-streaming warp's.
 __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
-                                               WarpRing& R, unsigned& rpar, int lane,
+                                               const WarpRing R, unsigned& rpar, int lane,
                                                unsigned long long& t_gath) {
   const int m = T.m;
-  const int cs = kRingStageBytes / (8 * m);  // columns per stage (>= 16)
+  const int cs = p.ring_stage / (8 * m);  // columns per stage (>= 8)
   const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
@@ -822,7 +830,7 @@ __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T,
     const int cc = min(cs, T.ncols - j * cs);
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
-    bulk_load(R.buf[j & 1], (const void*)a0, (unsigned)(a1 - a0), &R.bar[j & 1]);
+    bulk_load(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
   };
   if (lane == 0) {
     issue(0);
@@ -839,10 +847,10 @@ __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T,
     const int col = jc * cs;
     const int cc = min(cs, T.ncols - col);
     const int st = jc & 1;
-    mbar_wait(&R.bar[st], (rpar >> st) & 1u);
+    mbar_wait(R.bar(st), (rpar >> st) & 1u);
     rpar ^= 1u << st;
     if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
-    const double* A = R.buf[st] + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* A = R.buf(st) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
     const double* xs = w.xs + col;
     int c = 0;
     for (; c + 8 <= cc; c += 8) {
@@ -887,17 +895,23 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   // staging: a TMA ring (ring warps) or one far-field buffer
   const int nring = NRHS >= 8 ? nw : p.ring_warps;
   const int first_ring = nw - nring;
-  WarpRing* ring = nullptr;
+  const int rstage = NRHS >= 8 ? kRingStageBytes : p.ring_stage;
+  WarpRing ring_v{nullptr, nullptr, 0};
+  bool has_ring = false;
   double* abuf;
   unsigned rpar = 0;  // ring stage parities (all lanes)
   {
     unsigned char* st = smem_raw + (size_t)nw * sizeof(WarpSmem);
     if (wib >= first_ring) {
-      ring = reinterpret_cast<WarpRing*>(st + (size_t)first_ring * kStageBytes) + (wib - first_ring);
-      abuf = ring->buf[0];
+      unsigned char* rb = st + (size_t)first_ring * kStageBytes + (size_t)(wib - first_ring) * ring_bytes(rstage);
+      ring_v.base = reinterpret_cast<double*>(rb);
+      ring_v.sdbl = (rstage + 32) / 8;
+      ring_v.bars = reinterpret_cast<uint64_t*>(rb + 2 * (rstage + 32));
+      has_ring = true;
+      abuf = ring_v.base;
       if (lane == 0) {
-        mbar_init(&ring->bar[0]);
-        mbar_init(&ring->bar[1]);
+        mbar_init(ring_v.bars);
+        mbar_init(ring_v.bars + 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       }
     } else {
@@ -1087,16 +1101,16 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         run_item_mma<NRHS, true>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
         phase ^= 1u;
       } else if (T.ld == T.m && T.m <= 64 && T.ncols > 0 && !(p.flags & kFlagNoRing)) {  // all warps ring
-        run_item_mma_ring<NRHS>(p, T, sin, w, *ring, rpar, lane, t_gath);
+        run_item_mma_ring<NRHS>(p, T, sin, w, ring_v, rpar, lane, t_gath);
       } else {
         run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       }
     } else if (off >= 0) {
       run_item<NRHS, true, 16>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
       phase ^= 1u;
-    } else if (NRHS == 1 && ring != nullptr && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
+    } else if (NRHS == 1 && has_ring && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
                T.ncols <= kChunkBytes / 8) {
-      run_item_ring1(p, T, sin, w, *ring, rpar, lane, t_gath);
+      run_item_ring1(p, T, sin, w, ring_v, rpar, lane, t_gath);
     } else if (stream_u == 4) {
       run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     } else {
@@ -1248,6 +1262,8 @@ struct h2b_op {
   double* d_xp = nullptr;  // x in tree order
   int flags = 0;
   int ring_warps = 0;  // NRHS < 8: TMA-ring warps per CTA (sched_flags bits 4-7)
+  int sched = 0;       // effective sched_flags (defaults applied)
+  int ring_stage = kRingStageBytes;  // NRHS < 8: ring stage payload (sched_flags bits 18-19)
   std::vector<PhaseDev> ph;
   // multi-GPU
   int rank = 0, world = 1;
@@ -1317,8 +1333,8 @@ int nrhs_index(int nrhs) {
 }
 
 template <int NRHS>
-int occupancy_grid(int wpc, int ring_warps, int ctas_per_sm, int* grid) {
-  const size_t sm = smem_bytes(wpc, NRHS >= 8 ? wpc : ring_warps);
+int occupancy_grid(int wpc, int ring_warps, int ring_stage, int ctas_per_sm, int* grid) {
+  const size_t sm = NRHS >= 8 ? smem_bytes(wpc, wpc, kRingStageBytes) : smem_bytes(wpc, ring_warps, ring_stage);
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -1358,8 +1374,10 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   p.y = y;
   p.flags = op->flags;
   p.ring_warps = op->ring_warps;
+  p.ring_stage = op->ring_stage;
   const int gi = nrhs_index(NRHS);
-  const size_t smem = smem_bytes(op->wpc, NRHS >= 8 ? op->wpc : op->ring_warps);
+  const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kRingStageBytes)
+                                : smem_bytes(op->wpc, op->ring_warps, op->ring_stage);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   if (k == 0) {
     const int64_t total = op->n * NRHS;
@@ -1524,9 +1542,20 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->wpc = (o && o->warps_per_cta > 0) ? o->warps_per_cta : 8;
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
-  op->flags = ((o && (o->sched_flags & H2B_SCHED_NEAR_FIRST)) ? 0 : kFlagSlackFirst) |
-              (o ? (o->sched_flags & 0x3df3ff00) : 0);
-  op->ring_warps = o ? std::min((o->sched_flags >> 4) & 0xf, op->wpc) : 0;
+  int sf = o ? o->sched_flags : 0;
+  if (!(sf & H2B_SCHED_EXPLICIT) && 8 * (int64_t)P.mat.size() >= H2B_STREAM_DEFAULT_BYTES) {
+    // streaming defaults (measured on config 3)
+    if (((sf >> 4) & 0xf) == 0) sf |= H2B_SCHED_RING_WARPS(8) | H2B_SCHED_RING_STAGE(2);
+    if (((sf >> 26) & 0xf) == 0) sf |= H2B_SCHED_NEAR_PRIO(6);
+    if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(2);
+  }
+  op->sched = sf;
+  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3df3ff00);
+  op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
+  {
+    const int sel = (sf >> 18) & 3;
+    op->ring_stage = sel == 1 ? 6144 : sel == 2 ? 4096 : kRingStageBytes;
+  }
   op->rank = P.rank;
   op->world = P.world_size;
   op->exch_off = P.exch_off;
@@ -1547,11 +1576,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
-  if ((rc = occupancy_grid<1>(op->wpc, op->ring_warps, cps, &op->grid[0]))) return rc;
-  if ((rc = occupancy_grid<2>(op->wpc, op->ring_warps, cps, &op->grid[1]))) return rc;
-  if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, cps, &op->grid[2]))) return rc;
-  if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, cps, &op->grid[3]))) return rc;
-  if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, cps, &op->grid[4]))) return rc;
+  if ((rc = occupancy_grid<1>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[0]))) return rc;
+  if ((rc = occupancy_grid<2>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[1]))) return rc;
+  if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[2]))) return rc;
+  if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[4]))) return rc;
   if (op->world > 1 && o && o->nccl_unique_id) {
     ncclUniqueId id;
     std::memcpy(&id, o->nccl_unique_id, sizeof(id));
@@ -1562,6 +1591,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   fill_stats(P, &op->stats);
   op->stats.grid = op->grid[0];
   op->stats.warps_per_cta = op->wpc;
+  op->stats.sched_flags = op->sched;
+  op->stats.ring_warps = op->ring_warps;
   *out = op.release();
   return H2B_OK;
 }

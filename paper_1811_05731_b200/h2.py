@@ -189,6 +189,7 @@ def describe(op) -> _DescHolder:
 
 # h2b_options.sched_flags bits (include/h2b.h)
 SCHED_NEAR_FIRST = 1
+SCHED_EXPLICIT = 8
 SCHED_NO_RING = 1 << 24
 
 
