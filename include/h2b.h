@@ -77,12 +77,14 @@ typedef struct h2b_desc {
 } h2b_desc;
 
 /* sched_flags bit 3: take the flags literally.  Without it, an operator
-   whose matrix pool (this rank's) is at least H2B_STREAM_DEFAULT_BYTES gets
-   the streaming defaults for the fields left zero: every warp a ring warp
-   with 4 KB stages, 6 near-priority warps, leaf mix 2;
-   smaller operators, whose time is the far-field chain's latency, keep
-   plain scheduling. */
+   whose near-field and coupling bytes per rank are at least
+   H2B_STREAM_DEFAULT_BYTES gets the streaming defaults for the fields left
+   zero: every warp a ring warp with 4 KB stages, 6 near-priority warps,
+   leaf mix 2, 8 KB far-field pieces; smaller operators,
+   whose time is the far-field chain's latency, keep plain scheduling. */
 #define H2B_SCHED_EXPLICIT 8
+/* sched_flags bit 2: prefetch the chain successors' descriptors into L1 */
+#define H2B_SCHED_PREFETCH_SUCC 4
 #define H2B_STREAM_DEFAULT_BYTES (4LL << 30)
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */

@@ -123,6 +123,7 @@ struct KParams {
 // scheduling switches
 constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ahead near item
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
+constexpr int kFlagPrefetchSucc = 1 << 2;  // prefetch chain successors' descriptors into L1
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -900,6 +901,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   bool has_ring = false;
   double* abuf;
   unsigned rpar = 0;  // ring stage parities (all lanes)
+  int stage_cap = kStageBytes;  // far-field staging capacity (a ring warp: both stages)
   {
     unsigned char* st = smem_raw + (size_t)nw * sizeof(WarpSmem);
     if (wib >= first_ring) {
@@ -909,6 +911,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       ring_v.bars = reinterpret_cast<uint64_t*>(rb + 2 * (rstage + 32));
       has_ring = true;
       abuf = ring_v.base;
+      stage_cap = 2 * (rstage + 32);
       if (lane == 0) {
         mbar_init(ring_v.bars);
         mbar_init(ring_v.bars + 1);
@@ -1083,6 +1086,13 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     int2 sd_first = make_int2(-1, 0), sd_second = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (s0 + 32 + lane < s1) sd_second = __ldg(p.succ + s0 + 32 + lane);
+    // the chain successors' descriptors into this SM's L1: the continuation
+    // this warp may run next then starts without an L2 round trip
+    if ((p.flags & kFlagPrefetchSucc) && sd_first.x >= 0 && (sd_first.y >> 24) == 0) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.tasks + sd_first.x));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.seg_inline + (int64_t)sd_first.x * kInlineSegs));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.succ0 + sd_first.x));
+    }
     // Far-field items (the latency-critical chain) are staged whole into
     // shared memory by one TMA bulk copy, overlapping the source gather;
     // near-field items stream from global memory.
@@ -1091,7 +1101,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       const double* g0 = p.mat + T.data;
       const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
       const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
-      if (a1 - a0 <= (uintptr_t)kStageBytes) {
+      if (a1 - a0 <= (uintptr_t)stage_cap) {
         if (lane == 0) bulk_load(abuf, (const void*)a0, (unsigned)(a1 - a0), bar);
         off = (int)(((uintptr_t)g0 - a0) >> 3);
       }
@@ -1291,8 +1301,28 @@ namespace {
     if (r_ != ncclSuccess) return fail(H2B_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
-h2b::PlanOptions to_plan_options(const h2b_options* o) {
+// Near-field plus coupling bytes of the operator (the bulk of
+// storage_bytes()), per rank: decides the streaming defaults before planning.
+int64_t desc_stream_bytes_per_rank(const h2b_desc* d, const h2b_options* o) {
+  int64_t b = 0;
+  for (int64_t i = 0; i < d->nnear; ++i) {
+    const int64_t r = d->nr_row[i], c = d->nr_col[i];
+    b += (d->cl_end[r] - d->cl_start[r]) * (d->cl_end[c] - d->cl_start[c]);
+  }
+  for (int64_t i = 0; i < d->ncoupling; ++i) b += d->k_row[d->cp_row[i]] * d->k_col[d->cp_col[i]];
+  const int world = (o && o->world_size > 1) ? o->world_size : 1;
+  return 8 * b / world;
+}
+
+bool streaming_defaults(const h2b_desc* d, const h2b_options* o) {
+  return !(o && (o->sched_flags & H2B_SCHED_EXPLICIT)) && desc_stream_bytes_per_rank(d, o) >= H2B_STREAM_DEFAULT_BYTES;
+}
+
+h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
   h2b::PlanOptions po;
+  // streaming operators: 8 KB chain pieces (a ring warp stages both ring
+  // stages at once), halving the latency-bound up-leaf items
+  if (streaming_defaults(d, o)) po.far_task_bytes = 8192;
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
     if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
@@ -1524,7 +1554,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   }
   h2b::Plan P;
   std::string err;
-  int rc = h2b::build_plan(d, to_plan_options(o), &P, &err);
+  int rc = h2b::build_plan(d, to_plan_options(d, o), &P, &err);
   if (rc != H2B_OK) return fail(rc, err);
   for (const auto& F : P.ph) {
     if (F.ntasks() >= INT32_MAX / kQueues) return fail(H2B_EINVAL, "too many work items");
@@ -1543,14 +1573,14 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
   int sf = o ? o->sched_flags : 0;
-  if (!(sf & H2B_SCHED_EXPLICIT) && 8 * (int64_t)P.mat.size() >= H2B_STREAM_DEFAULT_BYTES) {
+  if (streaming_defaults(d, o)) {
     // streaming defaults (measured on config 3)
     if (((sf >> 4) & 0xf) == 0) sf |= H2B_SCHED_RING_WARPS(8) | H2B_SCHED_RING_STAGE(2);
     if (((sf >> 26) & 0xf) == 0) sf |= H2B_SCHED_NEAR_PRIO(6);
     if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(2);
   }
   op->sched = sf;
-  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3df3ff00);
+  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3df3ff04);
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
     const int sel = (sf >> 18) & 3;
@@ -1659,7 +1689,7 @@ int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
   try {
     std::unique_ptr<h2b_plan> p(new h2b_plan());
     std::string err;
-    int rc = h2b::build_plan(d, to_plan_options(opt), &p->plan, &err);
+    int rc = h2b::build_plan(d, to_plan_options(d, opt), &p->plan, &err);
     if (rc != H2B_OK) return fail(rc, err);
     fill_stats(p->plan, &p->stats);
     *out = p.release();
