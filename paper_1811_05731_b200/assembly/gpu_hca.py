@@ -248,33 +248,67 @@ def hca_gpu(*, bt, bs, lo, hi, start, end, perm, coords, order, eps, evaluator, 
         b2 = qb @ (np.swapaxes(vh, 1, 2) * mask[:, None, :])
         return a2, b2, keep
 
-    jobs, metas = [], []
-    for k in np.unique(kk):
-        k = int(k)
-        sel = np.flatnonzero(kk == k)
-        sel = sel[np.argsort(size[bt[ok[sel]]] + size[s_cl[sel]], kind="stable")]
-        rows = np.maximum(size[bt[ok[sel]]], ncol[sel])  # ascending
-        c0 = 0
-        while c0 < sel.size:
-            # at most 1024 blocks and ~64 MB of padded factors per job
-            cnt = int(min(1024, max(1, (64 << 20) // (16 * k * int(rows[min(sel.size, c0 + 1024) - 1])))))
-            qs = sel[c0:c0 + cnt]
-            c0 += cnt
-            Mt, Ms = int(size[bt[ok[qs]]].max()), int(ncol[qs].max())
-            A = np.zeros((qs.size, Mt, k))
-            Bm = np.zeros((qs.size, Ms, k))
-            for j, q in enumerate(qs):
-                a = a_parts[int(ok[q])]
-                A[j, :a.shape[0]] = a
-                m = int(ncol[q])
-                Bm[j, :m] = bflat[blk_off[q]: blk_off[q + 1]].reshape(k, m).T
-            jobs.append((A, Bm))
-            metas.append(qs)
-    for qs, (a2h, b2h, kh) in zip(metas, _host_pool_map(trunc, jobs)):
+    def job_specs():
+        for k in np.unique(kk):
+            k = int(k)
+            sel = np.flatnonzero(kk == k)
+            sel = sel[np.argsort(size[bt[ok[sel]]] + size[s_cl[sel]], kind="stable")]
+            rows = np.maximum(size[bt[ok[sel]]], ncol[sel])  # ascending
+            c0 = 0
+            while c0 < sel.size:
+                # at most 1024 blocks and ~64 MB of padded factors per job
+                cnt = int(min(1024, max(1, (64 << 20) // (16 * k * int(rows[min(sel.size, c0 + 1024) - 1])))))
+                yield k, sel[c0:c0 + cnt]
+                c0 += cnt
+
+    def run_job(spec):
+        # stack this job's factors (padded), truncate, cut the results back
+        k, qs = spec
+        Mt, Ms = int(size[bt[ok[qs]]].max()), int(ncol[qs].max())
+        A = np.zeros((qs.size, Mt, k))
+        Bm = np.zeros((qs.size, Ms, k))
+        for j, q in enumerate(qs):
+            a = a_parts[int(ok[q])]
+            A[j, :a.shape[0]] = a
+            m = int(ncol[q])
+            Bm[j, :m] = bflat[blk_off[q]: blk_off[q + 1]].reshape(k, m).T
+        a2h, b2h, kh = trunc((A, Bm))
+        res = []
         for j, q in enumerate(qs):
             kq = int(kh[j])
             mt, ms = int(size[bt[ok[q]]]), int(ncol[q])
-            out[int(ok[q])] = ("ok", np.ascontiguousarray(a2h[j, :mt, :kq]),
-                               np.ascontiguousarray(b2h[j, :ms, :kq]))
+            res.append((int(ok[q]), np.ascontiguousarray(a2h[j, :mt, :kq]), np.ascontiguousarray(b2h[j, :ms, :kq])))
+        return res
+
+    # streamed over the host cores with a bounded window of jobs in flight,
+    # so the padded stacks never all exist at once (the 1M-node disk peaked
+    # at 123 GB of host memory when every job was stacked up front)
+    from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait
+    import os
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:
+        lim = None
+    nthr = max(1, min(32, os.cpu_count() or 1))
+    try:
+        with ThreadPoolExecutor(max_workers=nthr) as ex:
+            inflight = set()
+            for spec in job_specs():
+                inflight.add(ex.submit(run_job, spec))
+                if len(inflight) >= 2 * nthr:
+                    done, inflight = wait(inflight, return_when=FIRST_COMPLETED)
+                    for f in done:
+                        for bi, a2, b2 in f.result():
+                            out[bi] = ("ok", a2, b2)
+                            a_parts.pop(bi, None)
+            for f in inflight:
+                for bi, a2, b2 in f.result():
+                    out[bi] = ("ok", a2, b2)
+                    a_parts.pop(bi, None)
+    finally:
+        if lim is not None:
+            lim.restore_original_limits()
+    del bflat
     lap("truncate", t0)
     return out

@@ -411,7 +411,16 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
     by batched HCA on the GPU (assembly/gpu_hca.py) and Gram-based bases in
     the recompression -- the same algorithm to rounding, for the large
     BASELINE workloads."""
-    say = log or (lambda *a: None)
+    _say = log or (lambda *a: None)
+
+    def say(msg):  # with the process's resident / peak memory
+        try:
+            import resource
+            rss = int(open("/proc/self/statm").read().split()[1]) * os.sysconf("SC_PAGE_SIZE") / 1e9
+            peak = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
+            _say(f"{msg} [rss {rss:.1f} GB, peak {peak:.1f} GB]")
+        except (OSError, ValueError):
+            _say(msg)
     times = {}
     t0 = time.perf_counter()
     workers = workers or max(1, min(32, os.cpu_count() or 1))
