@@ -481,9 +481,9 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
             t_c, s_c = int(bt[adm_ids[i]]), int(bs[adm_ids[i]])
             if st == "ok":
                 lowrank[i] = (a, b)
-                # a = Q_a U S, b = Q_b V: B^T B = I, A^T A = S^2 (see recompress)
-                sv = np.linalg.norm(a, axis=0)
-                weights[i] = (np.eye(a.shape[1]), np.diag(sv))
+                # a = Q_a U S, b = Q_b V: B^T B = I, A^T A = S^2 (see recompress):
+                # identity and diagonal weights
+                weights[i] = (None, np.linalg.norm(a, axis=0))
                 continue
             if st == "zero":
                 lowrank[i] = (np.zeros((end[t_c] - start[t_c], 0)), np.zeros((end[s_c] - start[s_c], 0)))
@@ -493,6 +493,7 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
                 lowrank[i] = _aca_block(evaluator, coords, perm, start, end, t_c, s_c, config.eps)
             aa, bb = lowrank[i]
             weights[i] = (np.linalg.qr(bb)[1], np.linalg.qr(aa)[1])
+        del res
         say(f"HCA (gpu): {adm_ids.size} blocks, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s: "
             + ", ".join(f"{k} {times[k]:.1f}s" for k in ("cross", "solve", "rows", "truncate") if k in times) + ")")
         t5 = time.perf_counter()

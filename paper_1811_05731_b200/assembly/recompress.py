@@ -93,12 +93,24 @@ class _Side:
         return self.combine(c, current, kids)
 
 
+def _weighted(f: np.ndarray, w) -> np.ndarray:
+    """f @ w.T for a weight given as a matrix, a diagonal (1-D array) or the
+    identity (None) -- the batched HCA's factors have orthonormal B and
+    A^T A = S^2, so their weights are I and diag(s) and need no k x k
+    matrices (37 GB of them on the 1M-node disk)."""
+    if w is None:
+        return f
+    if w.ndim == 1:
+        return f * w[None, :]
+    return f @ w.T
+
+
 def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0, fast: bool = False):
     """One side of the nested basis.  ``anchored[cid]`` lists (factor,
     weight) of the blocks whose cluster on this side is ``cid``."""
     side = _Side(eps, fast)
     items = [(cid, f, w) for cid, lst in anchored.items() for f, w in lst]
-    mats = list(pool.map(lambda t: t[1] @ t[2].T, items)) if pool else [f @ w.T for _, f, w in items]
+    mats = list(pool.map(lambda t: _weighted(t[1], t[2]), items)) if pool else [_weighted(f, w) for _, f, w in items]
     own: dict = {}
     for (cid, _, _), m in zip(items, mats):
         own.setdefault(cid, []).append((m, tree.clusters[cid].start))
@@ -132,7 +144,8 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
 
     ``weights`` (fast build of large operators): per low-rank block the
     pair (W_b, W_a) with W^T W = B^T B and A^T A, replacing the QR R factors
-    (only R^T R enters the bases); bases then come from Gram matrices."""
+    (only R^T R enters the bases); bases then come from Gram matrices.  A
+    weight may be a matrix, a 1-D diagonal or None (identity)."""
     if eps_rec < 0.0:
         raise ValueError("epsilon_rec must be >= 0")
     pool = None
