@@ -83,6 +83,10 @@ typedef struct h2b_desc {
    leaf mix 2, 8 KB far-field pieces; smaller operators,
    whose time is the far-field chain's latency, keep plain scheduling. */
 #define H2B_SCHED_EXPLICIT 8
+/* sched_flags bit 1 (planning): the final items (y rows) go to the slack
+   queue instead of the chain queue, so leaves whose last dependency lands
+   together do not pull every warp off the near-field stream at once */
+#define H2B_SCHED_FINAL_SLACK 2
 /* sched_flags bit 2: prefetch the chain successors' descriptors into L1 */
 #define H2B_SCHED_PREFETCH_SUCC 4
 #define H2B_STREAM_DEFAULT_BYTES (4LL << 30)

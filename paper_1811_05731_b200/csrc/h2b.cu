@@ -1023,12 +1023,22 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
           break;
         }
         if (nprio) {
+          // near-priority warps apply the leaf mix too: otherwise the leaf
+          // coupling rows wait for the other warps and trail the near field
+          if (leaf_mix && near_run >= leaf_thr && owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) {
+            near_run = 0;
+            break;
+          }
           if (pend >= 0) {
             item = pend;
             pend = -1;
+            ++near_run;
             break;
           }
-          if (!near_done && near_ok && (item = take_near()) >= 0) break;
+          if (!near_done && near_ok && (item = take_near()) >= 0) {
+            ++near_run;
+            break;
+          }
         }
         // class-0 static items (up-leaf) before any slack work
         if (!up_done && near_ok && (item = take_up()) >= 0) break;
@@ -1327,6 +1337,7 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
     if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
     if (o->band_depth > 0) po.band_depth = o->band_depth;
+    if (o->sched_flags & H2B_SCHED_FINAL_SLACK) po.final_class = 2;
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
   }

@@ -421,7 +421,7 @@ int Builder::run(std::string* err) {
     if (k > 0 && yhat_[l].exists())
       segs.push_back({kSegCoef, 0, k, &yhat_[l], d->row_basis[l], true, k});
     cur_cl_ = l;
-    emit_group(kFinal, 0, (int32_t)size(l), segs, nullptr, d->cl_start[l], &nearv_[l], false);
+    emit_group(kFinal, 0, (int32_t)size(l), segs, nullptr, d->cl_start[l], &nearv_[l], false, opt_.final_class);
   }
   // Entries never read by the product (e.g. row bases of an operator
   // without coupling blocks) are not packed, so the pool can be smaller.

@@ -49,6 +49,16 @@ def test_plan_far_and_near_ablations(golden):
         assert rel(y, ref) <= 1e-13, (name, key)
 
 
+@pytest.mark.parametrize("opts", [dict(far_task_bytes=8192), dict(sched_flags=2), dict(sched_flags=2, far_task_bytes=8192)])
+def test_plan_streaming_options(golden, opts):
+    """The planning side of the streaming defaults (8 KB far-field pieces,
+    finals in the slack queue) keeps the product exact."""
+    name, op, ex = golden
+    P = plan_view(op, **opts)
+    check_plan_invariants(P)
+    assert rel(run_plan(P, ex["X"][:, 0]), ex["y_full"][:, 0]) <= 1e-14
+
+
 def test_plan_small_items(golden):
     name, op, ex = golden
     P = plan_view(op, task_bytes=256)
