@@ -112,6 +112,9 @@ typedef struct h2b_desc {
 /* sched_flags bit 24: multi-RHS items stream through registers instead of
    the per-warp TMA ring (A/B switch) */
 #define H2B_SCHED_NO_RING (1 << 24)
+/* sched_flags bit 25: TMA-ring copies carry an L2 evict-first hint (the
+   streamed matrix is read once; the gathered sources should stay in L2) */
+#define H2B_SCHED_STREAM_EVICT_FIRST (1 << 25)
 /* sched_flags bits 26-29: the top k warps of each CTA take near-field items
    before the up-leaf items and the coupling queues (0: none) */
 #define H2B_SCHED_NEAR_PRIO(k) (((k) & 0xf) << 26)

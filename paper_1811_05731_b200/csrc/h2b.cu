@@ -124,6 +124,7 @@ struct KParams {
 constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ahead near item
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
 constexpr int kFlagPrefetchSucc = 1 << 2;  // prefetch chain successors' descriptors into L1
+constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -217,6 +218,29 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// The same with an L2 eviction-priority hint (createpolicy): the streamed
+// matrix is read once, so it should not evict the gathered sources.
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                               uint64_t policy) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// ring copies: with an evict-first hint when the stream_ef flag is set
+__device__ __forceinline__ void ring_load(const KParams& p, void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  if (p.flags & kFlagStreamEvictFirst) bulk_load_hint(dst, src, bytes, bar, evict_first_policy());
+  else bulk_load(dst, src, bytes, bar);
 }
 
 // xp = x[perm] (h2.py:192-193), node-major with NRHS columns.
@@ -751,7 +775,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     const int cc = min(cs, T.ncols - j * cs);
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
-    bulk_load(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+    ring_load(p, R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
   };
   if (lane == 0) {
     issue(0);
@@ -831,7 +855,7 @@ __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T,
     const int cc = min(cs, T.ncols - j * cs);
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
-    bulk_load(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+    ring_load(p, R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
   };
   if (lane == 0) {
     issue(0);
@@ -1591,7 +1615,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(8);
   }
   op->sched = sf;
-  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3df3ff04);
+  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3ff3ff04);
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
     const int sel = (sf >> 18) & 3;
