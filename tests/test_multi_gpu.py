@@ -118,9 +118,14 @@ def test_two_processes_gloo(tmp_path):
     assert "REL_ERR" in outs[0]
 
 
+# the streaming defaults a large rank operator gets, forced
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (8 << 20), far_task_bytes=8192)
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("opts", [{}, STREAMING])
 @pytest.mark.parametrize("world", [2, 4])
-def test_virtual_ranks_on_one_gpu(world):
+def test_virtual_ranks_on_one_gpu(world, opts):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -129,7 +134,7 @@ def test_virtual_ranks_on_one_gpu(world):
     from paper_1811_05731_b200.h2 import DeviceOperator
     for name in ("config1_sphere4", "prism_20_40_2_default"):
         op, ex = load_golden(name)
-        devs = [DeviceOperator(op, world_size=world, rank=r) for r in range(world)]
+        devs = [DeviceOperator(op, world_size=world, rank=r, **opts) for r in range(world)]
         x = torch.from_numpy(ex["X"][:, 0]).cuda()
         ys = [torch.zeros_like(x) for _ in range(world)]
         s = torch.cuda.current_stream().cuda_stream
@@ -143,7 +148,7 @@ def test_virtual_ranks_on_one_gpu(world):
             for r, d in enumerate(devs):
                 d.matvec_phase(1, x.data_ptr(), ys[r].data_ptr(), 1, s)
             torch.cuda.synchronize()
-            plans = [plan_view(op, world_size=world, rank=r) for r in range(world)]
+            plans = [plan_view(op, world_size=world, rank=r, **opts) for r in range(world)]
             y = np.zeros(op.n)
             for r in range(world):
                 lo, hi = plans[r]["rank_lo_hi"][r]
