@@ -1613,6 +1613,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     if (((sf >> 4) & 0xf) == 0) sf |= H2B_SCHED_RING_WARPS(8) | H2B_SCHED_RING_STAGE(2);
     if (((sf >> 26) & 0xf) == 0) sf |= H2B_SCHED_NEAR_PRIO(6);
     if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(8);
+    sf |= H2B_SCHED_STREAM_EVICT_FIRST;
   }
   op->sched = sf;
   op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3ff3ff04);
