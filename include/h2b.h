@@ -49,6 +49,7 @@ extern "C" {
 #define H2B_ENOMEM (-4)
 #define H2B_ENODEV (-5)
 #define H2B_EIO (-6)     /* corrupt or incompatible operator file (OperatorIOError) */
+#define H2B_ECONV (-7)   /* solver breakdown (ConvergenceError, errors.py) */
 
 /* One H2Matrix, as the reference holds it (h2.py:23-42, cluster.py:13-59).
  * Host arrays; they are only read during h2b_create / h2b_plan_create and may
@@ -265,6 +266,24 @@ int h2b_colloc_eval(h2b_colloc* c, int64_t njobs, const double* points, const in
                     const int32_t* col_count, const int64_t* diag_node, const int64_t* out_off,
                     int64_t ncolidx, const int64_t* colidx, int64_t out_len, double* out);
 void h2b_colloc_destroy(h2b_colloc* c);
+
+/* ---- FEM solves either side of the boundary operator --
+ * Jacobi-preconditioned CG with optional deflation of the constant mode:
+ * solver.py:44-98 cg_solve(a, b, tol, max_iter, deflate_constants,
+ * precond=jacobi_preconditioner(a)), as called by fem.py:79-121 solve_u1
+ * (deflate = 1) and solve_u2 (deflate = 0, on the interior block).  The
+ * matrix is CSR (int64 row_ptr, int32 columns), symmetric positive
+ * (semi-)definite with a zero-free diagonal (else H2B_EINVAL, like
+ * jacobi_preconditioner's ValueError).  max_iter <= 0 means 10 n.  A
+ * non-positive p'Ap returns H2B_ECONV.  The caller checks the deflated
+ * right-hand side's compatibility (solver.py:68-70). */
+typedef struct h2b_cg h2b_cg;
+int h2b_cg_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val, h2b_cg** out);
+int h2b_cg_solve(h2b_cg* c, const double* b_host, double* x_host, double tol, int deflate, int64_t max_iter,
+                 int64_t* iterations, double* residual);
+int h2b_cg_solve_dev(h2b_cg* c, const double* b_dev, double* x_dev, double tol, int deflate, int64_t max_iter,
+                     int64_t* iterations, double* residual, void* stream);
+void h2b_cg_destroy(h2b_cg* c);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
 LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
 ABI_VERSION = 2  # include/h2b.h H2B_ABI_VERSION
-H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO = 0, -1, -2, -3, -4, -5, -6
+H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO, H2B_ECONV = 0, -1, -2, -3, -4, -5, -6, -7
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")
 
 _p64 = C.POINTER(C.c_int64)
@@ -92,6 +92,15 @@ def _load():
     if lib.h2b_abi_version() != ABI_VERSION:
         raise RuntimeError(f"{LIB_PATH} has ABI {lib.h2b_abi_version()}, this binding needs {ABI_VERSION}: rebuild it")
     lib.h2b_last_error.restype = C.c_char_p
+    # FEM solves (csrc/cg.cu)
+    lib.h2b_cg_create.argtypes = [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_void_p)]
+    lib.h2b_cg_solve.argtypes = [C.c_void_p, _pd, _pd, C.c_double, C.c_int, C.c_int64, C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_double)]
+    lib.h2b_cg_solve_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int64,
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_void_p]
+    lib.h2b_cg_destroy.argtypes = [C.c_void_p]
+    lib.h2b_cg_destroy.restype = None
     lib.h2b_plan_create.argtypes = [C.POINTER(Desc), C.POINTER(Options), C.POINTER(C.c_void_p)]
     lib.h2b_plan_view_get.argtypes = [C.c_void_p, C.POINTER(PlanView)]
     lib.h2b_plan_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]

@@ -1,0 +1,114 @@
+"""The FEM solves either side of the boundary operator:
+host assembly restated from fem.py (checked against the oracle restatement
+on CPU), and the GPU Jacobi-PCG (csrc/cg.cu) against the oracle's CG
+(solver.py:44-98 restated) on the same systems.
+
+CG tolerance: the GPU sums the dot products in a different order than
+numpy, so iterates agree to the solve tolerance (tol = 1e-10 relative
+residual), not bit for bit; the energy of the uniformly magnetized sphere
+(pipeline.py:46-63) is compared at 1e-9 relative, the iteration counts to
+within 2.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel
+
+gpu = pytest.mark.gpu
+
+
+def _mesh():
+    from oracle.mesh_ref import generate_sphere_mesh
+    return generate_sphere_mesh(1.0, 4)
+
+
+def test_assembly_matches_oracle_restatement():
+    from oracle import fem_ref
+    from paper_1811_05731_b200 import fem
+    mesh = _mesh()
+    vols, g = fem.tet_gradients(mesh)
+    vo, go = fem_ref._gradients(mesh.nodes, mesh.tets)
+    assert np.array_equal(vols, vo) and np.array_equal(g, go)
+    a = fem.assemble_stiffness(mesh)
+    ao = fem_ref._stiffness(mesh.nodes, mesh.tets, vo, go)
+    assert (a != ao).nnz == 0
+    m = np.zeros((mesh.n_nodes, 3))
+    m[:, 2] = 1.0
+    b = fem.assemble_u1_rhs(mesh, m)
+    assert abs(b.sum()) <= 1e-10 * np.abs(b).sum()   # compatible with the constant kernel
+    with pytest.raises(ValueError, match="magnetization must have shape"):
+        fem.assemble_u1_rhs(mesh, m[:-1])
+
+
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+@gpu
+@pytest.mark.parametrize("deflate", [True, False])
+def test_gpu_cg_matches_oracle_cg(deflate):
+    _cuda()
+    from oracle.fem_ref import _pcg
+    from paper_1811_05731_b200 import fem
+    mesh = _mesh()
+    a = fem.assemble_stiffness(mesh)
+    rng = np.random.default_rng(5)
+    if deflate:
+        m = rng.standard_normal((mesh.n_nodes, 3))
+        b = fem.assemble_u1_rhs(mesh, m)
+        mat = a
+    else:
+        interior = np.setdiff1d(np.arange(mesh.n_nodes), mesh.boundary_nodes)
+        mat = a[interior][:, interior].tocsr()
+        b = rng.standard_normal(interior.size)
+    x, rep = fem.cg_solve(mat, b, tol=1e-10, deflate_constants=deflate)
+    xo, ito = _pcg(mat, b, 1e-10, deflate)
+    assert rep.converged and rep.residual <= 1e-10
+    assert abs(rep.iterations - ito) <= 2
+    assert rel(x, xo) <= 1e-8
+    bb = b - b.mean() if deflate else b
+    assert np.linalg.norm(bb - mat @ x) <= 1.5e-10 * np.linalg.norm(b)
+    if deflate:
+        assert abs(x.mean()) <= 1e-14 * np.abs(x).max()
+
+
+@gpu
+def test_gpu_cg_contract():
+    _cuda()
+    from scipy.sparse import csr_matrix, diags
+    from paper_1811_05731_b200 import fem
+    a = diags([2.0, 3.0, 4.0]).tocsr()
+    x, rep = fem.cg_solve(a, np.zeros(3))
+    assert rep.iterations == 0 and np.array_equal(x, np.zeros(3))
+    x, rep = fem.cg_solve(a, np.array([2.0, 3.0, 4.0]))
+    assert np.allclose(x, 1.0) and rep.converged
+    with pytest.raises(ValueError, match="zero-free diagonal"):
+        fem.GpuCG(csr_matrix(np.array([[0.0, 1.0], [1.0, 2.0]])))
+    with pytest.raises(ValueError, match="incompatible rhs"):
+        fem.cg_solve(a, np.array([1.0, 1.0, 1.0]), deflate_constants=True)
+    with pytest.raises(fem.ConvergenceError, match="negative curvature"):
+        fem.cg_solve(diags([-1.0, -2.0]).tocsr(), np.array([1.0, 1.0]))
+
+
+@gpu
+def test_sphere_energy_with_gpu_solves_and_product():
+    """compute_demag with both solves and the H² product on the GPU matches
+    the reference energy e_d/K_d = 0.3329597004200991 (config 1)."""
+    _cuda()
+    from paper_1811_05731_b200.bem import BoundaryOperator
+    from paper_1811_05731_b200.pipeline import compute_demag
+    op, ex = load_golden("config1_sphere4")
+    mesh = _mesh()
+    m = np.zeros((mesh.n_nodes, 3))
+    m[:, 2] = 1.0
+    bop = BoundaryOperator(backend="h2", n=op.n, diag=np.zeros(op.n), payload=op)
+    res = compute_demag(mesh, m, bop)
+    ref = float(ex["energy_e_d_over_kd"])
+    assert abs(res.e_d_over_kd - ref) <= 1e-9 * abs(ref)
+    assert abs(res.u1_iterations - 248) <= 2 and abs(res.u2_iterations - 217) <= 2
+    assert rel(res.u2[mesh.boundary_nodes], ex["energy_u2_boundary"]) <= 1e-8
