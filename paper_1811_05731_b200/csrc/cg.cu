@@ -16,7 +16,7 @@
 // deflated z is formed as r'z0 - mean(z0) sum(r) (the same value in exact
 // arithmetic).  Iterates therefore agree to the solve tolerance, not bit for
 // bit.  The sparse product is HBM-bound (12 bytes per stored entry plus the
-// vectors); one warp-quarter (8 lanes) per row.
+// vectors); four lanes per row.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -43,7 +43,7 @@ int gfail(int code, const std::string& m) { return h2b_detail::set_error(code, m
   } while (0)
 
 constexpr int kThreads = 256;
-constexpr int kLanesPerRow = 8;
+constexpr int kLanesPerRow = 4;
 constexpr int kParts = 5;  // partial sums per CTA: p'Ap | r'z0, sum z0, sum r, r'r
 
 struct CGParams {
@@ -169,7 +169,21 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGParams P) {
       double v = 0.0;
       if (i < hi) {
         const int64_t e0 = P.rp[i], e1 = P.rp[i + 1];
-        for (int64_t e = e0 + sl; e < e1; e += kLanesPerRow) v += P.va[e] * __ldcg(P.p + P.ci[e]);
+        // four entries per lane per step, their loads issued together
+        for (int64_t e = e0 + sl; e < e1; e += 4 * kLanesPerRow) {
+          int c[4];
+          double a[4], q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t eu = e + u * kLanesPerRow;
+            c[u] = eu < e1 ? __ldg(P.ci + eu) : -1;
+            a[u] = eu < e1 ? __ldg(P.va + eu) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = c[u] >= 0 ? __ldcg(P.p + c[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v += a[u] * q[u];
+        }
       }
 #pragma unroll
       for (int o = kLanesPerRow / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, kLanesPerRow);
@@ -300,8 +314,11 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_kernel, kThreads, 0));
   CG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   if (per_sm < 1) return gfail(H2B_ECUDA, "cg kernel does not fit on an SM");
-  // one CTA per SM (co-resident for the grid barrier); fewer for small n
-  c->grid = (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (n + kThreads - 1) / kThreads));
+  // co-resident CTAs for the grid barrier: up to 4 per SM (the gathers of
+  // the sparse product need the memory-level parallelism; every CTA reads
+  // all partial sums after a barrier, so more CTAs cost L2 traffic)
+  c->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::min(per_sm, 4) * nsm,
+                                                        (n + kThreads - 1) / kThreads));
   CG_CUDA(cudaMalloc(&c->part, sizeof(double) * kParts * c->grid));
   CG_CUDA(cudaMalloc(&c->out, sizeof(double) * 4));
   int* d_zero = nullptr;
