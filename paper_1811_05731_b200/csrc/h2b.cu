@@ -125,6 +125,7 @@ constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ah
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
 constexpr int kFlagPrefetchSucc = 1 << 2;  // prefetch chain successors' descriptors into L1
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
+constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -1043,7 +1044,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
             atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
-        } else if (h[0] < t[0] && (item = claim(0)) >= 0) {
+        } else if (h[0] < t[0] && !(nprio && (p.flags & kFlagPrioNoChain)) && (item = claim(0)) >= 0) {
           break;
         }
         if (nprio) {
@@ -1616,7 +1617,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     sf |= H2B_SCHED_STREAM_EVICT_FIRST;
   }
   op->sched = sf;
-  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x3ff3ff04);
+  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x7ff3ff04);
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
     const int sel = (sf >> 18) & 3;
