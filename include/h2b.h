@@ -89,8 +89,10 @@ typedef struct h2b_desc {
    queue instead of the chain queue, so leaves whose last dependency lands
    together do not pull every warp off the near-field stream at once */
 #define H2B_SCHED_FINAL_SLACK 2
-/* sched_flags bit 2: prefetch the chain successors' descriptors into L1 */
-#define H2B_SCHED_PREFETCH_SUCC 4
+/* sched_flags bit 2: arrival counts by release-only atomics; only a warp
+   that completes a successor acquires (fence), instead of every arrival
+   being an acquire (which invalidates the SM's L1) */
+#define H2B_SCHED_RELEASE_ARRIVALS 4
 #define H2B_STREAM_DEFAULT_BYTES (4LL << 30)
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */

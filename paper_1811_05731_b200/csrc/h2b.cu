@@ -123,7 +123,7 @@ struct KParams {
 // scheduling switches
 constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ahead near item
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
-constexpr int kFlagPrefetchSucc = 1 << 2;  // prefetch chain successors' descriptors into L1
+constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, acquire fence on completion
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
 constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -190,6 +190,13 @@ __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gp
 __device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
   unsigned long long old;
   asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+// Release-only arrival: publishes this warp's outputs without the L1
+// invalidation an acquire costs; the completing warp acquires with a fence.
+__device__ __forceinline__ unsigned long long atom_add_release(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
 }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -1121,13 +1128,6 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     int2 sd_first = make_int2(-1, 0), sd_second = make_int2(-1, 0);
     if (s0 + lane < s1) sd_first = __ldg(p.succ + s0 + lane);
     if (s0 + 32 + lane < s1) sd_second = __ldg(p.succ + s0 + 32 + lane);
-    // the chain successors' descriptors into this SM's L1: the continuation
-    // this warp may run next then starts without an L2 round trip
-    if ((p.flags & kFlagPrefetchSucc) && sd_first.x >= 0 && (sd_first.y >> 24) == 0) {
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.tasks + sd_first.x));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.seg_inline + (int64_t)sd_first.x * kInlineSegs));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.succ0 + sd_first.x));
-    }
     // Far-field items (the latency-critical chain) are staged whole into
     // shared memory by one TMA bulk copy, overlapping the source gather;
     // near-field items stream from global memory.
@@ -1180,7 +1180,9 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
           const int2 sd = (k0 == s0 && u == 0) ? sd_first
                           : (k0 == s0 && u == 1) ? sd_second : __ldg(p.succ + k);
           const unsigned ndep = (unsigned)sd.y & 0xffffffu;
-          if (atom_add_acq_rel(p.arrived + sd.x, 1ull) + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
+          const unsigned long long old = (p.flags & kFlagReleaseArrivals) ? atom_add_release(p.arrived + sd.x, 1ull)
+                                                                          : atom_add_acq_rel(p.arrived + sd.x, 1ull);
+          if (old + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
           qq[u] = sd.y >> 24;
         }
       }
@@ -1190,6 +1192,10 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
 #pragma unroll
       for (int u = 0; u < 4; ++u) any |= __ballot_sync(0xffffffffu, dd[u] >= 0);
       if (!any) continue;
+      // release-only arrivals: the warp that completes a successor acquires
+      // the other producers' outputs here (acquire pattern: the atomic's
+      // read, then a fence), before running or publishing it
+      if (p.flags & kFlagReleaseArrivals) fence_acq_rel();
       if (cont < 0) {
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass)
