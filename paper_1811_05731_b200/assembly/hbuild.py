@@ -502,11 +502,12 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
                         [(int(bt[adm_ids[i]]), int(bs[adm_ids[i]]), lowrank[i][0], lowrank[i][1])
                          for i in range(adm_ids.size)],
                         [(int(dt[i]), int(ds[i]), near_mats[i]) for i in range(dense_ids.size)],
-                        config.eps_rec, workers=workers, weights=weights)
+                        config.eps_rec, workers=workers, weights=weights, timings=times)
         times["recompress"] = time.perf_counter() - t5
         times["total"] = time.perf_counter() - t0
-        say(f"recompress {times['recompress']:.1f}s; H² {op.storage_bytes() / 1e6:.1f} MB; "
-            f"total {times['total']:.1f}s")
+        say(f"recompress {times['recompress']:.1f}s (bases rows {times.get('rec_rows', 0):.1f}s, cols "
+            f"{times.get('rec_cols', 0):.1f}s, coupling {times.get('rec_coupling', 0):.1f}s); "
+            f"H² {op.storage_bytes() / 1e6:.1f} MB; total {times['total']:.1f}s")
         rep = BuildReport(n=surface.n, nclusters=len(cl), n_admissible=int(adm_ids.size),
                           n_dense=int(dense_ids.size), n_fallback=n_fb, seconds=times)
         return op, rep

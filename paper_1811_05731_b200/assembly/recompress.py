@@ -19,6 +19,7 @@ serial recursion operation for operation.
 from __future__ import annotations
 
 import os
+import time
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -138,7 +139,7 @@ def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0
 
 
 def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers: int = 1,
-               weights: list | None = None) -> H2Matrix:
+               weights: list | None = None, timings: dict | None = None) -> H2Matrix:
     """``lowrank``: (row cid, col cid, A, B) with block = A @ B.T, in leaf-
     block order; ``dense``: (row cid, col cid, matrix).
 
@@ -176,8 +177,13 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
             rows.setdefault(t, []).append((a, rb))
             cols.setdefault(s, []).append((b, ra))
         depth = max(1, int(np.ceil(np.log2(max(2, 4 * workers))))) if pool else 0
+        t0 = time.perf_counter()
         rbasis, rtrans, rexp = basis_side(tree, rows, eps_rec, pool, depth, fast)
+        t1 = time.perf_counter()
         cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec, pool, depth, fast)
+        t2 = time.perf_counter()
+        if timings is not None:
+            timings.update(rec_rows=t1 - t0, rec_cols=t2 - t1)
         op = H2Matrix(tree=tree, n=n, row_basis=rbasis, row_transfer=rtrans,
                       col_basis=cbasis, col_transfer=ctrans)
 
@@ -186,6 +192,8 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
             return (t, s, (rexp[t].T @ a) @ (b.T @ cexp[s]))
 
         op.coupling.extend(pool.map(coupling, lowrank) if pool else map(coupling, lowrank))
+        if timings is not None:
+            timings.update(rec_coupling=time.perf_counter() - t2)
         for t, s, m in dense:
             op.near.append((t, s, m))
         return op
