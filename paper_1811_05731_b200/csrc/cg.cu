@@ -163,33 +163,66 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGParams P) {
   const int rows_per_pass = kThreads / kLanesPerRow;
   while (res > P.tol && it < P.max_iter) {
     // ---- A: ap = A p on this CTA's rows, partial p'Ap
+    // four rows per lane group per pass, all their loads issued together
+    // (the row pointers, then up to 4 entries per lane of each row, then
+    // the gathers): the sparse product is latency-bound otherwise.  The
+    // per-lane and per-row summation order is that of a row-at-a-time loop.
+    constexpr int U = 4;
     double s_pap = 0.0;
-    for (int64_t r0 = lo; r0 < hi; r0 += rows_per_pass) {
-      const int64_t i = r0 + sub;
-      double v = 0.0;
-      if (i < hi) {
-        const int64_t e0 = P.rp[i], e1 = P.rp[i + 1];
-        // four entries per lane per step, their loads issued together
-        for (int64_t e = e0 + sl; e < e1; e += 4 * kLanesPerRow) {
-          int c[4];
-          double a[4], q[4];
+    for (int64_t r0 = lo; r0 < hi; r0 += (int64_t)rows_per_pass * U) {
+      int64_t e0[U], e1[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t ik = r0 + k * rows_per_pass + sub;
+        e0[k] = ik < hi ? __ldg(P.rp + ik) : 0;
+        e1[k] = ik < hi ? __ldg(P.rp + ik + 1) : 0;
+      }
+      double v[U];
+      int c[U][4];
+      double a[U][4];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t eu = e0[k] + sl + u * kLanesPerRow;
+          c[k][u] = eu < e1[k] ? __ldg(P.ci + eu) : -1;
+          a[k][u] = eu < e1[k] ? __ldg(P.va + eu) : 0.0;
+        }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        double q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = c[k][u] >= 0 ? __ldcg(P.p + c[k][u]) : 0.0;
+        v[k] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[k] += a[k][u] * q[u];
+      }
+      // rows longer than 4 entries per lane
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        for (int64_t e = e0[k] + sl + 4 * kLanesPerRow; e < e1[k]; e += 4 * kLanesPerRow) {
+          int cc[4];
+          double aa[4], q[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int64_t eu = e + u * kLanesPerRow;
-            c[u] = eu < e1 ? __ldg(P.ci + eu) : -1;
-            a[u] = eu < e1 ? __ldg(P.va + eu) : 0.0;
+            cc[u] = eu < e1[k] ? __ldg(P.ci + eu) : -1;
+            aa[u] = eu < e1[k] ? __ldg(P.va + eu) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) q[u] = c[u] >= 0 ? __ldcg(P.p + c[u]) : 0.0;
+          for (int u = 0; u < 4; ++u) q[u] = cc[u] >= 0 ? __ldcg(P.p + cc[u]) : 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) v += a[u] * q[u];
+          for (int u = 0; u < 4; ++u) v[k] += aa[u] * q[u];
         }
-      }
 #pragma unroll
-      for (int o = kLanesPerRow / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, kLanesPerRow);
-      if (i < hi && sl == 0) {
-        P.ap[i] = v;
-        s_pap += v * P.p[i];
+      for (int k = 0; k < U; ++k) {
+#pragma unroll
+        for (int o = kLanesPerRow / 2; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o, kLanesPerRow);
+        const int64_t ik = r0 + k * rows_per_pass + sub;
+        if (ik < hi && sl == 0) {
+          P.ap[ik] = v[k];
+          s_pap += v[k] * P.p[ik];
+        }
       }
     }
     s_pap = block_sum(s_pap, scratch);
