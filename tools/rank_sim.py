@@ -1,0 +1,70 @@
+"""Per-rank time of the sharded product, one rank at a time on one GPU.
+
+    python tools/rank_sim.py --config config3 --worlds 2,4,8 [--steps 30]
+
+For each world size and rank, the rank operator runs its two
+phases back to back on the local GPU; the all-gather between them is left
+out (its ~N_coef·8 bytes per rank move over NVLink in microseconds), so the
+coefficients phase 1 reads are stale -- the work and the bytes are the
+same, the values are not checked.  The max over ranks models the step time
+of an N-GPU run; ranks never wait on each other here.  Both scheduling
+modes are timed (plain, and the streaming defaults forced) to place the
+H2B_STREAM_DEFAULT_BYTES threshold."""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (8 << 20) | (1 << 25), far_task_bytes=8192)
+PLAIN = dict(sched_flags=8)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="config3")
+    ap.add_argument("--worlds", default="2,4,8")
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
+    a = ap.parse_args()
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1811_05731_b200.h2 import DeviceOperator
+    from paper_1811_05731_b200.workloads import build_workload, vector_for
+    op, _ = build_workload(a.config, cache_dir=a.cache_dir, log=lambda m: print(m, file=sys.stderr))
+    x = torch.from_numpy(vector_for(a.config, op.n)).cuda()
+    y = torch.zeros_like(x)
+    s = torch.cuda.current_stream()
+    for world in [int(w) for w in a.worlds.split(",")]:
+        for mode, opts in (("plain", PLAIN), ("streaming", STREAMING)):
+            per_rank = []
+            for r in range(world):
+                dev = DeviceOperator(op, world_size=world, rank=r, **opts)
+                st = dev.stats()
+                run = lambda: (dev.matvec_phase(0, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream),
+                               dev.matvec_phase(1, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream))
+                for _ in range(3):
+                    run()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                for _ in range(a.steps):
+                    run()
+                e1.record(s)
+                torch.cuda.synchronize()
+                per_rank.append((e0.elapsed_time(e1) / a.steps, int(st["local_bytes"])))
+                dev.close()
+            t = max(p[0] for p in per_rank)
+            print(json.dumps({"config": a.config, "world": world, "mode": mode, "max_rank_ms": round(t, 4),
+                              "rank_ms": [round(p[0], 4) for p in per_rank],
+                              "rank_bytes": [p[1] for p in per_rank],
+                              "modeled_DOF_per_s": op.n / (t * 1e-3)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
