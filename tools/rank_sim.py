@@ -47,8 +47,9 @@ def main():
             for r in range(world):
                 dev = DeviceOperator(op, world_size=world, rank=r, **opts)
                 st = dev.stats()
-                run = lambda: (dev.matvec_phase(0, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream),
-                               dev.matvec_phase(1, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream))
+                phases = 1 if world == 1 else 2
+                run = lambda: [dev.matvec_phase(k, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
+                               for k in range(phases)]
                 for _ in range(3):
                     run()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
