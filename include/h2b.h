@@ -143,6 +143,11 @@ typedef struct h2b_options {
   int32_t rank;
   int32_t world_size;
   const void* nccl_unique_id; /* 128-byte ncclUniqueId shared by all ranks  */
+  int32_t near_phase0_pct; /* multi-GPU: share (percent of bytes, 1-100) of
+                              the rank's near field run in phase 0, beside the
+                              latency-bound upward pass; 0 = default (50),
+                              -1 = none (all in phase 1)                    */
+  int32_t pad_;
 } h2b_options;
 
 typedef struct h2b_op h2b_op;      /* device-resident operator             */

@@ -45,6 +45,7 @@ class Options(C.Structure):
         ("task_bytes", C.c_int64), ("far_task_bytes", C.c_int64), ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
         ("max_nrhs", C.c_int32), ("sched_flags", C.c_int32), ("band_depth", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
+        ("near_phase0_pct", C.c_int32), ("pad_", C.c_int32),
     ]
 
 

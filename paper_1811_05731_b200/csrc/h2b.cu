@@ -1369,6 +1369,8 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
     if (o->band_depth > 0) po.band_depth = o->band_depth;
     if (o->sched_flags & H2B_SCHED_FINAL_SLACK) po.final_class = 2;
+    if (o->near_phase0_pct < 0) po.near_phase0_pct = 0;
+    else if (o->near_phase0_pct > 0) po.near_phase0_pct = std::min(100, o->near_phase0_pct);
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
   }

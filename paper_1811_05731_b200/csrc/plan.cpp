@@ -489,6 +489,22 @@ int Builder::run(std::string* err) {
       sel[i] = 1; in1[i] = 1;
     }
   }
+  // Part of the near field moves to phase 0: it needs only x (replicated),
+  // and streams while the upward pass -- a latency-bound chain with little
+  // work -- runs; the rest stays in phase 1 beside the downward chain.  The
+  // finals in phase 1 then find those partial slots already written.
+  if (opt_.near_phase0_pct > 0) {
+    int64_t total = 0, moved_b = 0;
+    for (int32_t i = 0; i < T; ++i)
+      if (sel[i] && tasks_[i].kind == kNear) total += 8 * (int64_t)tasks_[i].m * tasks_[i].ncols;
+    const int64_t goal = total * opt_.near_phase0_pct / 100;
+    for (int32_t i = 0; i < T && moved_b < goal; ++i)
+      if (sel[i] && tasks_[i].kind == kNear) {
+        in1[i] = 0;
+        in0[i] = 1;
+        moved_b += 8 * (int64_t)tasks_[i].m * tasks_[i].ncols;
+      }
+  }
   // coefficient layout: the x^ vectors of owned clusters move into
   // per-rank exchange regions of equal size at the start of the workspace
   {
@@ -551,7 +567,8 @@ int Builder::run(std::string* err) {
   // missing exchange: check the selection is closed
   for (int32_t i : ids1)
     for (int32_t dp : tasks_[i].deps)
-      if (!in1[dp] && !(tasks_[dp].kind == kUpLeaf || tasks_[dp].kind == kUpNode)) {
+      if (!in1[dp] && !(tasks_[dp].kind == kUpLeaf || tasks_[dp].kind == kUpNode ||
+                        (tasks_[dp].kind == kNear && in0[dp]))) {
         *err = "internal: rank plan is missing a dependency";
         return H2B_EINVAL;
       }

@@ -206,7 +206,7 @@ def SCHED_NEAR_PRIO(k: int) -> int:
 
 
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
-             band_depth=0, rank=0, world_size=1, nccl_unique_id=None) -> nat.Options:
+             band_depth=0, rank=0, world_size=1, nccl_unique_id=None, near_phase0_pct=0) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
     o.far_task_bytes = int(far_task_bytes)
@@ -217,6 +217,7 @@ def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max
     o.band_depth = int(band_depth)
     o.rank = int(rank)
     o.world_size = int(world_size)
+    o.near_phase0_pct = int(near_phase0_pct)
     if nccl_unique_id is not None:
         buf = C.create_string_buffer(bytes(nccl_unique_id), 128)
         o._keep_id = buf

@@ -36,6 +36,19 @@ def test_rank_plans_reproduce_reference(golden, world):
         assert rel(y, ex["y_full"][:, i]) <= 1e-13, (name, world, i)
 
 
+@pytest.mark.parametrize("pct", [-1, 1, 25, 100])
+def test_rank_plans_near_field_phase_split(golden, pct):
+    """Any share of a rank's near field may run in phase 0 (beside the
+    upward pass); the finals of phase 1 read those slots."""
+    name, op, ex = golden
+    for world in (2, 4):
+        plans = [plan_view(op, world_size=world, rank=r, near_phase0_pct=pct) for r in range(world)]
+        near0 = sum(int((p["phases"][0]["t_kind"] == 3).sum()) for p in plans)
+        assert (near0 == 0) == (pct == -1) or not op.near
+        y = run_ranks(plans, ex["X"][:, 0])
+        assert rel(y, ex["y_full"][:, 0]) <= 1e-13, (name, world, pct)
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_rank_plans_random_structures(seed):
     op = random_h2(seed)

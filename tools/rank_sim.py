@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--worlds", default="2,4,8")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
+    ap.add_argument("--pct", default="0", help="comma list of near_phase0_pct values (0: default)")
+    ap.add_argument("--modes", default="plain,streaming")
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -42,7 +44,9 @@ def main():
     y = torch.zeros_like(x)
     s = torch.cuda.current_stream()
     for world in [int(w) for w in a.worlds.split(",")]:
-        for mode, opts in (("plain", PLAIN), ("streaming", STREAMING)):
+        modes = [(m, dict(PLAIN if m == "plain" else STREAMING, near_phase0_pct=int(pc)))
+                 for m in a.modes.split(",") for pc in a.pct.split(",")]
+        for mode, opts in modes:
             per_rank = []
             for r in range(world):
                 dev = DeviceOperator(op, world_size=world, rank=r, **opts)
@@ -61,7 +65,8 @@ def main():
                 per_rank.append((e0.elapsed_time(e1) / a.steps, int(st["local_bytes"])))
                 dev.close()
             t = max(p[0] for p in per_rank)
-            print(json.dumps({"config": a.config, "world": world, "mode": mode, "max_rank_ms": round(t, 4),
+            print(json.dumps({"config": a.config, "world": world, "mode": mode,
+                              "near_phase0_pct": opts["near_phase0_pct"], "max_rank_ms": round(t, 4),
                               "rank_ms": [round(p[0], 4) for p in per_rank],
                               "rank_bytes": [p[1] for p in per_rank],
                               "modeled_DOF_per_s": op.n / (t * 1e-3)}), flush=True)
