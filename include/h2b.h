@@ -93,7 +93,7 @@ typedef struct h2b_desc {
    that completes a successor acquires (fence), instead of every arrival
    being an acquire (which invalidates the SM's L1) */
 #define H2B_SCHED_RELEASE_ARRIVALS 4
-#define H2B_STREAM_DEFAULT_BYTES (4LL << 30)
+#define H2B_STREAM_DEFAULT_BYTES (1LL << 30)
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */
 #define H2B_SCHED_NEAR_FIRST 1
@@ -145,7 +145,7 @@ typedef struct h2b_options {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId shared by all ranks  */
   int32_t near_phase0_pct; /* multi-GPU: share (percent of bytes, 1-100) of
                               the rank's near field run in phase 0, beside the
-                              latency-bound upward pass; 0 = default (50),
+                              latency-bound upward pass; 0 = default (75),
                               -1 = none (all in phase 1)                    */
   int32_t pad_;
 } h2b_options;
