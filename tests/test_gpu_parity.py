@@ -142,6 +142,29 @@ def test_effective_sched_flags_reported():
         dev.close()
 
 
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (8 << 20) | (1 << 25), far_task_bytes=8192)
+
+
+@pytest.mark.parametrize("nrhs", [1, 2, 4, 8, 16])
+def test_streaming_defaults_every_nrhs(nrhs):
+    """The scheduling large operators get (ring warps with 4 KB stages,
+    near-priority warps, leaf mix, 8 KB chain pieces staged in the ring,
+    evict-first copies), forced on small ones, for every right-hand-side
+    count: results within the parity bound."""
+    op, ex = load_golden("prism_20_40_2_default")
+    h2 = _gpu()
+    rng = np.random.default_rng(nrhs)
+    X = rng.standard_normal((op.n, nrhs))
+    dev = h2.DeviceOperator(op, **STREAMING)
+    try:
+        Y = dev.matvec(X[:, 0] if nrhs == 1 else X)
+    finally:
+        dev.close()
+    Y = Y.reshape(op.n, nrhs)
+    for i in range(nrhs):
+        assert rel(Y[:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_random_structures(seed):
     from synth import random_h2
