@@ -506,7 +506,9 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
         times["recompress"] = time.perf_counter() - t5
         times["total"] = time.perf_counter() - t0
         say(f"recompress {times['recompress']:.1f}s (bases rows {times.get('rec_rows', 0):.1f}s, cols "
-            f"{times.get('rec_cols', 0):.1f}s, coupling {times.get('rec_coupling', 0):.1f}s); "
+            f"{times.get('rec_cols', 0):.1f}s [weighting {times.get('rec_cols_weighting', 0):.1f}s, leaves "
+            f"{times.get('rec_cols_leaf_cpu', 0):.1f} / inner {times.get('rec_cols_inner_cpu', 0):.1f} thread-s], coupling "
+            f"{times.get('rec_coupling', 0):.1f}s); "
             f"H² {op.storage_bytes() / 1e6:.1f} MB; total {times['total']:.1f}s")
         rep = BuildReport(n=surface.n, nclusters=len(cl), n_admissible=int(adm_ids.size),
                           n_dense=int(dense_ids.size), n_fallback=n_fb, seconds=times)

@@ -58,10 +58,17 @@ class _Side:
         self.eps = eps
         self.tb = _truncated_basis_gram if fast else _truncated_basis
         self.basis, self.transfer, self.explicit = {}, {}, {}
+        self.t_leaf = self.t_inner = 0.0  # summed over threads (diagnostics)
 
     def combine(self, c, current, kids):
         """Inner cluster: projection of the stacked restricted factors onto
         the children's bases, truncated; children's transfers."""
+        t0 = time.perf_counter()
+        full = self._combine(c, current, kids)
+        self.t_inner += time.perf_counter() - t0
+        return full
+
+    def _combine(self, c, current, kids):
         pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
         if pieces:
             z = np.hstack(pieces)
@@ -85,8 +92,10 @@ class _Side:
     def visit(self, c, inherited, own):
         current = inherited + own.get(c.cid, [])
         if c.is_leaf:
+            t0 = time.perf_counter()
             pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
             v = self.tb(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), self.eps)
+            self.t_leaf += time.perf_counter() - t0
             self.basis[c.cid] = v
             self.explicit[c.cid] = v
             return v
@@ -110,13 +119,16 @@ def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0
     """One side of the nested basis.  ``anchored[cid]`` lists (factor,
     weight) of the blocks whose cluster on this side is ``cid``."""
     side = _Side(eps, fast)
+    t_start = time.perf_counter()
     items = [(cid, f, w) for cid, lst in anchored.items() for f, w in lst]
     mats = list(pool.map(lambda t: _weighted(t[1], t[2]), items)) if pool else [_weighted(f, w) for _, f, w in items]
     own: dict = {}
     for (cid, _, _), m in zip(items, mats):
         own.setdefault(cid, []).append((m, tree.clusters[cid].start))
+    basis_side.last = {"weighting": time.perf_counter() - t_start}
     if pool is None or split_depth <= 0:
         side.visit(tree.root, [], own)
+        basis_side.last.update(leaf_cpu=side.t_leaf, inner_cpu=side.t_inner)
         return side.basis, side.transfer, side.explicit
     # top-down: inherited lists down to the split depth
     frontier, top = [(tree.root, [])], []
@@ -135,6 +147,7 @@ def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0
     # bottom-up over the top part, children before parents
     for c, cur in reversed(top):
         side.combine(c, cur, [side.explicit[ch.cid] for ch in c.children])
+    basis_side.last.update(leaf_cpu=side.t_leaf, inner_cpu=side.t_inner)
     return side.basis, side.transfer, side.explicit
 
 
@@ -183,7 +196,8 @@ def recompress(tree, n: int, lowrank: list, dense: list, eps_rec: float, workers
         cbasis, ctrans, cexp = basis_side(tree, cols, eps_rec, pool, depth, fast)
         t2 = time.perf_counter()
         if timings is not None:
-            timings.update(rec_rows=t1 - t0, rec_cols=t2 - t1)
+            timings.update(rec_rows=t1 - t0, rec_cols=t2 - t1,
+                           **{f"rec_cols_{k}": v for k, v in getattr(basis_side, "last", {}).items()})
         op = H2Matrix(tree=tree, n=n, row_basis=rbasis, row_transfer=rtrans,
                       col_basis=cbasis, col_transfer=ctrans)
 
