@@ -119,11 +119,10 @@ typedef struct h2b_desc {
 /* sched_flags bit 25: TMA-ring copies carry an L2 evict-first hint (the
    streamed matrix is read once; the gathered sources should stay in L2) */
 #define H2B_SCHED_STREAM_EVICT_FIRST (1 << 25)
-/* sched_flags bit 30: a warp that continues into a chain successor counts
-   its item into the slack successors (coupling rows) only after that
-   continuation, so each link of the far-field chain waits for one batch of
-   arrival atomics instead of all of them */
-#define H2B_SCHED_DEFER_SLACK (1 << 30)
+/* sched_flags bit 30: near-priority warps take no chain-queue items (only
+   continuations): the leaf-level downward items, which become ready
+   together, then do not pull every warp off the near-field stream */
+#define H2B_SCHED_PRIO_NO_CHAIN (1 << 30)
 /* sched_flags bits 26-29: the top k warps of each CTA take near-field items
    before the up-leaf items and the coupling queues (0: none) */
 #define H2B_SCHED_NEAR_PRIO(k) (((k) & 0xf) << 26)

@@ -125,7 +125,7 @@ constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ah
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
 constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, acquire fence on completion
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
-constexpr int kFlagDeferSlack = 1 << 30;        // slack successors counted in after the continuation
+constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
@@ -913,86 +913,6 @@ __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T,
   store_rows<1>(p, T, acc0, acc1, lane);
 }
 
-// Count this warp's item into its successors [s0, s1) whose queue class is
-// in `classes` (bit q = class q); of the successors it completes, run one
-// itself next (`cont`, chain class first) when `allow_cont`, push the others
-// (one tail atomic per queue).  `sd_first`/`sd_second` are the prefetched
-// first 64 entries when `pref`.
-__device__ __forceinline__ void notify_successors(const KParams& p, Ctl* ctl, unsigned e1, int lane, int s0, int s1,
-                                                  int2 sd_first, int2 sd_second, bool pref, unsigned classes,
-                                                  bool allow_cont, int& cont) {
-  for (int k0 = s0; k0 < s1; k0 += 128) {
-    // arrival counts of up to 4 x 32 successors in flight at once
-    int dd[4], qq[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + 32 * u + lane;
-      dd[u] = -1;
-      qq[u] = 0;
-      if (k < s1) {
-        const int2 sd = (pref && k0 == s0 && u == 0) ? sd_first
-                        : (pref && k0 == s0 && u == 1) ? sd_second : __ldg(p.succ + k);
-        qq[u] = sd.y >> 24;
-        if (!((classes >> qq[u]) & 1u)) continue;
-        const unsigned ndep = (unsigned)sd.y & 0xffffffu;
-        const unsigned long long old = (p.flags & kFlagReleaseArrivals) ? atom_add_release(p.arrived + sd.x, 1ull)
-                                                                        : atom_add_acq_rel(p.arrived + sd.x, 1ull);
-        if (old + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
-      }
-    }
-    // of the successors this warp completed, run one itself next (chain
-    // class first) and push the others: one fence, one tail atomic per queue
-    unsigned any = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) any |= __ballot_sync(0xffffffffu, dd[u] >= 0);
-    if (!any) continue;
-    // release-only arrivals: the warp that completes a successor acquires
-    // the other producers' outputs here (acquire pattern: the atomic's
-    // read, then a fence), before running or publishing it
-    if (p.flags & kFlagReleaseArrivals) fence_acq_rel();
-    if (allow_cont && cont < 0) {
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned cand = __ballot_sync(0xffffffffu, dd[u] >= 0 && (pass == 1 || qq[u] == 0));
-          if (cont < 0 && cand) {
-            const int first = __ffs(cand) - 1;
-            cont = __shfl_sync(0xffffffffu, dd[u], first);
-            if (lane == first) dd[u] = -1;
-          }
-        }
-    }
-    unsigned cnt[kQueues], mask[4][kQueues];
-#pragma unroll
-    for (int q = 0; q < kQueues; ++q) cnt[q] = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int q = 0; q < kQueues; ++q) {
-        mask[u][q] = __ballot_sync(0xffffffffu, dd[u] >= 0 && qq[u] == q);
-        cnt[q] += __popc(mask[u][q]);
-      }
-    if (cnt[0] + cnt[1] + cnt[2] == 0) continue;
-    unsigned base = 0;
-    if (lane < kQueues && cnt[lane] > 0) base = atomicAdd(&ctl->tail[lane].v, cnt[lane]);
-    unsigned b[kQueues];
-#pragma unroll
-    for (int q = 0; q < kQueues; ++q) b[q] = __shfl_sync(0xffffffffu, base, q);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (dd[u] >= 0) {
-        const int q = qq[u];
-        const unsigned slot = (unsigned)q * (unsigned)p.ntasks + b[q] + __popc(mask[u][q] & ((1u << lane) - 1u));
-        p.ready_q[slot] = dd[u];
-        st_release(p.ready_flag + slot, e1);
-      }
-#pragma unroll
-      for (int q = 0; q < kQueues; ++q) b[q] += __popc(mask[u][q]);
-    }
-  }
-}
-
 template <int NRHS>
 __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1054,7 +974,6 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   int pend = -1;             // near item claimed ahead (slack work, no priority cost)
   int cont = -1;             // continuation (all lanes)
-  int def_s0 = 0, def_s1 = 0;  // deferred slack successors of the previous item (all lanes)
   // warps allowed to take near-field items (fewer loads in flight lower the
   // memory latency the far-field chain sees)
   const int near_lim = (p.flags >> 8) & 0xff;
@@ -1132,7 +1051,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
             atomicAdd(&ctl->dyn_started, 1u);
             break;
           }
-        } else if (h[0] < t[0] && (item = claim(0)) >= 0) {
+        } else if (h[0] < t[0] && !(nprio && (p.flags & kFlagPrioNoChain)) && (item = claim(0)) >= 0) {
           break;
         }
         if (nprio) {
@@ -1248,27 +1167,75 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     __syncwarp();
     unsigned long long t_run = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_run));
-    // successors of the previous item whose notification was deferred
-    // (slack classes, behind a continuation): counted in now
-    if (def_s1 > def_s0) {
-      int none = -1;
-      notify_successors(p, ctl, e1, lane, def_s0, def_s1, make_int2(-1, 0), make_int2(-1, 0), false, 0x6u, false,
-                        none);
-      def_s0 = def_s1 = 0;
-    }
     cont = -1;
-    if (p.flags & kFlagDeferSlack) {
-      // the chain successors first; when one of them continues in this warp,
-      // the slack successors are counted in after it (one item later)
-      notify_successors(p, ctl, e1, lane, s0, s1, sd_first, sd_second, true, 0x1u, true, cont);
-      if (cont >= 0) {
-        def_s0 = s0;
-        def_s1 = s1;
-      } else {
-        notify_successors(p, ctl, e1, lane, s0, s1, sd_first, sd_second, true, 0x6u, true, cont);
+    for (int k0 = s0; k0 < s1; k0 += 128) {
+      // arrival counts of up to 4 x 32 successors in flight at once
+      int dd[4], qq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 32 * u + lane;
+        dd[u] = -1;
+        qq[u] = 0;
+        if (k < s1) {
+          const int2 sd = (k0 == s0 && u == 0) ? sd_first
+                          : (k0 == s0 && u == 1) ? sd_second : __ldg(p.succ + k);
+          const unsigned ndep = (unsigned)sd.y & 0xffffffu;
+          const unsigned long long old = (p.flags & kFlagReleaseArrivals) ? atom_add_release(p.arrived + sd.x, 1ull)
+                                                                          : atom_add_acq_rel(p.arrived + sd.x, 1ull);
+          if (old + 1ull == (unsigned long long)e1 * ndep) dd[u] = sd.x;
+          qq[u] = sd.y >> 24;
+        }
       }
-    } else {
-      notify_successors(p, ctl, e1, lane, s0, s1, sd_first, sd_second, true, 0x7u, true, cont);
+      // of the successors this warp completed, run one itself next (chain
+      // class first) and push the others: one fence, one tail atomic per queue
+      unsigned any = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) any |= __ballot_sync(0xffffffffu, dd[u] >= 0);
+      if (!any) continue;
+      // release-only arrivals: the warp that completes a successor acquires
+      // the other producers' outputs here (acquire pattern: the atomic's
+      // read, then a fence), before running or publishing it
+      if (p.flags & kFlagReleaseArrivals) fence_acq_rel();
+      if (cont < 0) {
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned cand = __ballot_sync(0xffffffffu, dd[u] >= 0 && (pass == 1 || qq[u] == 0));
+            if (cont < 0 && cand) {
+              const int first = __ffs(cand) - 1;
+              cont = __shfl_sync(0xffffffffu, dd[u], first);
+              if (lane == first) dd[u] = -1;
+            }
+          }
+      }
+      unsigned cnt[kQueues], mask[4][kQueues];
+#pragma unroll
+      for (int q = 0; q < kQueues; ++q) cnt[q] = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < kQueues; ++q) {
+          mask[u][q] = __ballot_sync(0xffffffffu, dd[u] >= 0 && qq[u] == q);
+          cnt[q] += __popc(mask[u][q]);
+        }
+      if (cnt[0] + cnt[1] + cnt[2] == 0) continue;
+      unsigned base = 0;
+      if (lane < kQueues && cnt[lane] > 0) base = atomicAdd(&ctl->tail[lane].v, cnt[lane]);
+      unsigned b[kQueues];
+#pragma unroll
+      for (int q = 0; q < kQueues; ++q) b[q] = __shfl_sync(0xffffffffu, base, q);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (dd[u] >= 0) {
+          const int q = qq[u];
+          const unsigned slot = (unsigned)q * (unsigned)p.ntasks + b[q] + __popc(mask[u][q] & ((1u << lane) - 1u));
+          p.ready_q[slot] = dd[u];
+          st_release(p.ready_flag + slot, e1);
+        }
+#pragma unroll
+        for (int q = 0; q < kQueues; ++q) b[q] += __popc(mask[u][q]);
+      }
     }
     if (lane == 0 && ahead != 0xffffffffu) {
       if (ahead < n_near) pend = __ldg(p.ready0 + n_up + ahead);

@@ -58,8 +58,7 @@ def test_far_and_near_fields_separately(golden):
                                   dict(sched_flags=(2 << 20) | (8 << 26)),
                                   dict(sched_flags=(3 << 4) | (3 << 26)),
                                   dict(task_bytes=8192, sched_flags=(8 << 4)),
-                                  dict(sched_flags=4), dict(task_bytes=1024, sched_flags=4 | (8 << 4) | (6 << 26)),
-                                  dict(sched_flags=1 << 30), dict(task_bytes=2048, sched_flags=(1 << 30) | (8 << 4) | (6 << 26))])
+                                  dict(sched_flags=4), dict(task_bytes=1024, sched_flags=4 | (8 << 4) | (6 << 26))])
 def test_plan_variants(opts):
     op, ex = load_golden("config1_sphere4")
     dev = _gpu().DeviceOperator(op, **opts)
