@@ -913,6 +913,78 @@ __device__ __forceinline__ void run_item_ring1(const KParams& p, const DTask& T,
   store_rows<1>(p, T, acc0, acc1, lane);
 }
 
+
+// The same for 2 or 4 right-hand sides: lanes own rows, NRHS accumulators
+// each, columns in the order of run_item (bit-identical to it).
+template <int NRHS>
+__device__ __forceinline__ void run_item_ring_multi(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                                    const WarpRing R, unsigned& rpar, int lane,
+                                                    unsigned long long& t_gath) {
+  const int m = T.m;
+  const int cs = p.ring_stage / (8 * m);  // columns per stage (>= 8)
+  const int nch = (T.ncols + cs - 1) / cs;
+  const double* g0 = p.mat + T.data;
+  auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
+    const double* src = g0 + (int64_t)j * cs * m;
+    const int cc = min(cs, T.ncols - j * cs);
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
+    ring_load(p, R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+  };
+  if (lane == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  load_segtable(p, T, sin, w, lane);
+  double acc0[NRHS], acc1[NRHS];
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) acc0[r] = acc1[r] = 0.0;
+  add_bias<NRHS>(p, T, acc0, acc1, lane);
+  gather_chunk<NRHS>(p, w, lane, 0, T.ncols);
+  __syncwarp();
+  const bool v0 = lane < m, v1 = lane + 32 < m;
+  for (int jc = 0; jc < nch; ++jc) {
+    const int col = jc * cs;
+    const int cc = min(cs, T.ncols - col);
+    const int st = jc & 1;
+    mbar_wait(R.bar(st), (rpar >> st) & 1u);
+    rpar ^= 1u << st;
+    if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
+    const double* A = R.buf(st) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* xs = w.xs + (int64_t)col * NRHS;
+    int c = 0;
+    for (; c + 4 <= cc; c += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = v0 ? A[(c + u) * m + lane] : 0.0;
+        b[u] = v1 ? A[(c + u) * m + lane + 32] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          const double xv = xs[(c + u) * NRHS + r];
+          acc0[r] = fma(a[u], xv, acc0[r]);
+          acc1[r] = fma(b[u], xv, acc1[r]);
+        }
+    }
+    for (; c < cc; ++c) {
+      const double a = v0 ? A[c * m + lane] : 0.0;
+      const double b = v1 ? A[c * m + lane + 32] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double xv = xs[c * NRHS + r];
+        acc0[r] = fma(a, xv, acc0[r]);
+        acc1[r] = fma(b, xv, acc1[r]);
+      }
+    }
+    __syncwarp();  // every lane is done with stage st
+    if (lane == 0 && jc + 2 < nch) issue(jc + 2);
+  }
+  store_rows<NRHS>(p, T, acc0, acc1, lane);
+}
+
 template <int NRHS>
 __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1156,6 +1228,9 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     } else if (NRHS == 1 && has_ring && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
                T.ncols <= kChunkBytes / 8) {
       run_item_ring1(p, T, sin, w, ring_v, rpar, lane, t_gath);
+    } else if ((NRHS == 2 || NRHS == 4) && has_ring && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
+               T.ncols <= kChunkBytes / (8 * NRHS) && !(p.flags & kFlagNoRing)) {
+      if constexpr (NRHS == 2 || NRHS == 4) run_item_ring_multi<NRHS>(p, T, sin, w, ring_v, rpar, lane, t_gath);
     } else if (stream_u == 4) {
       run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
     } else {

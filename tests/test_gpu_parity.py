@@ -145,6 +145,25 @@ def test_effective_sched_flags_reported():
 STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (8 << 20) | (1 << 25), far_task_bytes=8192)
 
 
+@pytest.mark.parametrize("nrhs", [2, 4])
+def test_ring_multi_bit_identical(nrhs):
+    """2 and 4 right-hand sides through the TMA ring give the same bits as
+    the register-streamed path."""
+    op, ex = load_golden("prism_20_40_2_default")
+    h2 = _gpu()
+    X = np.random.default_rng(11).standard_normal((op.n, nrhs))
+    ys = []
+    for flags in (8 | (8 << 4) | (2 << 18), 8 | (8 << 4) | (2 << 18) | h2.SCHED_NO_RING):
+        dev = h2.DeviceOperator(op, sched_flags=flags)
+        try:
+            ys.append(dev.matvec(X))
+        finally:
+            dev.close()
+    assert np.array_equal(ys[0], ys[1])
+    for i in range(nrhs):
+        assert rel(ys[0][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+
+
 @pytest.mark.parametrize("nrhs", [1, 2, 4, 8, 16])
 def test_streaming_defaults_every_nrhs(nrhs):
     """The scheduling large operators get (ring warps with 4 KB stages,
