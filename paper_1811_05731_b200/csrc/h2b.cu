@@ -940,18 +940,28 @@ __device__ __forceinline__ void run_item_ring_multi(const KParams& p, const DTas
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) acc0[r] = acc1[r] = 0.0;
   add_bias<NRHS>(p, T, acc0, acc1, lane);
-  gather_chunk<NRHS>(p, w, lane, 0, T.ncols);
+  // sources in windows of the gather capacity (an item may have more
+  // columns than fit), each window starting at a stage boundary
+  constexpr int kCap = kChunkBytes / (8 * NRHS);
+  int wlo = 0, whi = min(kCap, T.ncols);
+  gather_chunk<NRHS>(p, w, lane, 0, whi);
   __syncwarp();
   const bool v0 = lane < m, v1 = lane + 32 < m;
   for (int jc = 0; jc < nch; ++jc) {
     const int col = jc * cs;
     const int cc = min(cs, T.ncols - col);
+    if (col + cc > whi) {
+      wlo = col;
+      whi = min(col + kCap, T.ncols);
+      gather_chunk<NRHS>(p, w, lane, wlo, whi - wlo);
+      __syncwarp();
+    }
     const int st = jc & 1;
     mbar_wait(R.bar(st), (rpar >> st) & 1u);
     rpar ^= 1u << st;
     if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
     const double* A = R.buf(st) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
-    const double* xs = w.xs + (int64_t)col * NRHS;
+    const double* xs = w.xs + (int64_t)(col - wlo) * NRHS;
     int c = 0;
     for (; c + 4 <= cc; c += 4) {
       double a[4], b[4];
@@ -1229,7 +1239,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
                T.ncols <= kChunkBytes / 8) {
       run_item_ring1(p, T, sin, w, ring_v, rpar, lane, t_gath);
     } else if ((NRHS == 2 || NRHS == 4) && has_ring && T.ld == T.m && T.m > 16 && T.m <= 64 && T.ncols > 0 &&
-               T.ncols <= kChunkBytes / (8 * NRHS) && !(p.flags & kFlagNoRing)) {
+               !(p.flags & kFlagNoRing)) {
       if constexpr (NRHS == 2 || NRHS == 4) run_item_ring_multi<NRHS>(p, T, sin, w, ring_v, rpar, lane, t_gath);
     } else if (stream_u == 4) {
       run_item<NRHS, false, 4>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
