@@ -14,12 +14,16 @@
 // critical path).  No warp ever waits on an unfinished item.
 //
 // Streaming: lanes own rows (r = lane, lane + 32) so every column is one
-// contiguous, coalesced read with no cross-lane reduction; 16 columns of
-// 64-bit ld.global.nc.L1::no_allocate loads are in flight per lane, and the
-// first 16 are issued before the item's sources are gathered.  Items with
-// m <= 16 pack 32/m columns per warp instruction and reduce once.  Split
-// rows write partial slots that the consumer adds in a fixed order:
-// deterministic, no floating-point atomics.
+// contiguous, coalesced read with no cross-lane reduction.  A warp either
+// keeps 8 columns of 64-bit ld.global.nc.L1::no_allocate loads in flight
+// (the first ones issued before the item's sources are gathered), or -- a
+// "ring warp" -- moves the item through a two-stage shared-memory ring by
+// 1-D TMA bulk copies (more bytes in flight, no registers); both run the
+// same column-ordered FMA chain.  Items with m <= 16 pack 32/m columns per
+// warp instruction and reduce once.  8 and 16 right-hand sides multiply on
+// the FP64 tensor cores (DMMA).  Split rows write partial slots that the
+// consumer adds in a fixed order: deterministic, no floating-point atomics.
+// Scheduling and streaming variants: h2b_options.sched_flags.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -130,9 +134,9 @@ constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered source
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
 constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+ alignment)
 
-// Per-warp shared memory: the TMA-staged matrix of a far-field item,
-// gathered sources, the item's segment table, the small-item reduction
-// scratch and the staging mbarrier.
+// Per-warp shared memory: gathered sources, the item's segment table, the
+// small-item reduction scratch and the far-field staging mbarrier (the
+// staging buffer or ring itself follows the WarpSmem array, see WarpRing).
 struct __align__(128) WarpSmem {
   double xs[kChunkBytes / 8];
   unsigned long long bar;
