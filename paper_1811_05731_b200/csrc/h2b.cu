@@ -1452,7 +1452,12 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
   h2b::PlanOptions po;
   // streaming operators: 8 KB chain pieces (a ring warp stages both ring
   // stages at once), halving the latency-bound up-leaf items
-  if (streaming_defaults(d, o)) po.far_task_bytes = 8192;
+  // and 128 KB near-field pieces (a ring warp keeps streaming across the
+  // whole item: fewer per-item round trips; config 3 2.47 -> 2.40 ms)
+  if (streaming_defaults(d, o)) {
+    po.far_task_bytes = 8192;
+    po.task_bytes = 131072;
+  }
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;
     if (o->far_task_bytes > 0) po.far_task_bytes = o->far_task_bytes;
