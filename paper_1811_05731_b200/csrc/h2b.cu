@@ -1715,7 +1715,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     // streaming defaults (measured on config 3)
     if (((sf >> 4) & 0xf) == 0) sf |= H2B_SCHED_RING_WARPS(8) | H2B_SCHED_RING_STAGE(2);
     if (((sf >> 26) & 0xf) == 0) sf |= H2B_SCHED_NEAR_PRIO(6);
-    if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(8);
+    if (((sf >> 20) & 0xf) == 0) sf |= H2B_SCHED_LEAF_MIX(4);
     sf |= H2B_SCHED_STREAM_EVICT_FIRST;
   }
   op->sched = sf;

@@ -21,7 +21,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (8 << 20) | (1 << 25), far_task_bytes=8192, task_bytes=131072)
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20) | (1 << 25), far_task_bytes=8192, task_bytes=131072)
 PLAIN = dict(sched_flags=8)
 
 
