@@ -287,7 +287,8 @@ void h2b_colloc_destroy(h2b_colloc* c);
  * (semi-)definite with a zero-free diagonal (else H2B_EINVAL, like
  * jacobi_preconditioner's ValueError).  max_iter <= 0 means 10 n.  A
  * non-positive p'Ap returns H2B_ECONV.  The caller checks the deflated
- * right-hand side's compatibility (solver.py:68-70). */
+ * right-hand side's compatibility (solver.py:68-70).  An h2b_cg owns its
+ * work vectors: one solve at a time per object. */
 typedef struct h2b_cg h2b_cg;
 int h2b_cg_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val, h2b_cg** out);
 int h2b_cg_solve(h2b_cg* c, const double* b_host, double* x_host, double tol, int deflate, int64_t max_iter,

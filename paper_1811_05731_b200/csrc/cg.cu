@@ -356,11 +356,14 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   CG_CUDA(cudaMalloc(&c->out, sizeof(double) * 4));
   int* d_zero = nullptr;
   CG_CUDA(cudaMalloc(&d_zero, sizeof(int)));
-  CG_CUDA(cudaMemset(d_zero, 0, sizeof(int)));
-  inv_diag_kernel<<<std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256)), 256>>>(n, c->rp, c->ci, c->va,
-                                                                                            c->inv, d_zero);
+  cudaError_t e = cudaMemset(d_zero, 0, sizeof(int));
+  if (e == cudaSuccess) {
+    inv_diag_kernel<<<std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256)), 256>>>(n, c->rp, c->ci, c->va,
+                                                                                              c->inv, d_zero);
+    e = cudaGetLastError();
+  }
   int zero = 0;
-  cudaError_t e = cudaMemcpy(&zero, d_zero, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&zero, d_zero, sizeof(int), cudaMemcpyDeviceToHost);
   cudaFree(d_zero);
   if (e != cudaSuccess) return gfail(H2B_ECUDA, std::string("inv_diag: ") + cudaGetErrorString(e));
   if (zero) return gfail(H2B_EINVAL, "Jacobi preconditioner requires a zero-free diagonal");
