@@ -145,7 +145,7 @@ typedef struct h2b_options {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId shared by all ranks  */
   int32_t near_phase0_pct; /* multi-GPU: share (percent of bytes, 1-100) of
                               the rank's near field run in phase 0, beside the
-                              latency-bound upward pass; 0 = default (75),
+                              latency-bound upward pass; 0 = default (90),
                               -1 = none (all in phase 1)                    */
   int32_t pad_;
 } h2b_options;

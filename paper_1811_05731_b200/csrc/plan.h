@@ -95,7 +95,7 @@ struct PlanOptions {
   int64_t far_task_bytes = 4096;  // up-leaf, up-node and down items
   int32_t band_depth = 1;         // tree levels fused into one run of the far-field chain (1: none)
   int32_t final_class = 0;        // queue class of the final items (0: chain, 2: slack)
-  int32_t near_phase0_pct = 75;   // multi-GPU: percent of the rank's near bytes in phase 0 (0: none)
+  int32_t near_phase0_pct = 90;   // multi-GPU: percent of the rank's near bytes in phase 0 (0: none)
   bool interleave = true;
   int32_t rank = 0;
   int32_t world_size = 1;
