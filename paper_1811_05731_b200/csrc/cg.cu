@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/h2b.h"
@@ -63,6 +64,7 @@ struct CGParams {
   double tol;
   int64_t max_iter;
   int deflate;
+  int rp_smem;  // the CTA's row pointers cached in dynamic shared memory (32-bit, relative)
 };
 
 // Block sum of v (all threads get it); scratch: kThreads/32 doubles.
@@ -92,13 +94,23 @@ __device__ void rows_of_block(int64_t n, int64_t* lo, int64_t* hi) {
   *hi = min(n, *lo + per);
 }
 
-__global__ void __launch_bounds__(kThreads) cg_kernel(CGParams P) {
+// U: rows per lane group per pass of the sparse product; MINB: co-resident
+// CTAs per SM the register allocation is bounded for.
+template <int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) cg_kernel(CGParams P) {
   cgk::grid_group grid = cgk::this_grid();
   __shared__ double scratch[kThreads / 32];
+  extern __shared__ int32_t rps[];  // rp[lo..hi] - rp[lo] when P.rp_smem
   int64_t lo, hi;
   rows_of_block(P.n, &lo, &hi);
   const int tid = threadIdx.x;
   const int64_t n = P.n;
+  // The matrix is fixed for the solve: with the row pointers in shared
+  // memory a pass of the sparse product has two dependent global round trips
+  // (entries, then the gathers of p) instead of three.
+  const int64_t ebase = lo < hi ? P.rp[lo] : 0;
+  if (P.rp_smem)
+    for (int64_t i = lo + tid; i <= hi; i += blockDim.x) rps[i - lo] = (int32_t)(P.rp[i] - ebase);
 
   // ---- setup: ||b||, deflated b, x = 0, r = b, z0 = inv r
   double s_bb = 0.0, s_b = 0.0;
@@ -163,19 +175,23 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGParams P) {
   const int rows_per_pass = kThreads / kLanesPerRow;
   while (res > P.tol && it < P.max_iter) {
     // ---- A: ap = A p on this CTA's rows, partial p'Ap
-    // four rows per lane group per pass, all their loads issued together
+    // U rows per lane group per pass, all their loads issued together
     // (the row pointers, then up to 4 entries per lane of each row, then
     // the gathers): the sparse product is latency-bound otherwise.  The
     // per-lane and per-row summation order is that of a row-at-a-time loop.
-    constexpr int U = 4;
     double s_pap = 0.0;
     for (int64_t r0 = lo; r0 < hi; r0 += (int64_t)rows_per_pass * U) {
       int64_t e0[U], e1[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const int64_t ik = r0 + k * rows_per_pass + sub;
-        e0[k] = ik < hi ? __ldg(P.rp + ik) : 0;
-        e1[k] = ik < hi ? __ldg(P.rp + ik + 1) : 0;
+        if (P.rp_smem) {
+          e0[k] = ik < hi ? ebase + rps[ik - lo] : 0;
+          e1[k] = ik < hi ? ebase + rps[ik - lo + 1] : 0;
+        } else {
+          e0[k] = ik < hi ? __ldg(P.rp + ik) : 0;
+          e1[k] = ik < hi ? __ldg(P.rp + ik + 1) : 0;
+        }
       }
       double v[U];
       int c[U][4];
@@ -311,6 +327,8 @@ struct h2b_cg {
   double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr, *part = nullptr, *out = nullptr;
   double* hb = nullptr;  // host path: device b
   int grid = 0;
+  const void* kernel = nullptr;
+  size_t smem = 0;  // dynamic shared memory: the CTA's row pointers, or 0
 };
 
 namespace {
@@ -343,15 +361,38 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   CG_CUDA(cudaMemcpy(c->va, val, sizeof(double) * c->nnz, cudaMemcpyHostToDevice));
   for (double** v : {&c->inv, &c->x, &c->r, &c->z, &c->p, &c->ap, &c->hb})
     CG_CUDA(cudaMalloc(v, sizeof(double) * std::max<int64_t>(1, n)));
+  // Kernel variant: rows per lane group and CTAs per SM (H2B_CG_VARIANT;
+  // tools/cg_bench.py compares them).  913k-node cube, us per iteration with
+  // / without the row pointers in shared memory: <2,4> 76 / 80, <1,4> 77 /
+  // 86, <2,3> 80 / 86, <4,2> (128 registers) 88 / 91.
+  static const struct {
+    const void* fn;
+    int minb;
+  } variants[] = {{(const void*)cg_kernel<2, 4>, 4}, {(const void*)cg_kernel<4, 2>, 2},
+                  {(const void*)cg_kernel<2, 3>, 3}, {(const void*)cg_kernel<1, 4>, 4}};
+  int v = 0;
+  if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 3);
+  c->kernel = variants[v].fn;
   int per_sm = 0, nsm = 0;
-  CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_kernel, kThreads, 0));
   CG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  // co-resident CTAs for the grid barrier: the variant's count per SM (the
+  // gathers of the sparse product need the memory-level parallelism; every
+  // CTA reads all partial sums after a barrier, so more CTAs cost L2 traffic)
+  const int want = variants[v].minb;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)want * nsm, (n + kThreads - 1) / kThreads));
+  const int64_t per_cta = (n + grid - 1) / grid;
+  size_t smem = sizeof(int32_t) * (per_cta + 1);
+  const char* no_smem = getenv("H2B_CG_RP_SMEM");
+  if (smem > 48 * 1024 || (no_smem && atoi(no_smem) == 0)) smem = 0;
+  CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, kThreads, smem));
+  if (per_sm < want && smem) {
+    smem = 0;
+    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, kThreads, 0));
+  }
   if (per_sm < 1) return gfail(H2B_ECUDA, "cg kernel does not fit on an SM");
-  // co-resident CTAs for the grid barrier: up to 4 per SM (the gathers of
-  // the sparse product need the memory-level parallelism; every CTA reads
-  // all partial sums after a barrier, so more CTAs cost L2 traffic)
-  c->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::min(per_sm, 4) * nsm,
-                                                        (n + kThreads - 1) / kThreads));
+  c->grid = (int)std::min<int64_t>(grid, (int64_t)per_sm * nsm);
+  if (c->grid < grid) smem = 0;  // rows per CTA changed; use the global row pointers
+  c->smem = smem;
   CG_CUDA(cudaMalloc(&c->part, sizeof(double) * kParts * c->grid));
   CG_CUDA(cudaMalloc(&c->out, sizeof(double) * 4));
   int* d_zero = nullptr;
@@ -412,8 +453,9 @@ int h2b_cg_solve_dev(h2b_cg* c, const double* b_dev, double* x_dev, double tol, 
   P.tol = tol;
   P.max_iter = max_iter > 0 ? max_iter : 10 * c->n;  // solver.py:62-63
   P.deflate = deflate ? 1 : 0;
+  P.rp_smem = c->smem ? 1 : 0;
   void* args[] = {&P};
-  CG_CUDA(cudaLaunchCooperativeKernel((const void*)cg_kernel, dim3(c->grid), dim3(kThreads), args, 0, st));
+  CG_CUDA(cudaLaunchCooperativeKernel(c->kernel, dim3(c->grid), dim3(kThreads), args, c->smem, st));
   double out[4];
   CG_CUDA(cudaMemcpyAsync(out, c->out, sizeof(out), cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaStreamSynchronize(st));
