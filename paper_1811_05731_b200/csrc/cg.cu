@@ -96,10 +96,10 @@ __device__ void rows_of_block(int64_t n, int64_t* lo, int64_t* hi) {
 
 // U: rows per lane group per pass of the sparse product; MINB: co-resident
 // CTAs per SM the register allocation is bounded for.
-template <int U, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) cg_kernel(CGParams P) {
+template <int U, int MINB, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) cg_kernel(CGParams P) {
   cgk::grid_group grid = cgk::this_grid();
-  __shared__ double scratch[kThreads / 32];
+  __shared__ double scratch[NT / 32];
   extern __shared__ int32_t rps[];  // rp[lo..hi] - rp[lo] when P.rp_smem
   int64_t lo, hi;
   rows_of_block(P.n, &lo, &hi);
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cg_kernel(CGParams P) {
   grid.sync();
 
   const int sub = tid / kLanesPerRow, sl = tid % kLanesPerRow;
-  const int rows_per_pass = kThreads / kLanesPerRow;
+  const int rows_per_pass = NT / kLanesPerRow;
   while (res > P.tol && it < P.max_iter) {
     // ---- A: ap = A p on this CTA's rows, partial p'Ap
     // U rows per lane group per pass, all their loads issued together
@@ -328,6 +328,7 @@ struct h2b_cg {
   double* hb = nullptr;  // host path: device b
   int grid = 0;
   const void* kernel = nullptr;
+  int threads = kThreads;
   size_t smem = 0;  // dynamic shared memory: the CTA's row pointers, or 0
 };
 
@@ -362,16 +363,26 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   for (double** v : {&c->inv, &c->x, &c->r, &c->z, &c->p, &c->ap, &c->hb})
     CG_CUDA(cudaMalloc(v, sizeof(double) * std::max<int64_t>(1, n)));
   // Kernel variant: rows per lane group and CTAs per SM (H2B_CG_VARIANT;
-  // tools/cg_bench.py compares them).  913k-node cube, us per iteration with
+  // tools/cg_bench.py compares them; <U, CTAs per SM[, threads]>).  913k-node cube, us per iteration with
   // / without the row pointers in shared memory: <2,4> 76 / 80, <1,4> 77 /
   // 86, <2,3> 80 / 86, <4,2> (128 registers) 88 / 91.
   static const struct {
     const void* fn;
     int minb;
-  } variants[] = {{(const void*)cg_kernel<2, 4>, 4}, {(const void*)cg_kernel<4, 2>, 2},
-                  {(const void*)cg_kernel<2, 3>, 3}, {(const void*)cg_kernel<1, 4>, 4}};
-  int v = 0;
-  if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 3);
+    int threads;
+  } variants[] = {{(const void*)cg_kernel<2, 4>, 4, kThreads},      {(const void*)cg_kernel<4, 2>, 2, kThreads},
+                  {(const void*)cg_kernel<2, 3>, 3, kThreads},      {(const void*)cg_kernel<1, 4>, 4, kThreads},
+                  {(const void*)cg_kernel<2, 2, 512>, 2, 512},      {(const void*)cg_kernel<2, 1, 1024>, 1, 1024}};
+  int nsm0 = 0;
+  CG_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, c->device));
+  // default: 512 threads at 2 CTAs per SM (half the CTAs at each grid
+  // barrier) while its row pointers fit the 48 KB of shared memory, else 256
+  // at 4.  us per iteration: 913 k nodes 72-74 vs 76-77; 118 k 18.6 vs 19.0;
+  // 4.17 M (rows do not fit) 317 vs 296 (profiles/r01_cg_variants_512.log).
+  int v = (int64_t)sizeof(int32_t) * ((n + 2 * nsm0 - 1) / (2 * nsm0) + 1) <= 48 * 1024 ? 4 : 0;
+  if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 5);
+  const int nt = variants[v].threads;
+  c->threads = nt;
   c->kernel = variants[v].fn;
   int per_sm = 0, nsm = 0;
   CG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
@@ -379,15 +390,15 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   // gathers of the sparse product need the memory-level parallelism; every
   // CTA reads all partial sums after a barrier, so more CTAs cost L2 traffic)
   const int want = variants[v].minb;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)want * nsm, (n + kThreads - 1) / kThreads));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)want * nsm, (n + nt - 1) / nt));
   const int64_t per_cta = (n + grid - 1) / grid;
   size_t smem = sizeof(int32_t) * (per_cta + 1);
   const char* no_smem = getenv("H2B_CG_RP_SMEM");
   if (smem > 48 * 1024 || (no_smem && atoi(no_smem) == 0)) smem = 0;
-  CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, kThreads, smem));
+  CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, nt, smem));
   if (per_sm < want && smem) {
     smem = 0;
-    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, kThreads, 0));
+    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, nt, 0));
   }
   if (per_sm < 1) return gfail(H2B_ECUDA, "cg kernel does not fit on an SM");
   c->grid = (int)std::min<int64_t>(grid, (int64_t)per_sm * nsm);
@@ -455,7 +466,7 @@ int h2b_cg_solve_dev(h2b_cg* c, const double* b_dev, double* x_dev, double tol, 
   P.deflate = deflate ? 1 : 0;
   P.rp_smem = c->smem ? 1 : 0;
   void* args[] = {&P};
-  CG_CUDA(cudaLaunchCooperativeKernel(c->kernel, dim3(c->grid), dim3(kThreads), args, c->smem, st));
+  CG_CUDA(cudaLaunchCooperativeKernel(c->kernel, dim3(c->grid), dim3(c->threads), args, c->smem, st));
   double out[4];
   CG_CUDA(cudaMemcpyAsync(out, c->out, sizeof(out), cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaStreamSynchronize(st));
