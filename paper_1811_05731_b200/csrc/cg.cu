@@ -96,7 +96,9 @@ __device__ void rows_of_block(int64_t n, int64_t* lo, int64_t* hi) {
 
 // U: rows per lane group per pass of the sparse product; MINB: co-resident
 // CTAs per SM the register allocation is bounded for.
-template <int U, int MINB, int NT = kThreads>
+// NT: threads per CTA; PF: passes ahead whose entries are prefetched to L2
+// (needs the row pointers in shared memory).
+template <int U, int MINB, int NT = kThreads, int PF = 0>
 __global__ void __launch_bounds__(NT, MINB) cg_kernel(CGParams P) {
   cgk::grid_group grid = cgk::this_grid();
   __shared__ double scratch[NT / 32];
@@ -240,6 +242,24 @@ __global__ void __launch_bounds__(NT, MINB) cg_kernel(CGParams P) {
           s_pap += v[k] * P.p[ik];
         }
       }
+      // L2 prefetch of the entries PF passes ahead (one 128-byte line of va
+      // or ci per thread): their loads then wait on L2, not HBM
+      if (PF > 0 && P.rp_smem) {
+        const int64_t pass = (int64_t)rows_per_pass * U;
+        const int64_t a = r0 + PF * pass;
+        if (a < hi) {
+          const int64_t b = min(hi, a + pass);
+          const int64_t f0 = ebase + rps[a - lo], f1 = ebase + rps[b - lo];
+          const char* va0 = (const char*)(P.va + f0);
+          const char* ci0 = (const char*)(P.ci + f0);
+          const int64_t nva = ((const char*)(P.va + f1) - va0 + 127) >> 7;
+          const int64_t nci = ((const char*)(P.ci + f1) - ci0 + 127) >> 7;
+          for (int64_t j = tid; j < nva + nci; j += NT) {
+            const char* addr = j < nva ? va0 + (j << 7) : ci0 + ((j - nva) << 7);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(addr));
+          }
+        }
+      }
     }
     s_pap = block_sum(s_pap, scratch);
     if (tid == 0) P.part[blockIdx.x * kParts + 0] = s_pap;
@@ -372,15 +392,19 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
     int threads;
   } variants[] = {{(const void*)cg_kernel<2, 4>, 4, kThreads},      {(const void*)cg_kernel<4, 2>, 2, kThreads},
                   {(const void*)cg_kernel<2, 3>, 3, kThreads},      {(const void*)cg_kernel<1, 4>, 4, kThreads},
-                  {(const void*)cg_kernel<2, 2, 512>, 2, 512},      {(const void*)cg_kernel<2, 1, 1024>, 1, 1024}};
+                  {(const void*)cg_kernel<2, 2, 512, 2>, 2, 512},   {(const void*)cg_kernel<2, 1, 1024>, 1, 1024},
+                  {(const void*)cg_kernel<2, 2, 512>, 2, 512}};
   int nsm0 = 0;
   CG_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, c->device));
   // default: 512 threads at 2 CTAs per SM (half the CTAs at each grid
-  // barrier) while its row pointers fit the 48 KB of shared memory, else 256
-  // at 4.  us per iteration: 913 k nodes 72-74 vs 76-77; 118 k 18.6 vs 19.0;
-  // 4.17 M (rows do not fit) 317 vs 296 (profiles/r01_cg_variants_512.log).
+  // barrier) with the entries two passes ahead prefetched to L2, while its
+  // row pointers fit the 48 KB of shared memory, else 256 at 4.  us per
+  // iteration: 913 k nodes 72-74 vs 76-77 without the prefetch, 69.5-71 with
+  // (1 / 3 / 4 passes ahead: 71 / 73.4 / 77); 118 k 18.6 vs 19.0; 2.1 M 150.6
+  // vs 155.3 without the prefetch; 4.17 M (rows do not fit) 317 vs 296
+  // (profiles/r01_cg_variants_512.log, r01_cg_prefetch.log).
   int v = (int64_t)sizeof(int32_t) * ((n + 2 * nsm0 - 1) / (2 * nsm0) + 1) <= 48 * 1024 ? 4 : 0;
-  if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 5);
+  if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 6);
   const int nt = variants[v].threads;
   c->threads = nt;
   c->kernel = variants[v].fn;
