@@ -112,3 +112,34 @@ def test_sphere_energy_with_gpu_solves_and_product():
     assert abs(res.e_d_over_kd - ref) <= 1e-9 * abs(ref)
     assert abs(res.u1_iterations - 248) <= 2 and abs(res.u2_iterations - 217) <= 2
     assert rel(res.u2[mesh.boundary_nodes], ex["energy_u2_boundary"]) <= 1e-8
+
+
+@gpu
+def test_gpu_cg_kernel_variants(monkeypatch):
+    """Every kernel variant of csrc/cg.cu (H2B_CG_VARIANT, read when the
+    solver is created) solves the same system to the oracle's solution.
+    Variants with the same grid sum in the same order: <2,4,256> and
+    <1,4,256> (592 CTAs), and <2,2,512> with and without the L2 prefetch,
+    give bit-identical iterates."""
+    _cuda()
+    from oracle.fem_ref import _pcg
+    from paper_1811_05731_b200 import fem
+    mesh = _mesh()
+    a = fem.assemble_stiffness(mesh)
+    b = fem.assemble_u1_rhs(mesh, np.random.default_rng(9).standard_normal((mesh.n_nodes, 3)))
+    xo, ito = _pcg(a, b, 1e-10, True)
+    out = {}
+    for v in range(7):
+        for rp_smem in ("1", "0"):
+            monkeypatch.setenv("H2B_CG_VARIANT", str(v))
+            monkeypatch.setenv("H2B_CG_RP_SMEM", rp_smem)
+            solver = fem.GpuCG(a)
+            x, rep = solver.solve(b, deflate_constants=True)
+            assert rep.converged and abs(rep.iterations - ito) <= 2, (v, rp_smem)
+            assert rel(x, xo) <= 1e-8, (v, rp_smem)
+            out[v, rp_smem] = x
+    for v in range(7):
+        # the row pointers' location changes no arithmetic (L2 prefetch off without them)
+        assert np.array_equal(out[v, "1"], out[v, "0"]), v
+    assert np.array_equal(out[0, "1"], out[3, "1"])
+    assert np.array_equal(out[4, "1"], out[6, "1"])
