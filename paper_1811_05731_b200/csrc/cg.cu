@@ -45,6 +45,7 @@ int gfail(int code, const std::string& m) { return h2b_detail::set_error(code, m
 
 constexpr int kThreads = 256;
 constexpr int kLanesPerRow = 4;
+constexpr size_t kRpSmemPerSm = 200 * 1024;  // row-pointer cache budget per SM
 constexpr int kParts = 5;  // partial sums per CTA: p'Ap | r'z0, sum z0, sum r, r'r
 
 struct CGParams {
@@ -398,12 +399,13 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   CG_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, c->device));
   // default: 512 threads at 2 CTAs per SM (half the CTAs at each grid
   // barrier) with the entries two passes ahead prefetched to L2, while its
-  // row pointers fit the 48 KB of shared memory, else 256 at 4.  us per
+  // row pointers fit 100 KB of shared memory, else 256 at 4.  us per
   // iteration: 913 k nodes 72-74 vs 76-77 without the prefetch, 69.5-71 with
   // (1 / 3 / 4 passes ahead: 71 / 73.4 / 77); 118 k 18.6 vs 19.0; 2.1 M 150.6
-  // vs 155.3 without the prefetch; 4.17 M (rows do not fit) 317 vs 296
-  // (profiles/r01_cg_variants_512.log, r01_cg_prefetch.log).
-  int v = (int64_t)sizeof(int32_t) * ((n + 2 * nsm0 - 1) / (2 * nsm0) + 1) <= 48 * 1024 ? 4 : 0;
+  // vs 155.3 without the prefetch; 4.17 M 295-296 vs 296 (317 when its row
+  // pointers were limited to 48 KB and read from global memory)
+  // (profiles/r01_cg_variants_512.log, r01_cg_prefetch.log, r01_cg_rp_smem_200k.log).
+  int v = sizeof(int32_t) * (size_t)((n + 2 * nsm0 - 1) / (2 * nsm0) + 1) <= kRpSmemPerSm / 2 ? 4 : 0;
   if (const char* e = getenv("H2B_CG_VARIANT")) v = std::min(std::max(atoi(e), 0), 6);
   const int nt = variants[v].threads;
   c->threads = nt;
@@ -418,7 +420,10 @@ int cg_create_impl(int64_t n, const int64_t* row_ptr, const int32_t* col, const 
   const int64_t per_cta = (n + grid - 1) / grid;
   size_t smem = sizeof(int32_t) * (per_cta + 1);
   const char* no_smem = getenv("H2B_CG_RP_SMEM");
-  if (smem > 48 * 1024 || (no_smem && atoi(no_smem) == 0)) smem = 0;
+  // up to ~200 KB of row pointers per SM (beyond 48 KB per CTA by opt-in)
+  if (smem > kRpSmemPerSm / (size_t)want || (no_smem && atoi(no_smem) == 0)) smem = 0;
+  if (smem > 48 * 1024)
+    CG_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kernel, nt, smem));
   if (per_sm < want && smem) {
     smem = 0;
