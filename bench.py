@@ -16,10 +16,13 @@ all-gathered over NCCL between the two phases of every rank): a step is one
 product of the whole operator, its time the max over ranks (strong
 scaling).
 
-``--impl reference`` times the CPU restatement of the reference matvec
-(oracle/h2_matvec_ref.py, the "port": a Python loop over small numpy GEMVs,
-exactly the reference's h2.py:186-244) on the host cores, one product per
-process on every core, same workload/metric/unit.
+``--impl reference`` times the UNMODIFIED reference matvec
+(``strayfield.hmatrix.h2.h2_matvec``, h2.py:186-244, imported from
+baseline/_ref) on the host cores, one process per core, on an operator with
+exactly the workload's structure (oracle/reference.py ``structure_twin``:
+same tree, block partition and ranks -- hence the same GEMV shapes and
+storage_bytes -- seeded entries), built on the host CPU only: this arm never
+touches the GPU or loads a native library of this repo.
 """
 
 from __future__ import annotations
@@ -30,7 +33,6 @@ import os
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -178,49 +180,74 @@ class DeviceTimer:
         return sum(a.elapsed_time(b) for a, b in ev) / steps
 
 
-def _config_block(args, n, op_bytes, extra=None):
+def _config_block(args, n, op_bytes):
+    """The workload description -- identical in both arms."""
     from paper_1811_05731_b200.workloads import WORKLOADS
-    c = {"workload": f"{args.config}: {WORKLOADS[args.config]['desc']}", "n": n, "nrhs": args.nrhs,
-         "h2_bytes": op_bytes, "parallelism": f"shard{args.world}" if args.world > 1 else "single",
-         "l2": "flushed before every timed step (a 252 MB buffer rewritten outside the timed interval); "
-               "the operator is also larger than the 126 MB L2" if args.l2_flush else
-               "not flushed: the operator streamed per step is larger than the 126 MB L2"}
-    if extra:
-        c.update(extra)
-    return c
+    return {"workload": f"{args.config}: {WORKLOADS[args.config]['desc']}", "n": n, "nrhs": args.nrhs,
+            "h2_bytes": op_bytes, "parallelism": f"shard{args.world}" if args.world > 1 else "single",
+            "l2": "flushed before every timed step (a 252 MB buffer rewritten outside the timed interval); "
+                  "the operator is also larger than the 126 MB L2" if args.l2_flush else
+                  "not flushed: the operator streamed per step is larger than the 126 MB L2"}
 
 
-def _cpu_port_single(op, x, seconds=10.0, max_reps=40):
-    """Oracle port, one thread (threadpoolctl), bounded sample."""
-    from oracle.h2_matvec_ref import h2_matvec_ref
+def _peak_rss_gb():
+    import resource
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
+
+
+def _loaded_native():
+    """In-tree shared objects mapped into this process."""
+    try:
+        maps = Path("/proc/self/maps").read_text()
+    except OSError:
+        return None
+    return sorted({ln.split()[-1] for ln in maps.splitlines()
+                   if ln.endswith(".so") and str(ROOT) in ln})
+
+
+def _cpu_reference_single(op, x, seconds=10.0, max_reps=40):
+    """The unmodified reference h2_matvec (baseline/_ref) on the same
+    operator, one BLAS thread, bounded sample; the oracle port when the
+    reference is not vendored."""
+    try:
+        from oracle.reference import available, reference_h2_matvec, to_reference
+        if not available():
+            raise ImportError
+        fn, target, kind = reference_h2_matvec(), to_reference(op), "reference"
+    except ImportError:
+        from oracle.h2_matvec_ref import h2_matvec_ref
+        fn, target, kind = h2_matvec_ref, op, "port"
     try:
         from threadpoolctl import threadpool_limits
         lim = threadpool_limits(1)
     except Exception:
         lim = None
     try:
-        h2_matvec_ref(op, x)
+        fn(target, x)
         reps, t0 = 0, time.perf_counter()
         while reps < max_reps and (reps < 3 or time.perf_counter() - t0 < seconds):
-            h2_matvec_ref(op, x)
+            fn(target, x)
             reps += 1
         dt = (time.perf_counter() - t0) / reps
     finally:
         if lim is not None:
-            lim.unregister() if hasattr(lim, "unregister") else None
-    return dt, reps
+            lim.restore_original_limits()
+    return dt, reps, kind
 
 
-_POOL_OP = {}
-
-
-def _pool_task(i):
-    from oracle.h2_matvec_ref import h2_matvec_ref
-    op = _POOL_OP["op"]
-    x = np.random.default_rng(1234 + i).standard_normal(op.n)
-    t = time.perf_counter()
-    h2_matvec_ref(op, x)
-    return time.perf_counter() - t
+def _ref_worker(op, n_products, nrhs, barrier, q, seed):
+    """One reference process: warm-up product, then n_products timed ones
+    (each product of a multi-RHS step is nrhs single-vector calls: the
+    reference has no multi-RHS entry point)."""
+    from oracle.reference import reference_h2_matvec
+    fn = reference_h2_matvec()
+    x = np.random.default_rng(seed).standard_normal(op.n)
+    fn(op, x)
+    barrier.wait()
+    t0 = time.perf_counter()
+    for _ in range(n_products * nrhs):
+        fn(op, x)
+    q.put((t0, time.perf_counter()))
 
 
 def run_reference(args):
@@ -228,31 +255,53 @@ def run_reference(args):
     if ws > 1 and rank != 0:
         return 0  # rank 0 alone runs the CPU reference arm
     log = (lambda m: print(m, file=sys.stderr, flush=True))
-    op, info = _build(args, 0, 1, log)
     import multiprocessing as mp
+    from oracle.reference import available, rank_fixture_path, structure_twin, to_reference
+    name = "config3" if args.config == "config4" else args.config
+    why = None
+    if not available():
+        why = "baseline/_ref is not vendored (tools/vendor_reference.sh)"
+    elif not rank_fixture_path(name).exists():
+        why = f"no structure fixture {rank_fixture_path(name).name} for {args.config}"
+    if why:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return 0
+    twin, info = structure_twin(name, log=log)
+    op = to_reference(twin)
     cores = os.cpu_count() or 1
-    _POOL_OP["op"] = op
     try:  # one BLAS thread per process; inherited by the forked workers
         from threadpoolctl import threadpool_limits
         threadpool_limits(1)
     except Exception:
         pass
+    per_proc = max(1, -(-args.steps // cores))   # ceil: every core runs the same count
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_pool_task, range(min(args.warmup, cores) or 1))
-        t0 = time.perf_counter()
-        per = pool.map(_pool_task, range(args.steps), chunksize=1)
-        wall = time.perf_counter() - t0
-    value = args.steps * op.n * args.nrhs / wall
+    barrier, q = ctx.Barrier(cores), ctx.Queue()
+    procs = [ctx.Process(target=_ref_worker, args=(op, per_proc, args.nrhs, barrier, q, 1234 + i))
+             for i in range(cores)]
+    for p_ in procs:
+        p_.start()
+    spans = [q.get() for _ in procs]
+    for p_ in procs:
+        p_.join()
+    wall = max(b for _, b in spans) - min(a for a, _ in spans)
+    total = cores * per_proc
+    value = total * op.n * args.nrhs / wall
+    lat = float(np.mean([(b - a) / (per_proc * args.nrhs) for a, b in spans]))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / total,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_block(args, op.n, op.storage_bytes()),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full products of the workload, one per process on "
-                                       f"{cores} processes (OPENBLAS_NUM_THREADS=1 each); mean single-product "
-                                       f"latency {1e3 * float(np.mean(per)):.1f} ms"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic", "config": _config_block(args, op.n, twin.storage_bytes()),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"{total} products ({per_proc} per process on {cores} processes, "
+                                       f"OPENBLAS_NUM_THREADS=1 each, after one warm-up product each) of the "
+                                       f"unmodified strayfield.hmatrix.h2.h2_matvec from baseline/_ref on an "
+                                       f"operator with the workload's exact structure (tree, blocks, ranks: "
+                                       f"{twin.storage_bytes()} bytes) and seeded entries; mean single-product "
+                                       f"latency {1e3 * lat:.1f} ms"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "build": {"twin_seconds": round(info["build_seconds"], 1)},
+            "native_so_loaded": _loaded_native(), "host_peak_rss_gb": round(_peak_rss_gb(), 1)}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -266,31 +315,43 @@ def run_b200(args):
     torch.cuda.set_device(local)
     log = (lambda m: print(m, file=sys.stderr, flush=True)) if rank == 0 else (lambda m: None)
     op, info = _build(args, rank, ws, log)
-    from paper_1811_05731_b200.h2 import DeviceOperator, h2_matvec, h2_matmat, nccl_unique_id
+    from paper_1811_05731_b200.h2 import DeviceOperator, device_operator, h2_matvec, h2_matmat, nccl_unique_id
     if ws > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
         dev = DeviceOperator(op, rank=rank, world_size=ws, nccl_unique_id=obj[0])
     else:
-        dev = DeviceOperator(op)
+        dev = device_operator(op)   # the one h2_matvec(op, x) uses: one device copy
+    log(f"[bench] device operator ready [host peak rss {_peak_rss_gb():.1f} GB]")
     st = dev.stats()
     n, nrhs = op.n, args.nrhs
-    from paper_1811_05731_b200.workloads import vector_for
+    from paper_1811_05731_b200.workloads import vector_for, z_over_3
     xh = vector_for(args.config, n, nrhs, seed=1234)
     x = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
-    # parity spot-check of this very operator against the oracle (rank 0)
+    # parity of this very operator against the oracle (rank 0): every column
+    # of the seeded N(0,1) input and, where the node coordinates are known,
+    # u1 = z/3 (BASELINE configs 1 and 5)
     parity = None
     if not args.profile:
-        yg = dev.matvec(xh)   # full y on every rank (multi-GPU: rows assembled over NCCL)
+        vecs = {"randn": xh}
+        if info.get("coords") is not None and nrhs == 1:
+            vecs["z_over_3"] = z_over_3(info["coords"])
+        ys = {k: dev.matvec(v) for k, v in vecs.items()}   # multi-GPU: rows assembled over NCCL
     if rank == 0 and not args.profile:
         from oracle.h2_matvec_ref import h2_matvec_ref
-        x0 = xh if nrhs == 1 else xh[:, 0]
-        y0 = yg if nrhs == 1 else yg[:, 0]
-        yr = h2_matvec_ref(op, x0)
-        parity = float(np.linalg.norm(y0 - yr) / np.linalg.norm(yr))
+        parity = {}
+        for k, v in vecs.items():
+            cols = [v] if v.ndim == 1 else [v[:, j] for j in range(v.shape[1])]
+            ycols = [ys[k]] if v.ndim == 1 else [ys[k][:, j] for j in range(v.shape[1])]
+            errs = []
+            for xc, yc in zip(cols, ycols):
+                yr = h2_matvec_ref(op, np.ascontiguousarray(xc))
+                errs.append(float(np.linalg.norm(yc - yr) / np.linalg.norm(yr)))
+            parity[k] = max(errs)
+            log(f"[bench] parity {k}: {parity[k]:.2e} over {len(errs)} column(s)")
     for _ in range(args.warmup):
         dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, sp)
     torch.cuda.synchronize()
@@ -311,58 +372,66 @@ def run_b200(args):
     value = n * nrhs / (ms * 1e-3)          # one product of the whole operator per step
     b_alg = st["stream_bytes"] + 16 * n * nrhs
     achieved = b_alg / (ms * 1e-3) / 1e9   # aggregate over the GPUs
-    # end to end through the public API with host buffers (pinned), rank-local
+    # end to end through the public API with host buffers: the pageable
+    # numpy arrays the real callers pass (apply_operator, compute_demag) --
+    # the headline -- and, beside it, pinned host arrays
     e2e = None
+    e2e_pinned = None
     if not args.profile:
-        xp = torch.from_numpy(np.ascontiguousarray(xh)).pin_memory().numpy()
-        if ws > 1:
-            call = lambda: dev.matvec(xp)    # the rank operator's host entry point
-        else:
-            call = (lambda: h2_matvec(op, xp)) if nrhs == 1 else (lambda: h2_matmat(op, xp))
-        for _ in range(3):
-            call()
-        k = max(5, min(args.steps, 200))
-        te = 0.0
-        for i in range(k):
-            if timer.buf is not None:  # same L2 treatment as the device-timed steps
-                timer.buf.fill_(i)
-                torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            call()
-            te += time.perf_counter() - t0
-        te /= k
-        if ws > 1:
-            t = torch.tensor([te], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            te = float(t.item())
-        e2e = {"value": n * nrhs / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n * nrhs,
-               "d2h_bytes_per_step": 8 * n * nrhs, "ms_per_step": te * 1e3, "steps": k}
+        def e2e_time(xin):
+            if ws > 1:
+                call = lambda: dev.matvec(xin)    # the rank operator's host entry point
+            else:
+                call = (lambda: h2_matvec(op, xin)) if nrhs == 1 else (lambda: h2_matmat(op, xin))
+            for _ in range(3):
+                call()
+            k = max(5, min(args.steps, 200))
+            te = 0.0
+            for i in range(k):
+                if timer.buf is not None:  # same L2 treatment as the device-timed steps
+                    timer.buf.fill_(i)
+                    torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                call()
+                te += time.perf_counter() - t0
+            te /= k
+            if ws > 1:
+                t = torch.tensor([te], device="cuda")
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                te = float(t.item())
+            return {"value": n * nrhs / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n * nrhs,
+                    "d2h_bytes_per_step": 8 * n * nrhs, "ms_per_step": te * 1e3, "steps": k}
+        e2e = e2e_time(np.ascontiguousarray(xh))
+        e2e["host_input"] = "pageable numpy array (as apply_operator / compute_demag pass it)"
+        e2e_pinned = e2e_time(torch.from_numpy(np.ascontiguousarray(xh)).pin_memory().numpy())
+        e2e_pinned["host_input"] = "pinned"
     cpu = None
     if rank == 0 and ws == 1 and not args.profile and not args.no_cpu_baseline:
-        x0 = xh if nrhs == 1 else xh[:, 0]
-        dt, reps = _cpu_port_single(op, x0)
-        cpu = {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{reps} single-vector products of the same operator, oracle/h2_matvec_ref.py "
-                         f"(Python loop of numpy GEMVs like h2.py:186-244), 1 thread, "
+        x0 = xh if nrhs == 1 else np.ascontiguousarray(xh[:, 0])
+        dt, reps, kind = _cpu_reference_single(op, x0)
+        what = ("the unmodified strayfield.hmatrix.h2.h2_matvec (baseline/_ref, h2.py:186-244)" if kind == "reference"
+                else "oracle/h2_matvec_ref.py (restatement of h2.py:186-244)")
+        cpu = {"value": n / dt, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"{reps} single-vector products of the same operator, {what}, 1 thread, "
                          f"{dt * 1e3:.1f} ms per product"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong" if ws > 1 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": _config_block(args, n, op.storage_bytes(),
-                                        {"build": {k: v for k, v in info.items() if k != "build_seconds"},
-                                         "build_seconds": {k: round(v, 2) for k, v in
-                                                           (info.get("build_seconds") or {}).items()},
-                                         "work_items": st["ntasks"], "grid": st["grid"],
-                                         "bytes_by_kind": st["bytes_by_kind"]}),
+                "config": _config_block(args, n, op.storage_bytes()),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"] * ws, "unit": "GB/s",
                              "frac": achieved / (peaks["hbm_gbs"] * ws), "traffic": _traffic(args),
                              "peak_kind": peak_kind, "aggregate_over_gpus": ws,
                              "algorithmic_bytes_per_launch": b_alg},
-                "cpu_baseline": cpu, "e2e": e2e,
+                "cpu_baseline": cpu, "e2e": e2e, "e2e_pinned": e2e_pinned,
                 "gpu_launches": (2 if ws == 1 else 3) * args.steps, "clocks": clocks,
-                "parity_rel_err_vs_oracle": parity}
+                "parity_rel_err_vs_oracle": max(parity.values()) if parity else None,
+                "parity": parity,
+                "build": {**{k: v for k, v in info.items() if k not in ("build_seconds", "coords")},
+                          "seconds": {k: round(v, 2) for k, v in (info.get("build_seconds") or {}).items()}},
+                "plan": {"work_items": st["ntasks"], "grid": st["grid"], "bytes_by_kind": st["bytes_by_kind"]},
+                "host_peak_rss_gb": round(_peak_rss_gb(), 1)}
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()

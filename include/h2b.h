@@ -132,7 +132,7 @@ typedef struct h2b_options {
   int64_t task_bytes;   /* max bytes per near-field work item (def. 65536)   */
   int64_t far_task_bytes; /* max bytes per far-field item (default 4096): each
                              is staged to shared memory by one TMA bulk copy */
-  int32_t warps_per_cta;/* persistent CTA width in warps (default 8, <= 16)  */
+  int32_t warps_per_cta;/* persistent CTA width in warps (default 8, <= 8)   */
   int32_t ctas_per_sm;  /* 0 = occupancy-derived                             */
   int32_t max_nrhs;     /* largest nrhs the op will be called with (def. 16) */
   int32_t sched_flags;  /* H2B_SCHED_* bits; 0 = default scheduling          */
@@ -213,11 +213,24 @@ int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* out);
 int h2b_plan_partition(const h2b_plan* p, int64_t* rank_lo_hi, int64_t* exchange);
 void h2b_plan_destroy(h2b_plan* p);
 
-/* Device operator on the current CUDA device (cudaSetDevice beforehand). */
+/* Device operator on the current CUDA device (cudaSetDevice beforehand).
+ *
+ * Concurrency: an operator is shareable between host threads and streams,
+ * but runs ONE product at a time (its scheduler state and coefficient
+ * workspace are per operator, like the single workspace of the reference's
+ * per-call dicts).  Every product waits on the device for the previous
+ * product of the same operator (an event chain across streams) and the
+ * host-side calls are serialised by a per-operator lock, so products issued
+ * from several threads or streams run one after another in issue order.
+ * For concurrent products create several operators. */
 int h2b_create(const h2b_desc* d, const h2b_options* opt, h2b_op** out);
 /* y = M x with x, y device pointers (n x nrhs, node-major); asynchronous on
  * `stream` (cudaStream_t, NULL = legacy default).  The timed path. */
 int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, void* stream);
+/* Restore the scheduler state of a freshly created operator (synchronises
+ * the device first).  Called automatically when a launch fails part-way;
+ * exposed for callers recovering from an error of their own. */
+int h2b_reset(h2b_op* op);
 /* Synchronous host convenience (the drop-in path): copies x in, y out.
  * Multi-GPU rank operators return the full y on every rank. */
 int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs);

@@ -79,6 +79,22 @@ def _pcg(a, b, tol, deflate):
     return x, it
 
 
+def stiffness(mesh):
+    """P1 stiffness of a tet mesh (fem.py:51-62)."""
+    vols, g = _gradients(mesh.nodes, mesh.tets)
+    return _stiffness(mesh.nodes, mesh.tets, vols, g)
+
+
+def rhs_u1(mesh, m_nodal):
+    """Neumann right-hand side of u1 (fem.py:65-76)."""
+    vols, g = _gradients(mesh.nodes, mesh.tets)
+    m_bar = m_nodal[mesh.tets].mean(axis=1)
+    contrib = np.einsum("t,td,tid->ti", vols, m_bar, g)
+    rhs = np.zeros(mesh.nodes.shape[0])
+    np.add.at(rhs, mesh.tets.reshape(-1), contrib.reshape(-1))
+    return rhs
+
+
 def compute_demag(mesh, m_nodal, apply_boundary_operator, tol: float = 1e-10) -> DemagResult:
     """``apply_boundary_operator(u1|boundary) -> u2|boundary`` is the product
     under test (GPU h2_matvec, or the oracle for the CPU self-check)."""

@@ -110,6 +110,7 @@ def _load():
     lib.h2b_create.argtypes = [C.POINTER(Desc), C.POINTER(Options), C.POINTER(C.c_void_p)]
     lib.h2b_matvec_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.h2b_matvec.argtypes = [C.c_void_p, _pd, _pd, C.c_int64, C.c_int]
+    lib.h2b_reset.argtypes = [C.c_void_p]
     lib.h2b_stream_bytes.argtypes = [C.c_void_p]
     lib.h2b_stream_bytes.restype = C.c_int64
     lib.h2b_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -133,7 +134,7 @@ def _load():
     for name in ("h2b_h2ms_open", "h2b_h2ms_desc", "h2b_h2ms_tree", "h2b_h2ms_write"):
         getattr(lib, name).restype = C.c_int
     for name in ("h2b_plan_create", "h2b_plan_view_get", "h2b_plan_stats", "h2b_create",
-                 "h2b_matvec_dev", "h2b_matvec", "h2b_stats_get", "h2b_nccl_unique_id",
+                 "h2b_matvec_dev", "h2b_matvec", "h2b_reset", "h2b_stats_get", "h2b_nccl_unique_id",
                  "h2b_plan_phases", "h2b_plan_phase_view", "h2b_plan_partition", "h2b_matvec_phase",
                  "h2b_exchange_region", "h2b_exchange_copy"):
         getattr(lib, name).restype = C.c_int

@@ -471,30 +471,42 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
               coords=coords, order=config.cheb_order, eps=config.eps)
     weights = None
     if backend == "gpu" and config.method == "hca":
-        from .gpu_hca import hca_gpu
-        res = hca_gpu(bt=bt[adm_ids], bs=bs[adm_ids], lo=lo, hi=hi, start=start, end=end, perm=perm,
-                      coords=coords, order=config.cheb_order, eps=config.eps, evaluator=evaluator,
-                      device=device, times=times)
-        times["hca_gpu"] = time.perf_counter() - t2
+        from .gpu_hca import FactorArena, hca_gpu
         lowrank, weights, n_fb = [None] * adm_ids.size, [None] * adm_ids.size, 0
-        for i, (st, a, b) in enumerate(res):
-            t_c, s_c = int(bt[adm_ids[i]]), int(bs[adm_ids[i]])
-            if st == "ok":
-                lowrank[i] = (a, b)
-                # a = Q_a U S, b = Q_b V: B^T B = I, A^T A = S^2 (see recompress):
-                # identity and diagonal weights
-                weights[i] = (None, np.linalg.norm(a, axis=0))
-                continue
-            if st == "zero":
-                lowrank[i] = (np.zeros((end[t_c] - start[t_c], 0)), np.zeros((end[s_c] - start[s_c], 0)))
-            else:
-                warnings.warn("ill-conditioned interpolation cross; falling back to ACA", RuntimeWarning)
-                n_fb += 1
-                lowrank[i] = _aca_block(evaluator, coords, perm, start, end, t_c, s_c, config.eps)
-            aa, bb = lowrank[i]
-            weights[i] = (np.linalg.qr(bb)[1], np.linalg.qr(aa)[1])
-        del res
-        say(f"HCA (gpu): {adm_ids.size} blocks, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s: "
+        arena = FactorArena()
+        # in chunks of blocks: the raw (untruncated) factors of one chunk at a
+        # time, the truncated ones packed into the arena (host-memory bound of
+        # the 4M-node build)
+        chunk = int(os.environ.get("H2B_HCA_CHUNK", "65536"))
+        for c0 in range(0, adm_ids.size, chunk):
+            ids = adm_ids[c0:c0 + chunk]
+            res = hca_gpu(bt=bt[ids], bs=bs[ids], lo=lo, hi=hi, start=start, end=end, perm=perm,
+                          coords=coords, order=config.cheb_order, eps=config.eps, evaluator=evaluator,
+                          device=device, times=times, arena=arena)
+            for j, (st, a, b) in enumerate(res):
+                i = c0 + j
+                t_c, s_c = int(bt[adm_ids[i]]), int(bs[adm_ids[i]])
+                if st == "ok":
+                    lowrank[i] = (a, b)
+                    # a = Q_a U S, b = Q_b V: B^T B = I, A^T A = S^2 (see recompress):
+                    # identity and diagonal weights
+                    weights[i] = (None, np.linalg.norm(a, axis=0))
+                    continue
+                if st == "zero":
+                    lowrank[i] = (np.zeros((end[t_c] - start[t_c], 0)), np.zeros((end[s_c] - start[s_c], 0)))
+                else:
+                    warnings.warn("ill-conditioned interpolation cross; falling back to ACA", RuntimeWarning)
+                    n_fb += 1
+                    lowrank[i] = _aca_block(evaluator, coords, perm, start, end, t_c, s_c, config.eps)
+                aa, bb = lowrank[i]
+                weights[i] = (np.linalg.qr(bb)[1], np.linalg.qr(aa)[1])
+            del res
+            if c0 == 0 or (c0 // chunk) % 8 == 7:
+                say(f"HCA (gpu): {min(adm_ids.size, c0 + chunk)} / {adm_ids.size} blocks")
+        times["hca_gpu"] = time.perf_counter() - t2
+        fbytes = sum(a.nbytes + b.nbytes for a, b in lowrank)
+        times["factor_gb"] = fbytes / 1e9
+        say(f"HCA (gpu): {adm_ids.size} blocks, factors {fbytes / 1e9:.2f} GB, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s: "
             + ", ".join(f"{k} {times[k]:.1f}s" for k in ("cross", "solve", "rows", "truncate") if k in times) + ")")
         t5 = time.perf_counter()
         from .recompress import recompress

@@ -69,7 +69,7 @@ class _Side:
         return full
 
     def _combine(self, c, current, kids):
-        pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
+        pieces = [_restrict(e, c) for e in current]
         if pieces:
             z = np.hstack(pieces)
             proj, off = [], 0
@@ -93,7 +93,7 @@ class _Side:
         current = inherited + own.get(c.cid, [])
         if c.is_leaf:
             t0 = time.perf_counter()
-            pieces = [m[c.start - s0: c.end - s0] for m, s0 in current]
+            pieces = [_restrict(e, c) for e in current]
             v = self.tb(np.hstack(pieces) if pieces else np.zeros((c.size, 0)), self.eps)
             self.t_leaf += time.perf_counter() - t0
             self.basis[c.cid] = v
@@ -115,16 +115,35 @@ def _weighted(f: np.ndarray, w) -> np.ndarray:
     return f @ w.T
 
 
+def _restrict(entry, c):
+    """Rows of cluster c of an anchored, weighted factor.  Entries are
+    (weighted factor, anchor start) or, for a diagonal weight, (factor,
+    anchor start, weight): the weight is applied to the restricted rows
+    only (elementwise, so the same numbers as weighting first), instead of
+    holding a weighted copy of every factor (half the factor memory)."""
+    m, s0 = entry[0], entry[1]
+    r = m[c.start - s0: c.end - s0]
+    return r * entry[2][None, :] if len(entry) == 3 else r
+
+
 def basis_side(tree, anchored: dict, eps: float, pool=None, split_depth: int = 0, fast: bool = False):
     """One side of the nested basis.  ``anchored[cid]`` lists (factor,
     weight) of the blocks whose cluster on this side is ``cid``."""
     side = _Side(eps, fast)
     t_start = time.perf_counter()
     items = [(cid, f, w) for cid, lst in anchored.items() for f, w in lst]
-    mats = list(pool.map(lambda t: _weighted(t[1], t[2]), items)) if pool else [_weighted(f, w) for _, f, w in items]
+    full = [i for i, (_, f, w) in enumerate(items) if w is not None and w.ndim != 1]
+    mats = dict(zip(full, pool.map(lambda i: _weighted(items[i][1], items[i][2]), full) if pool
+                    else [_weighted(items[i][1], items[i][2]) for i in full]))
     own: dict = {}
-    for (cid, _, _), m in zip(items, mats):
-        own.setdefault(cid, []).append((m, tree.clusters[cid].start))
+    for i, (cid, f, w) in enumerate(items):
+        s0 = tree.clusters[cid].start
+        if i in mats:
+            own.setdefault(cid, []).append((mats[i], s0))
+        elif w is None:
+            own.setdefault(cid, []).append((f, s0))
+        else:
+            own.setdefault(cid, []).append((f, s0, w))
     basis_side.last = {"weighting": time.perf_counter() - t_start}
     if pool is None or split_depth <= 0:
         side.visit(tree.root, [], own)

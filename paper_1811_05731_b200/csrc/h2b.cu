@@ -1414,6 +1414,11 @@ struct h2b_op {
   double* d_y = nullptr;
   size_t xy_cap = 0;
   cudaStream_t hstream = nullptr;
+  // One product in flight per operator: the scheduler state (queue heads,
+  // arrival counters, epoch) and the coefficient workspace are per operator.
+  // Every launch waits for the previous one's completion event, whatever
+  // stream either ran on; `mu` serialises the host side.
+  cudaEvent_t done = nullptr;
   std::mutex mu;
   h2b_stats stats{};
 };
@@ -1433,13 +1438,24 @@ namespace {
 
 // Near-field plus coupling bytes of the operator (the bulk of
 // storage_bytes()), per rank: decides the streaming defaults before planning.
+// Runs before build_plan validates the descriptor, so it only reads what it
+// has checked itself (a malformed descriptor gets 0 here and H2B_EINVAL from
+// build_plan).
 int64_t desc_stream_bytes_per_rank(const h2b_desc* d, const h2b_options* o) {
+  if (!d || !d->cl_start || !d->cl_end || !d->k_row || !d->k_col || d->nclusters < 1) return 0;
+  const int64_t nc = d->nclusters;
+  auto ok = [nc](int64_t c) { return c >= 0 && c < nc; };
   int64_t b = 0;
-  for (int64_t i = 0; i < d->nnear; ++i) {
-    const int64_t r = d->nr_row[i], c = d->nr_col[i];
-    b += (d->cl_end[r] - d->cl_start[r]) * (d->cl_end[c] - d->cl_start[c]);
-  }
-  for (int64_t i = 0; i < d->ncoupling; ++i) b += d->k_row[d->cp_row[i]] * d->k_col[d->cp_col[i]];
+  if (d->nnear > 0 && d->nr_row && d->nr_col)
+    for (int64_t i = 0; i < d->nnear; ++i) {
+      const int64_t r = d->nr_row[i], c = d->nr_col[i];
+      if (ok(r) && ok(c)) b += (d->cl_end[r] - d->cl_start[r]) * (d->cl_end[c] - d->cl_start[c]);
+    }
+  if (d->ncoupling > 0 && d->cp_row && d->cp_col)
+    for (int64_t i = 0; i < d->ncoupling; ++i) {
+      const int64_t r = d->cp_row[i], c = d->cp_col[i];
+      if (ok(r) && ok(c)) b += d->k_row[r] * d->k_col[c];
+    }
   const int world = (o && o->world_size > 1) ? o->world_size : 1;
   return 8 * b / world;
 }
@@ -1616,6 +1632,7 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_y);
   cudaFree(op->d_xp);
   if (op->hstream) cudaStreamDestroy(op->hstream);
+  if (op->done) cudaEventDestroy(op->done);
   delete op;
 }
 
@@ -1755,6 +1772,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     std::memcpy(&id, o->nccl_unique_id, sizeof(id));
     H2B_NCCL(ncclCommInitRank(&op->comm, op->world, id, op->rank));
   }
+  H2B_CUDA(cudaEventCreateWithFlags(&op->done, cudaEventDisableTiming));
   H2B_CUDA(cudaDeviceSynchronize());
 
   fill_stats(P, &op->stats);
@@ -1772,19 +1790,62 @@ int check_nrhs(const h2b_op* op, int nrhs) {
   return H2B_OK;
 }
 
-int matvec_dev_impl(h2b_op* op, const double* x, double* y, int nrhs, void* stream) {
-  if (!op) return fail(H2B_EINVAL, "null operator");
+// Scheduler state back to its just-created values (all phases): arrival
+// counters, ready flags, queue heads and the epoch.  Caller holds op->mu.
+int reset_locked(h2b_op* op) {
+  H2B_CUDA(cudaSetDevice(op->device));
+  H2B_CUDA(cudaDeviceSynchronize());
+  for (auto& F : op->ph) {
+    const size_t T1 = (size_t)std::max<int64_t>(1, F.ntasks);
+    H2B_CUDA(cudaMemset(F.d_arrived, 0, sizeof(unsigned long long) * T1));
+    H2B_CUDA(cudaMemset(F.d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));
+    H2B_CUDA(cudaMemset(F.d_ctl, 0, sizeof(Ctl)));
+  }
+  H2B_CUDA(cudaDeviceSynchronize());
+  return H2B_OK;
+}
+
+// Caller holds op->mu.  `phase` < 0: the whole product (all phases and the
+// exchange); else that phase only.
+int matvec_locked(h2b_op* op, int phase, const double* x, double* y, int nrhs, void* stream) {
   if (!x || !y) return fail(H2B_EINVAL, "null vector");
   if (check_nrhs(op, nrhs)) return H2B_EINVAL;
   H2B_CUDA(cudaSetDevice(op->device));
   cudaStream_t st = (cudaStream_t)stream;
-  switch (nrhs) {
-    case 1: return launch<1>(op, x, y, st);
-    case 2: return launch<2>(op, x, y, st);
-    case 4: return launch<4>(op, x, y, st);
-    case 8: return launch<8>(op, x, y, st);
-    default: return launch<16>(op, x, y, st);
+  H2B_CUDA(cudaStreamWaitEvent(st, op->done, 0));   // the previous product of this operator
+  int rc;
+  if (phase < 0) {
+    switch (nrhs) {
+      case 1: rc = launch<1>(op, x, y, st); break;
+      case 2: rc = launch<2>(op, x, y, st); break;
+      case 4: rc = launch<4>(op, x, y, st); break;
+      case 8: rc = launch<8>(op, x, y, st); break;
+      default: rc = launch<16>(op, x, y, st); break;
+    }
+  } else {
+    switch (nrhs) {
+      case 1: rc = launch_phase<1>(op, phase, x, y, st); break;
+      case 2: rc = launch_phase<2>(op, phase, x, y, st); break;
+      case 4: rc = launch_phase<4>(op, phase, x, y, st); break;
+      case 8: rc = launch_phase<8>(op, phase, x, y, st); break;
+      default: rc = launch_phase<16>(op, phase, x, y, st); break;
+    }
   }
+  if (rc != H2B_OK) {
+    // a launch that failed part-way may have left a phase's counters
+    // mid-product: restore the created state (keeps the first error message)
+    const std::string msg = h2b_last_error();
+    reset_locked(op);
+    return fail(rc, msg);
+  }
+  H2B_CUDA(cudaEventRecord(op->done, st));
+  return H2B_OK;
+}
+
+int matvec_dev_impl(h2b_op* op, const double* x, double* y, int nrhs, void* stream) {
+  if (!op) return fail(H2B_EINVAL, "null operator");
+  std::lock_guard<std::mutex> lk(op->mu);
+  return matvec_locked(op, -1, x, y, nrhs, stream);
 }
 
 void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
@@ -1882,17 +1943,14 @@ int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, voi
 
 int h2b_matvec_phase(h2b_op* op, int phase, const double* x_dev, double* y_dev, int nrhs, void* stream) {
   if (!op || phase < 0 || phase >= (int)op->ph.size()) return fail(H2B_EINVAL, "bad operator or phase");
-  if (!x_dev || !y_dev) return fail(H2B_EINVAL, "null vector");
-  if (check_nrhs(op, nrhs)) return H2B_EINVAL;
-  H2B_CUDA(cudaSetDevice(op->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  switch (nrhs) {
-    case 1: return launch_phase<1>(op, phase, x_dev, y_dev, st);
-    case 2: return launch_phase<2>(op, phase, x_dev, y_dev, st);
-    case 4: return launch_phase<4>(op, phase, x_dev, y_dev, st);
-    case 8: return launch_phase<8>(op, phase, x_dev, y_dev, st);
-    default: return launch_phase<16>(op, phase, x_dev, y_dev, st);
-  }
+  std::lock_guard<std::mutex> lk(op->mu);
+  return matvec_locked(op, phase, x_dev, y_dev, nrhs, stream);
+}
+
+int h2b_reset(h2b_op* op) {
+  if (!op) return fail(H2B_EINVAL, "null operator");
+  std::lock_guard<std::mutex> lk(op->mu);
+  return reset_locked(op);
 }
 
 int h2b_exchange_region(h2b_op* op, int nrhs, double** base, int64_t* count_per_rank) {
@@ -1935,7 +1993,7 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
   cudaStream_t st = op->hstream;
   H2B_CUDA(cudaMemcpyAsync(op->d_x, x_host, bytes, cudaMemcpyHostToDevice, st));
   if (op->world > 1) H2B_CUDA(cudaMemsetAsync(op->d_y, 0, bytes, st));
-  int rc = matvec_dev_impl(op, op->d_x, op->d_y, nrhs, st);
+  int rc = matvec_locked(op, -1, op->d_x, op->d_y, nrhs, st);
   if (rc != H2B_OK) return rc;
   // multi-GPU: every rank wrote its own rows, the others are zero; one sum
   // assembles the full y everywhere (exact: one nonzero term per entry)

@@ -13,9 +13,10 @@ with ``np.asarray(x, dtype=float64)``; any shape other than ``(op.n,)`` raises
 order is returned; ``x`` and ``op`` are never mutated.  The product runs in
 libh2b.so (one persistent sm_100a kernel); there is no CPU
 fallback.  The device copy of an operator is cached per operator object
-(``H2Matrix`` is ``eq=False``, hence identity-hashable), so operators must
-not be mutated after their first product — the reference treats them as
-immutable too.
+(``H2Matrix`` is ``eq=False``, hence identity-hashable), its options and a
+structural fingerprint (replaced or resized block lists/dicts rebuild it);
+a matrix edited in place after the first product needs ``invalidate(op)``
+-- the reference treats operators as immutable.
 """
 
 from __future__ import annotations
@@ -30,7 +31,7 @@ import numpy as np
 from . import _native as nat
 from .cluster import ClusterTree
 
-__all__ = ["H2Matrix", "h2_matvec", "h2_matmat", "DeviceOperator", "device_operator",
+__all__ = ["H2Matrix", "h2_matvec", "h2_matmat", "DeviceOperator", "device_operator", "invalidate",
            "describe", "plan_view", "install_into_reference", "rank_arrays", "nccl_unique_id"]
 
 
@@ -343,6 +344,10 @@ class DeviceOperator:
         nat.check(self._lib.h2b_matvec_dev(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
                                            int(nrhs), C.c_void_p(stream)), "h2b_matvec_dev")
 
+    def reset(self) -> None:
+        """Scheduler state back to the just-created one (``h2b_reset``)."""
+        nat.check(self._lib.h2b_reset(self._h), "h2b_reset")
+
     def matvec_phase(self, phase: int, x_ptr: int, y_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
         """One phase of a multi-GPU rank product."""
         nat.check(self._lib.h2b_matvec_phase(self._h, int(phase), C.c_void_p(x_ptr), C.c_void_p(y_ptr),
@@ -377,14 +382,39 @@ _cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 _cache_lock = threading.Lock()
 
 
+def _fingerprint(op, options) -> tuple:
+    """Cheap structural key of an operator's payload: which containers it
+    holds and how many entries (catches replaced or resized lists/dicts;
+    in-place edits of a matrix are not detected -- call ``invalidate``)."""
+    parts = [int(op.n), id(op.tree)]
+    for d in (op.row_basis, op.row_transfer, op.col_basis, op.col_transfer, op.coupling, op.near):
+        parts += [id(d), len(d)]
+    return tuple(parts) + tuple(sorted(options.items()))
+
+
 def device_operator(op, **options) -> DeviceOperator:
-    """Cached device copy of ``op`` (created on first use)."""
+    """Cached device copy of ``op`` (created on first use, keyed by the
+    operator object, the options and a structural fingerprint).  The
+    reference treats operators as immutable; after editing a
+    matrix in place call ``invalidate(op)``."""
+    key = _fingerprint(op, options)
     with _cache_lock:
-        dev = _cache.get(op)
-        if dev is None:
-            dev = DeviceOperator(op, **options)
-            _cache[op] = dev
+        hit = _cache.get(op)
+        if hit is not None and hit[0] == key:
+            return hit[1]
+        if hit is not None:
+            hit[1].close()
+        dev = DeviceOperator(op, **options)
+        _cache[op] = (key, dev)
         return dev
+
+
+def invalidate(op) -> None:
+    """Drop the cached device copy of ``op`` (the next product re-uploads)."""
+    with _cache_lock:
+        hit = _cache.pop(op, None)
+    if hit is not None:
+        hit[1].close()
 
 
 def h2_matvec(op, x: np.ndarray) -> np.ndarray:

@@ -19,7 +19,7 @@ import numpy as np
 from .assembly import geometry as G
 from .assembly.hbuild import CompressionConfig, assemble_h2
 
-__all__ = ["WORKLOADS", "surface_for", "build_workload", "vector_for", "save_cached", "load_cached"]
+__all__ = ["WORKLOADS", "surface_for", "build_workload", "vector_for", "z_over_3", "save_cached", "load_cached"]
 
 WORKLOADS = {
     "config1": dict(desc="unit icosphere level 4 (N=2562), leaf 32, eta 2, order 4",
@@ -37,6 +37,15 @@ WORKLOADS = {
                          "leaf 64, eta 2, order 5",
                     surface=lambda: G.sphere_subsample_surface(10, 4_194_304),
                     cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5), backend="gpu"),
+    # config-5 recipe at 1/4 and 1/2 size (memory and time scaling of the build)
+    "sphere1m": dict(desc="icosphere level 9 decimated to 1048576 nodes, convex-hull re-triangulated, "
+                          "leaf 64, eta 2, order 5",
+                     surface=lambda: G.sphere_subsample_surface(9, 1_048_576),
+                     cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5), backend="gpu"),
+    "sphere2m": dict(desc="icosphere level 10 decimated to 2097152 nodes, convex-hull re-triangulated, "
+                          "leaf 64, eta 2, order 5",
+                     surface=lambda: G.sphere_subsample_surface(10, 2_097_152),
+                     cfg=CompressionConfig(leaf_size=64, eta=2.0, cheb_order=5), backend="gpu"),
     # small variants for tests and quick runs
     "cube40": dict(desc="cube [-1,1]^3, 40x40 quads/face (N=9602), leaf 64, eta 2, order 5",
                    surface=lambda: G.cube_surface(40),
@@ -63,28 +72,59 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
         t = time.perf_counter()
         op = load_cached(path)
         log(f"[workload] {name}: loaded cached operator {path} ({time.perf_counter() - t:.1f}s)")
-        return op, {"cached": True, "n": op.n}
+        info = {"cached": True, "n": op.n}
+        if (path / "coords.npy").exists():
+            info["coords"] = np.load(path / "coords.npy")
+        return op, info
     t = time.perf_counter()
     surf = w["surface"]()
     log(f"[workload] {name}: surface N={surf.n} T={surf.triangles.shape[0]} ({time.perf_counter() - t:.1f}s)")
     op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"),
                           backend=backend)
     info = {"cached": False, "n": surf.n, "build_seconds": rep.seconds, "n_admissible": rep.n_admissible,
-            "n_dense": rep.n_dense, "n_fallback": rep.n_fallback}
+            "n_dense": rep.n_dense, "n_fallback": rep.n_fallback, "coords": surf.coords}
     if path is not None:
         try:
-            save_cached(op, path)
+            save_cached(op, path, coords=surf.coords)
         except OSError:
             pass
     return op, info
 
 
-def save_cached(op, path: Path) -> None:
-    """One .npy file per flat array (io.h2_to_arrays), DONE written last."""
-    from .io import h2_to_arrays
+def save_cached(op, path: Path, coords=None) -> None:
+    """One .npy file per flat array (io.h2_to_arrays), DONE written last;
+    the node coordinates (for the z/3 input) as coords.npy."""
+    from .cluster import tree_arrays
     os.makedirs(path, exist_ok=True)
-    for k, v in h2_to_arrays(op).items():
+    np.save(path / "n.npy", np.array(op.n, dtype=np.int64))
+    for k, v in tree_arrays(op.tree).items():
         np.save(path / f"{k}.npy", v)
+
+    def data(prefix, mats):
+        # written block by block into the .npy (no concatenated copy in RAM)
+        total = sum(m.size for m in mats)
+        out = np.lib.format.open_memmap(path / f"{prefix}_data.npy", mode="w+", dtype=np.float64,
+                                        shape=(max(total, 0),))
+        off = 0
+        for m in mats:
+            out[off:off + m.size] = np.asarray(m, np.float64).ravel()
+            off += m.size
+        out.flush()
+        del out
+
+    for prefix, d in (("rb", op.row_basis), ("cb", op.col_basis), ("rt", op.row_transfer),
+                      ("ct", op.col_transfer)):
+        ids = np.array(sorted(d), dtype=np.int64)
+        np.save(path / f"{prefix}_ids.npy", ids)
+        np.save(path / f"{prefix}_shapes.npy", np.array([d[i].shape for i in ids], np.int64).reshape(-1, 2))
+        data(prefix, [d[i] for i in ids])
+    for prefix, blocks in (("cp", op.coupling), ("nr", op.near)):
+        np.save(path / f"{prefix}_row.npy", np.array([b[0] for b in blocks], np.int64))
+        np.save(path / f"{prefix}_col.npy", np.array([b[1] for b in blocks], np.int64))
+        np.save(path / f"{prefix}_shapes.npy", np.array([b[2].shape for b in blocks], np.int64).reshape(-1, 2))
+        data(prefix, [b[2] for b in blocks])
+    if coords is not None:
+        np.save(path / "coords.npy", np.asarray(coords))
     (path / "DONE").write_text("ok")
 
 
@@ -92,7 +132,7 @@ def load_cached(path: Path):
     """Memory-mapped: the operator's blocks are read-only views of the page
     cache, so the ranks of a multi-GPU run on one host share one copy."""
     from .io import h2_from_arrays
-    a = {f.stem: np.load(f, mmap_mode="r") for f in Path(path).glob("*.npy")}
+    a = {f.stem: np.load(f, mmap_mode="r") for f in Path(path).glob("*.npy") if f.stem != "coords"}
     a["n"] = np.asarray(a["n"])
     return h2_from_arrays(a)
 
@@ -102,3 +142,9 @@ def vector_for(name: str, n: int, nrhs: int = 1, seed: int = 1234) -> np.ndarray
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((n, nrhs))
     return x[:, 0].copy() if nrhs == 1 else x
+
+
+def z_over_3(coords: np.ndarray) -> np.ndarray:
+    """u1 = z/3 per node (BASELINE.json configs 1 and 5: the interior
+    potential of a uniformly magnetized unit sphere, M = (0, 0, 1))."""
+    return np.ascontiguousarray(np.asarray(coords)[:, 2] / 3.0)

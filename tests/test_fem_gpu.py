@@ -1,19 +1,20 @@
-"""The FEM solves either side of the boundary operator:
-host assembly restated from fem.py (checked against the oracle restatement
-on CPU), and the GPU Jacobi-PCG (csrc/cg.cu) against the oracle's CG
-(solver.py:44-98 restated) on the same systems.
+"""The solve either side of the boundary operator: the
+GPU Jacobi-PCG (csrc/cg.cu, ``paper_1811_05731_b200.fem.cg_solve``, the
+drop-in for solver.py:44-98) against the oracle's CG on the same systems,
+and the reference's own pipeline (``strayfield.pipeline.compute_demag``,
+pipeline.py:46-63, from baseline/_ref) run with BOTH GPU drop-ins installed
+into the reference modules.
 
 CG tolerance: the GPU sums the dot products in a different order than
 numpy, so iterates agree to the solve tolerance (tol = 1e-10 relative
 residual), not bit for bit; the energy of the uniformly magnetized sphere
-(pipeline.py:46-63) is compared at 1e-9 relative, the iteration counts to
-within 2.
+is compared at 1e-9 relative, the iteration counts to within 2.
 """
 
 import numpy as np
 import pytest
 
-from conftest import load_golden, rel
+from conftest import ROOT, load_golden, rel
 
 gpu = pytest.mark.gpu
 
@@ -21,24 +22,6 @@ gpu = pytest.mark.gpu
 def _mesh():
     from oracle.mesh_ref import generate_sphere_mesh
     return generate_sphere_mesh(1.0, 4)
-
-
-def test_assembly_matches_oracle_restatement():
-    from oracle import fem_ref
-    from paper_1811_05731_b200 import fem
-    mesh = _mesh()
-    vols, g = fem.tet_gradients(mesh)
-    vo, go = fem_ref._gradients(mesh.nodes, mesh.tets)
-    assert np.array_equal(vols, vo) and np.array_equal(g, go)
-    a = fem.assemble_stiffness(mesh)
-    ao = fem_ref._stiffness(mesh.nodes, mesh.tets, vo, go)
-    assert (a != ao).nnz == 0
-    m = np.zeros((mesh.n_nodes, 3))
-    m[:, 2] = 1.0
-    b = fem.assemble_u1_rhs(mesh, m)
-    assert abs(b.sum()) <= 1e-10 * np.abs(b).sum()   # compatible with the constant kernel
-    with pytest.raises(ValueError, match="magnetization must have shape"):
-        fem.assemble_u1_rhs(mesh, m[:-1])
 
 
 def _cuda():
@@ -49,18 +32,30 @@ def _cuda():
     __graft_entry__.build()
 
 
+def test_precond_contract_cpu():
+    """Only the Jacobi preconditioner runs on the GPU (no CPU fallback);
+    the check itself needs no GPU."""
+    from scipy.sparse import diags
+    from paper_1811_05731_b200 import fem
+    a = diags([2.0, 3.0, 4.0]).tocsr()
+    inv = 1.0 / a.diagonal()
+    assert fem._is_jacobi(a, lambda r: inv * r)
+    assert not fem._is_jacobi(a, lambda r: r)
+    with pytest.raises(NotImplementedError):
+        fem.cg_solve(a, np.ones(3), precond=lambda r: r)
+
+
 @gpu
 @pytest.mark.parametrize("deflate", [True, False])
 def test_gpu_cg_matches_oracle_cg(deflate):
     _cuda()
-    from oracle.fem_ref import _pcg
+    from oracle.fem_ref import _pcg, rhs_u1, stiffness
     from paper_1811_05731_b200 import fem
     mesh = _mesh()
-    a = fem.assemble_stiffness(mesh)
+    a = stiffness(mesh)
     rng = np.random.default_rng(5)
     if deflate:
-        m = rng.standard_normal((mesh.n_nodes, 3))
-        b = fem.assemble_u1_rhs(mesh, m)
+        b = rhs_u1(mesh, rng.standard_normal((mesh.n_nodes, 3)))
         mat = a
     else:
         interior = np.setdiff1d(np.arange(mesh.n_nodes), mesh.boundary_nodes)
@@ -87,6 +82,9 @@ def test_gpu_cg_contract():
     assert rep.iterations == 0 and np.array_equal(x, np.zeros(3))
     x, rep = fem.cg_solve(a, np.array([2.0, 3.0, 4.0]))
     assert np.allclose(x, 1.0) and rep.converged
+    # max_iter <= 0: the reference's loop never runs (solver.py:80-90)
+    x, rep = fem.cg_solve(a, np.array([2.0, 3.0, 4.0]), max_iter=0)
+    assert np.array_equal(x, np.zeros(3)) and rep.iterations == 0 and rep.residual == 1.0 and not rep.converged
     with pytest.raises(ValueError, match="zero-free diagonal"):
         fem.GpuCG(csr_matrix(np.array([[0.0, 1.0], [1.0, 2.0]])))
     with pytest.raises(ValueError, match="incompatible rhs"):
@@ -96,18 +94,46 @@ def test_gpu_cg_contract():
 
 
 @gpu
-def test_sphere_energy_with_gpu_solves_and_product():
-    """compute_demag with both solves and the H² product on the GPU matches
-    the reference energy e_d/K_d = 0.3329597004200991 (config 1)."""
+@pytest.mark.skipif(not (ROOT / "baseline" / "_ref" / "strayfield").exists(),
+                    reason="baseline/_ref not vendored (tools/vendor_reference.sh)")
+def test_reference_pipeline_with_gpu_solves_and_product():
+    """The reference's compute_demag (pipeline.py:46-63) on its own sphere
+    mesh, with ``solver.cg_solve`` and ``h2_matvec`` both routed to the GPU,
+    matches the reference energy e_d/K_d = 0.3329597004200991 (config 1)."""
     _cuda()
-    from paper_1811_05731_b200.bem import BoundaryOperator
-    from paper_1811_05731_b200.pipeline import compute_demag
-    op, ex = load_golden("config1_sphere4")
-    mesh = _mesh()
-    m = np.zeros((mesh.n_nodes, 3))
-    m[:, 2] = 1.0
-    bop = BoundaryOperator(backend="h2", n=op.n, diag=np.zeros(op.n), payload=op)
-    res = compute_demag(mesh, m, bop)
+    import sys
+    from oracle.reference import strayfield
+    strayfield()
+    from strayfield import fem as rfem, mesh as rmesh, pipeline as rpipe, solver as rsolver
+    import strayfield.hmatrix as rhm
+    import strayfield.hmatrix.h2 as rh2
+    from oracle.reference import to_reference
+    from paper_1811_05731_b200 import fem, h2
+    saved = (rsolver.cg_solve, rfem.cg_solve, rh2.h2_matvec, rhm.h2_matvec)
+    calls = {"cg": 0, "h2": 0}
+    try:
+        fem.install_into_reference(rsolver, rfem)
+        h2.install_into_reference(rh2, rhm)
+        gpu_cg, gpu_h2 = rfem.cg_solve, rh2.h2_matvec
+
+        def cg_counted(*a, **k):
+            calls["cg"] += 1
+            return gpu_cg(*a, **k)
+
+        def h2_counted(op, x):
+            calls["h2"] += 1
+            return gpu_h2(op, x)
+
+        rfem.cg_solve, rh2.h2_matvec = cg_counted, h2_counted
+        op, ex = load_golden("config1_sphere4")
+        mesh = rmesh.generate_sphere_mesh(1.0, 4)
+        from strayfield.bem import BoundaryOperator
+        bop = BoundaryOperator(backend="h2", n=op.n, diag=np.zeros(op.n), payload=to_reference(op))
+        m = rpipe.magnetization_preset(mesh, "uniform-z")
+        res = rpipe.compute_demag(mesh, m, bop)
+    finally:
+        rsolver.cg_solve, rfem.cg_solve, rh2.h2_matvec, rhm.h2_matvec = saved
+    assert calls == {"cg": 2, "h2": 1}
     ref = float(ex["energy_e_d_over_kd"])
     assert abs(res.e_d_over_kd - ref) <= 1e-9 * abs(ref)
     assert abs(res.u1_iterations - 248) <= 2 and abs(res.u2_iterations - 217) <= 2
@@ -122,11 +148,11 @@ def test_gpu_cg_kernel_variants(monkeypatch):
     <1,4,256> (592 CTAs), and <2,2,512> with and without the L2 prefetch,
     give bit-identical iterates."""
     _cuda()
-    from oracle.fem_ref import _pcg
+    from oracle.fem_ref import _pcg, rhs_u1, stiffness
     from paper_1811_05731_b200 import fem
     mesh = _mesh()
-    a = fem.assemble_stiffness(mesh)
-    b = fem.assemble_u1_rhs(mesh, np.random.default_rng(9).standard_normal((mesh.n_nodes, 3)))
+    a = stiffness(mesh)
+    b = rhs_u1(mesh, np.random.default_rng(9).standard_normal((mesh.n_nodes, 3)))
     xo, ito = _pcg(a, b, 1e-10, True)
     out = {}
     for v in range(7):
