@@ -31,6 +31,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -265,6 +266,34 @@ __global__ void __launch_bounds__(256) h2b_permute_kernel(const double* __restri
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pos = i / NRHS, r = i - pos * NRHS;
     xp[i] = __ldg(x + __ldg(perm + pos) * NRHS + r);
+  }
+}
+
+// Multi-GPU host path: this rank's rows (tree positions [lo, lo + cnt)) of
+// y, packed in tree order, then every rank's packed rows back to node order.
+__global__ void __launch_bounds__(256) h2b_pack_rows_kernel(const double* __restrict__ y,
+                                                            const int64_t* __restrict__ perm, int64_t lo,
+                                                            int64_t cnt, int nrhs, double* __restrict__ out) {
+  const int64_t total = cnt * nrhs;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = i / nrhs, r = i - pos * nrhs;
+    out[i] = y[perm[lo + pos] * nrhs + r];
+  }
+}
+
+__global__ void __launch_bounds__(256) h2b_unpack_rows_kernel(const double* __restrict__ rows,
+                                                              const int64_t* __restrict__ perm,
+                                                              const int64_t* __restrict__ rank_lo, int world,
+                                                              int64_t n, int64_t rows_max, int nrhs,
+                                                              double* __restrict__ y) {
+  const int64_t total = n * nrhs;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = i / nrhs, r = i - pos * nrhs;
+    int q = world - 1;  // owner of tree position pos (ranges ascending)
+    while (q > 0 && rank_lo[q] > pos) --q;
+    y[perm[pos] * nrhs + r] = rows[((int64_t)q * rows_max + (pos - rank_lo[q])) * nrhs + r];
   }
 }
 
@@ -1408,6 +1437,11 @@ struct h2b_op {
   // multi-GPU
   int rank = 0, world = 1;
   int64_t exch_off = 0, exch_count = 0;
+  std::vector<int64_t> rank_lo, rank_hi;  // tree-position rows of every rank
+  int64_t rows_max = 0;                   // max rows of a rank
+  int64_t* d_rank_lo = nullptr;           // [world] on the device
+  double* d_rows = nullptr;               // host path: gathered rows (world * rows_max * nrhs)
+  size_t rows_cap = 0;
   ncclComm_t comm = nullptr;
   // host path buffers
   double* d_x = nullptr;
@@ -1491,7 +1525,7 @@ void fill_stats(const h2b::Plan& P, h2b_stats* s) {
   std::memset(s, 0, sizeof(*s));
   s->n = P.n;
   s->stream_bytes = P.stream_bytes;
-  s->pool_bytes = 8 * (int64_t)P.mat.size();
+  s->pool_bytes = 8 * P.mat_len;
   s->coef_doubles = P.coef_len;
   for (const auto& F : P.ph) {
     s->ntasks += F.ntasks();
@@ -1631,6 +1665,8 @@ void free_op(h2b_op* op) {
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_xp);
+  cudaFree(op->d_rank_lo);
+  cudaFree(op->d_rows);
   if (op->hstream) cudaStreamDestroy(op->hstream);
   if (op->done) cudaEventDestroy(op->done);
   delete op;
@@ -1699,6 +1735,78 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   return H2B_OK;
 }
 
+int host_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(16u, h ? h : 1u));
+}
+
+// The pool straight from the descriptor's matrices to the device, packed
+// by host threads into two pinned staging buffers that alternate with the
+// copies: no host copy of the whole pool (config 5: ~29 GB).
+int upload_pool(const h2b::Plan& P, double* d_mat) {
+  constexpr size_t kStage = size_t(64) << 20;  // doubles per staging buffer (512 MB)
+  double* stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  int rc = H2B_OK;
+  auto cleanup = [&]() {
+    if (st) cudaStreamSynchronize(st);
+    for (int k = 0; k < 2; ++k) {
+      if (stage[k]) cudaFreeHost(stage[k]);
+      if (ev[k]) cudaEventDestroy(ev[k]);
+    }
+    if (st) cudaStreamDestroy(st);
+  };
+  auto cuda = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == H2B_OK) rc = fail(H2B_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return e == cudaSuccess;
+  };
+  const size_t cap = std::min<size_t>(kStage, std::max<int64_t>(1, P.mat_len));
+  if (!cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream") ||
+      !cuda(cudaMallocHost((void**)&stage[0], sizeof(double) * cap), "cudaMallocHost") ||
+      !cuda(cudaMallocHost((void**)&stage[1], sizeof(double) * cap), "cudaMallocHost") ||
+      !cuda(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event") ||
+      !cuda(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event")) {
+    cleanup();
+    return rc;
+  }
+  const int threads = host_threads();
+  size_t g = 0, k = 0;
+  const size_t G = P.groups.size();
+  while (g < G && rc == H2B_OK) {
+    while (g < G && P.groups[g].base < 0) ++g;
+    if (g >= G) break;
+    // groups [g, g1) fill at most one staging buffer (a larger group alone)
+    const int64_t b0 = P.groups[g].base;
+    size_t g1 = g;
+    int64_t end = b0;
+    while (g1 < G) {
+      const auto& q = P.groups[g1];
+      if (q.base >= 0) {
+        if (q.base + q.size() - b0 > (int64_t)cap && g1 > g) break;
+        end = q.base + q.size();
+      }
+      ++g1;
+    }
+    if (end - b0 > (int64_t)cap) {  // one group above 512 MB: pack it through host memory
+      std::vector<double> tmp((size_t)(end - b0));
+      h2b::pack_groups(P, g, g1, tmp.data(), threads);
+      cuda(cudaStreamSynchronize(st), "sync");
+      cuda(cudaMemcpy(d_mat + b0, tmp.data(), sizeof(double) * tmp.size(), cudaMemcpyHostToDevice), "upload");
+    } else {
+      cuda(cudaEventSynchronize(ev[k]), "sync");   // the copy that last used this buffer
+      h2b::pack_groups(P, g, g1, stage[k], threads);
+      cuda(cudaMemcpyAsync(d_mat + b0, stage[k], sizeof(double) * (size_t)(end - b0), cudaMemcpyHostToDevice, st),
+           "upload");
+      cuda(cudaEventRecord(ev[k], st), "event");
+      k ^= 1;
+    }
+    g = g1;
+  }
+  cleanup();
+  return rc;
+}
+
 int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (!out) return fail(H2B_EINVAL, "null output pointer");
   *out = nullptr;
@@ -1746,18 +1854,19 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->world = P.world_size;
   op->exch_off = P.exch_off;
   op->exch_count = P.exch_count;
+  op->rank_lo = P.rank_lo;
+  op->rank_hi = P.rank_hi;
+  for (size_t r = 0; r < P.rank_lo.size(); ++r) op->rows_max = std::max(op->rows_max, P.rank_hi[r] - P.rank_lo[r]);
 
-  // +2 doubles: a 16-byte-rounded TMA copy of the last item may read past the end
-  P.mat.push_back(0.0);
-  P.mat.push_back(0.0);
-  // the pool plus 32 bytes: bulk copies round a matrix's end up to 16 bytes
-  if ((rc = upload<double>(&op->d_mat, nullptr, P.mat.size() + 4))) return rc;
-  H2B_CUDA(cudaMemcpy(op->d_mat, P.mat.data(), sizeof(double) * P.mat.size(), cudaMemcpyHostToDevice));
-  P.mat.resize(P.mat.size() - 2);
+  // the pool plus 48 bytes: bulk copies round a matrix's end up to 16 bytes
+  if ((rc = upload<double>(&op->d_mat, nullptr, (size_t)P.mat_len + 6))) return rc;
+  H2B_CUDA(cudaMemset(op->d_mat + P.mat_len, 0, sizeof(double) * 6));
+  if ((rc = upload_pool(P, op->d_mat))) return rc;
   op->ph.resize(P.ph.size());
   for (size_t k = 0; k < P.ph.size(); ++k)
     if ((rc = upload_phase(P.ph[k], &op->ph[k]))) return rc;
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
+  if ((rc = upload(&op->d_rank_lo, P.rank_lo.data(), P.rank_lo.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
   if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
@@ -1891,6 +2000,7 @@ int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
     std::string err;
     int rc = h2b::build_plan(d, to_plan_options(d, opt), &p->plan, &err);
     if (rc != H2B_OK) return fail(rc, err);
+    h2b::pack_pool(&p->plan, host_threads());
     fill_stats(p->plan, &p->stats);
     *out = p.release();
     return H2B_OK;
@@ -1992,14 +2102,30 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
   if (!op->hstream) H2B_CUDA(cudaStreamCreate(&op->hstream));
   cudaStream_t st = op->hstream;
   H2B_CUDA(cudaMemcpyAsync(op->d_x, x_host, bytes, cudaMemcpyHostToDevice, st));
-  if (op->world > 1) H2B_CUDA(cudaMemsetAsync(op->d_y, 0, bytes, st));
   int rc = matvec_locked(op, -1, op->d_x, op->d_y, nrhs, st);
   if (rc != H2B_OK) return rc;
-  // multi-GPU: every rank wrote its own rows, the others are zero; one sum
-  // assembles the full y everywhere (exact: one nonzero term per entry)
+  // multi-GPU: every rank wrote its own rows; an all-gather of the owned
+  // rows (packed in tree order, padded to the largest rank) assembles the
+  // full y everywhere
   if (op->world > 1) {
     if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
-    H2B_NCCL(ncclAllReduce(op->d_y, op->d_y, (size_t)n * std::max(1, nrhs), ncclDouble, ncclSum, op->comm, st));
+    const int nr = std::max(1, nrhs);
+    const size_t per = (size_t)op->rows_max * nr;
+    if (op->rows_cap < per * op->world) {
+      cudaFree(op->d_rows);
+      op->d_rows = nullptr;
+      op->rows_cap = 0;
+      H2B_CUDA(cudaMalloc(&op->d_rows, sizeof(double) * per * op->world));
+      op->rows_cap = per * op->world;
+    }
+    const int64_t lo = op->rank_lo[op->rank], cnt = op->rank_hi[op->rank] - lo;
+    double* mine = op->d_rows + per * op->rank;
+    h2b_pack_rows_kernel<<<(int)std::min<int64_t>(1184, (cnt * nr + 255) / 256 + 1), 256, 0, st>>>(
+        op->d_y, op->d_perm, lo, cnt, nr, mine);
+    H2B_NCCL(ncclAllGather(mine, op->d_rows, per, ncclDouble, op->comm, st));
+    h2b_unpack_rows_kernel<<<(int)std::min<int64_t>(1184, (n * nr + 255) / 256 + 1), 256, 0, st>>>(
+        op->d_rows, op->d_perm, op->d_rank_lo, op->world, n, op->rows_max, nr, op->d_y);
+    H2B_CUDA(cudaGetLastError());
   }
   H2B_CUDA(cudaMemcpyAsync(y_host, op->d_y, bytes, cudaMemcpyDeviceToHost, st));
   H2B_CUDA(cudaStreamSynchronize(st));

@@ -17,6 +17,7 @@
 #include <array>
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 namespace h2b {
 namespace {
@@ -47,7 +48,10 @@ struct Piece {
 };
 
 struct TaskTmp {
-  int64_t data, out, bias;
+  int64_t data;      // pool offset (set once the groups have their bases)
+  int32_t group;     // pool group
+  int64_t goff;      // offset inside the group
+  int64_t out, bias;
   int32_t m, ld, ncols, kind, bias_nslots, bias_stride;
   int32_t stage;
   int32_t qclass = 0;
@@ -83,6 +87,8 @@ class Builder {
   bool is_leaf(int32_t c) const { return d_->cl_child[2 * c] < 0; }
 
   int validate(std::string* err);
+  // pool offsets of the groups used by the selected tasks (in group order)
+  void assign_bases(const std::vector<char>& sel);
   void alloc_vec(Vec* v, int32_t len, int32_t nslots) {
     v->len = len;
     v->nslots = nslots;
@@ -196,21 +202,17 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
                          bool seg0_hi) {
   Plan& P = *plan_;
   if (m_total <= 0) return;
-  // 1. pack the group matrix (m_total x C, column-major, ld = m_total)
+  // 1. the group matrix (m_total x C, column-major, ld = m_total): recorded,
+  // packed later (pack_groups) once it is known whether this rank uses it
   int64_t C = 0;
   for (auto& s : segs) C += s.ncols;
-  const int64_t base = (int64_t)P.mat.size();
-  P.mat.resize(base + (size_t)m_total * C);
-  double* dst = P.mat.data() + base;
-  for (auto& s : segs) {
-    const int64_t cnt = (int64_t)m_total * s.ncols;
-    if (!s.transpose) {
-      std::memcpy(dst, s.a, sizeof(double) * cnt);
-    } else {
-      for (int64_t j = 0; j < s.ncols; ++j)
-        for (int64_t i = 0; i < m_total; ++i) dst[j * m_total + i] = s.a[i * s.a_ld + j];
-    }
-    dst += cnt;
+  const int32_t gid = (int32_t)P.groups.size();
+  {
+    Group g;
+    g.m = m_total;
+    g.ncols = C;
+    for (auto& s : segs) g.segs.push_back({s.a, s.ncols, s.transpose, s.a_ld});
+    P.groups.push_back(std::move(g));
   }
   P.bytes_by_kind[kind] += 8 * (int64_t)m_total * C;
   // 2. split columns into pieces of <= task_bytes (at segment boundaries when possible)
@@ -276,7 +278,9 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
     deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
     for (int32_t r0 = 0; r0 < m_total; r0 += kMaxRows) {
       TaskTmp t;
-      t.data = base + pc.col0 * m_total + r0;
+      t.data = -1;
+      t.group = gid;
+      t.goff = pc.col0 * m_total + r0;
       t.m = std::min<int32_t>(kMaxRows, m_total - r0);
       t.ld = m_total;
       t.ncols = (int32_t)pc.ncols;
@@ -330,7 +334,6 @@ int Builder::run(std::string* err) {
   for (int64_t b = 0; b < d->ncoupling; ++b) entries += d->k_row[d->cp_row[b]] * d->k_col[d->cp_col[b]];
   for (int64_t b = 0; b < d->nnear; ++b) entries += size((int32_t)d->nr_row[b]) * size((int32_t)d->nr_col[b]);
   P.stream_bytes = 8 * entries;
-  P.mat.reserve((size_t)entries);
 
   xhat_.assign(nc, Vec());
   yhat_.assign(nc, Vec());
@@ -425,9 +428,13 @@ int Builder::run(std::string* err) {
   }
   // Entries never read by the product (e.g. row bases of an operator
   // without coupling blocks) are not packed, so the pool can be smaller.
-  if ((int64_t)P.mat.size() > entries) {
-    *err = "internal: packed pool larger than storage_bytes";
-    return H2B_EINVAL;
+  {
+    int64_t all = 0;
+    for (const auto& g : P.groups) all += g.size();
+    if (all > entries) {
+      *err = "internal: packed pool larger than storage_bytes";
+      return H2B_EINVAL;
+    }
   }
 
   const int32_t T = (int32_t)tasks_.size();
@@ -438,6 +445,7 @@ int Builder::run(std::string* err) {
     std::iota(all.begin(), all.end(), 0);
     P.ph.resize(1);
     P.local_bytes = P.stream_bytes;
+    assign_bases(std::vector<char>(T, 1));
     return finalize(&P.ph[0], all, std::vector<char>(T, 1), err);
   }
 
@@ -572,9 +580,27 @@ int Builder::run(std::string* err) {
         *err = "internal: rank plan is missing a dependency";
         return H2B_EINVAL;
       }
+  // this rank's pool: only the matrices of its selected items (the
+  // replicated upper clusters plus its own rows), so per-rank host and
+  // device memory scale as 1/world
+  assign_bases(sel);
   rc = finalize(&P.ph[0], ids0, in0, err);
   if (rc != H2B_OK) return rc;
   return finalize(&P.ph[1], ids1, in1, err);
+}
+
+void Builder::assign_bases(const std::vector<char>& sel) {
+  Plan& P = *plan_;
+  std::vector<char> used(P.groups.size(), 0);
+  for (size_t i = 0; i < tasks_.size(); ++i)
+    if (sel[i]) used[tasks_[i].group] = 1;
+  int64_t off = 0;
+  for (size_t g = 0; g < P.groups.size(); ++g) {
+    P.groups[g].base = used[g] ? off : -1;
+    if (used[g]) off += P.groups[g].size();
+  }
+  P.mat_len = off;
+  for (auto& t : tasks_) t.data = P.groups[t.group].base >= 0 ? P.groups[t.group].base + t.goff : -1;
 }
 
 int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char>& in_phase, std::string* err) {
@@ -759,6 +785,55 @@ int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char
 }
 
 }  // namespace
+
+namespace {
+void pack_one(const Group& g, double* dst) {
+  const int64_t m = g.m;
+  for (const auto& s : g.segs) {
+    const int64_t cnt = m * s.ncols;
+    if (!s.transpose) {
+      std::memcpy(dst, s.a, sizeof(double) * cnt);
+    } else {
+      // row-major (m x ncols) with row stride a_ld -> column-major: tiles
+      // of 32 rows so both sides stay in cache lines
+      for (int64_t i0 = 0; i0 < m; i0 += 32) {
+        const int64_t i1 = std::min<int64_t>(m, i0 + 32);
+        for (int64_t j = 0; j < s.ncols; ++j)
+          for (int64_t i = i0; i < i1; ++i) dst[j * m + i] = s.a[i * s.a_ld + j];
+      }
+    }
+    dst += cnt;
+  }
+}
+}  // namespace
+
+void pack_groups(const Plan& P, size_t g0, size_t g1, double* dst, int threads) {
+  if (g0 >= g1) return;
+  int64_t b0 = -1;
+  std::vector<size_t> used;
+  for (size_t g = g0; g < g1; ++g)
+    if (P.groups[g].base >= 0) {
+      if (b0 < 0) b0 = P.groups[g].base;
+      used.push_back(g);
+    }
+  if (used.empty()) return;
+  threads = std::max(1, std::min<int>(threads, (int)used.size()));
+  auto work = [&](int t) {
+    for (size_t k = t; k < used.size(); k += threads) {
+      const Group& G = P.groups[used[k]];
+      pack_one(G, dst + (G.base - b0));
+    }
+  };
+  if (threads == 1) { work(0); return; }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (auto& th : pool) th.join();
+}
+
+void pack_pool(Plan* P, int threads) {
+  P->mat.assign((size_t)P->mat_len, 0.0);
+  pack_groups(*P, 0, P->groups.size(), P->mat.data(), threads);
+}
 
 int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string* err) {
   if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= std::max(1, opt.world_size)) {

@@ -68,6 +68,24 @@ struct Phase {
   int64_t nsegs() const { return (int64_t)s_ncols.size(); }
 };
 
+// One packed matrix of the pool: the column blocks of a work-item group
+// (m rows, column-major, ld = m), copied from the descriptor's host arrays
+// when the pool is materialised (pack_pool).  base < 0: not used by this
+// rank's plan (multi-GPU) and not packed.
+struct PackSeg {
+  const double* a;   // source block
+  int64_t ncols;
+  bool transpose;    // false: a is (ncols x m) row-major == (m x ncols) col-major
+  int64_t a_ld;      // row stride of a when transposed
+};
+struct Group {
+  int64_t base = -1;
+  int32_t m = 0;
+  int64_t ncols = 0;
+  std::vector<PackSeg> segs;
+  int64_t size() const { return (int64_t)m * ncols; }
+};
+
 // The execution plan of one operator on one rank.  Single GPU: one phase.
 // world_size > 1: phase 0 computes the upward coefficients
 // x^ of the clusters this rank owns into its exchange region of the
@@ -79,7 +97,9 @@ struct Phase {
 struct Plan {
   int64_t n = 0;
   std::vector<int64_t> perm;
-  std::vector<double> mat;  // packed matrix pool
+  std::vector<Group> groups;  // the pool's matrices (pointers into the descriptor)
+  int64_t mat_len = 0;        // doubles of this rank's pool
+  std::vector<double> mat;    // host copy of the pool (pack_pool; empty after a streamed upload)
   int64_t coef_len = 0;     // doubles per right-hand side
   int64_t stream_bytes = 0; // == H2Matrix.storage_bytes()
   int64_t bytes_by_kind[5] = {0, 0, 0, 0, 0};
@@ -102,7 +122,15 @@ struct PlanOptions {
 };
 
 // Validates the descriptor and builds the plan.  Returns H2B_OK or an error
-// code with a message in *err.
+// code with a message in *err.  The pool itself is not packed (the groups
+// point into the descriptor's arrays): see pack_pool / pack_groups.
 int build_plan(const h2b_desc* d, const PlanOptions& opt, Plan* out, std::string* err);
+
+// Copies groups [g0, g1) of the pool to dst, which corresponds to pool offset
+// groups[g0].base (the used groups are contiguous in group order); skips
+// unused groups.  Uses up to `threads` host threads.
+void pack_groups(const Plan& P, size_t g0, size_t g1, double* dst, int threads);
+// Materialises the whole pool in P.mat (host).
+void pack_pool(Plan* P, int threads);
 
 }  // namespace h2b
