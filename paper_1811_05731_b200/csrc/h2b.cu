@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -796,7 +797,7 @@ __device__ __forceinline__ void gather_commit(GatherBatch<NRHS>& g, int lane, in
 // leaves HBM idle).  The sources of chunk j + 1 are gathered into the other
 // half of the warp's source buffer while chunk j multiplies.  `rpar` holds
 // the ring's mbarrier parities (bit s).
-template <int NRHS>
+template <int NRHS, int STAGE = kRingStageBytes>
 __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
                                                   const WarpRing R, unsigned& rpar, int lane,
                                                   unsigned long long& t_gath) {
@@ -808,7 +809,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   const int g = lane >> 2, t = lane & 3;
   // columns per stage (>= 16), a whole number of 4-column k-steps so that
   // the DMMA sums group columns exactly like the register-staged loop
-  const int cs = min(kHalf, kRingStageBytes / (8 * m)) & ~3;  // multi-RHS rings: 8 KB stages
+  const int cs = min(kHalf, STAGE / (8 * m)) & ~3;  // multi-RHS rings: 8 KB stages (4 KB: lean kernel option)
   const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
@@ -1393,6 +1394,53 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   }
 }
 
+// The near field of a multi-RHS product (8 or 16 right-hand sides) on its
+// own: near items have no inputs but x, so this lean kernel needs none of
+// the dataflow kernel's scheduling -- warps claim items (longest first) from
+// one counter and stream each through a TMA ring onto the DMMA tiles
+// (run_item_mma_ring), writing the items' partial slots.  Small code and
+// register footprint; the dataflow kernel then runs the rest of the product
+// (Plan::ph_split).  STAGE: ring stage bytes (8 KB: 8 warps per SM; 4 KB:
+// 16 warps per SM, the same bytes in flight).
+template <int NRHS, int STAGE>
+__global__ void __launch_bounds__(256, STAGE <= 4096 ? 2 : 1) h2b_near_kernel(KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
+  unsigned char* rb = smem_raw + (size_t)nw * sizeof(WarpSmem) + (size_t)wib * ring_bytes(STAGE);
+  WarpRing ring{reinterpret_cast<double*>(rb), reinterpret_cast<uint64_t*>(rb + 2 * (STAGE + 32)),
+                (STAGE + 32) / 8};
+  if (lane == 0) {
+    mbar_init(ring.bars);
+    mbar_init(ring.bars + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned rpar = 0;
+  unsigned long long t_gath = 0;
+  for (;;) {
+    int item = -1;
+    if (lane == 0) {
+      const unsigned s = atomicAdd(&p.ctl->near_head, 1u);
+      if (s < (unsigned)p.nready0) item = __ldg(p.ready0 + s);
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item < 0) break;
+    const DTask T = p.tasks[item];
+    DSeg sin{0, 0, 0, 0, 0};
+    if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
+    if (T.ld == T.m && T.m <= 64 && T.ncols > 0) {
+      run_item_mma_ring<NRHS, STAGE>(p, T, sin, w, ring, rpar, lane, t_gath);
+    } else {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(&w.bar);
+      run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, 0u, t_gath);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 namespace h2b_detail {
@@ -1434,6 +1482,10 @@ struct h2b_op {
   int sched = 0;       // effective sched_flags (defaults applied)
   int ring_stage = kRingStageBytes;  // NRHS < 8: ring stage payload (sched_flags bits 18-19)
   std::vector<PhaseDev> ph;
+  // single GPU, 8/16 right-hand sides: near field (lean kernel), then the rest
+  std::vector<PhaseDev> ph_split;
+  int near_stage = 8192;    // lean near kernel ring stage (H2B_NEAR_STAGE=4096: 16 warps per SM)
+  int near_grid = 0;
   // multi-GPU
   int rank = 0, world = 1;
   int64_t exch_off = 0, exch_count = 0;
@@ -1565,10 +1617,9 @@ int occupancy_grid(int wpc, int ring_warps, int ring_stage, int ctas_per_sm, int
   return H2B_OK;
 }
 
-// xp = x[perm] then phase k of the plan.
+// xp = x[perm] (when `permute`) then one phase of the plan.
 template <int NRHS>
-int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st) {
-  const PhaseDev& F = op->ph[k];
+int launch_phase_dev(h2b_op* op, const PhaseDev& F, const double* x, double* y, cudaStream_t st, bool permute) {
   KParams p;
   p.tasks = F.d_tasks;
   p.segs = F.d_segs;
@@ -1597,7 +1648,7 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kRingStageBytes)
                                 : smem_bytes(op->wpc, op->ring_warps, op->ring_stage);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
-  if (k == 0) {
+  if (permute) {
     const int64_t total = op->n * NRHS;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
     h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
@@ -1616,9 +1667,55 @@ int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st)
   return H2B_OK;
 }
 
+template <int NRHS>
+int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st) {
+  return launch_phase_dev<NRHS>(op, op->ph[k], x, y, st, k == 0);
+}
+
+template <int NRHS, int STAGE>
+int launch_near(h2b_op* op, cudaStream_t st) {
+  const PhaseDev& F = op->ph_split[0];
+  if (F.ntasks == 0) return H2B_OK;
+  KParams p{};
+  p.tasks = F.d_tasks;
+  p.segs = F.d_segs;
+  p.seg_inline = F.d_seg_inline;
+  p.ready0 = F.d_ready0;
+  p.nready0 = F.nready0;
+  p.ctl = F.d_ctl;
+  p.ntasks = (int32_t)F.ntasks;
+  p.mat = op->d_mat;
+  p.coef = op->d_coef;
+  p.perm = op->d_perm;
+  p.xp = op->d_xp;
+  p.flags = op->flags;
+  const size_t smem = (size_t)op->wpc * sizeof(WarpSmem) + (size_t)op->wpc * ring_bytes(STAGE);
+  H2B_CUDA(cudaMemsetAsync(&F.d_ctl->near_head, 0, sizeof(unsigned), st));
+  H2B_CUDA(cudaFuncSetAttribute(h2b_near_kernel<NRHS, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  h2b_near_kernel<NRHS, STAGE><<<op->near_grid, op->wpc * 32, smem, st>>>(p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(H2B_ECUDA, std::string("near kernel launch: ") + cudaGetErrorString(e));
+  return H2B_OK;
+}
+
+// 8/16 right-hand sides on one GPU: xp, the near field (lean kernel), then
+// the rest of the product (dataflow kernel, near dependencies satisfied).
+template <int NRHS>
+int launch_split(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+  const int64_t total = op->n * NRHS;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
+  int rc = op->near_stage == 4096 ? launch_near<NRHS, 4096>(op, st) : launch_near<NRHS, 8192>(op, st);
+  if (rc != H2B_OK) return rc;
+  return launch_phase_dev<NRHS>(op, op->ph_split[1], x, y, st, false);
+}
+
 // The whole product: all phases, with the x^ all-gather between them.
 template <int NRHS>
 int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+  if constexpr (NRHS >= 8) {
+    if (!op->ph_split.empty()) return launch_split<NRHS>(op, x, y, st);
+  }
   for (int k = 0; k < (int)op->ph.size(); ++k) {
     int rc = launch_phase<NRHS>(op, k, x, y, st);
     if (rc != H2B_OK) return rc;
@@ -1658,6 +1755,7 @@ void free_phase(PhaseDev& F) {
 void free_op(h2b_op* op) {
   if (!op) return;
   for (auto& F : op->ph) free_phase(F);
+  for (auto& F : op->ph_split) free_phase(F);
   if (op->comm) ncclCommDestroy(op->comm);
   cudaFree(op->d_mat);
   cudaFree(op->d_coef);
@@ -1817,7 +1915,13 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   }
   h2b::Plan P;
   std::string err;
-  int rc = h2b::build_plan(d, to_plan_options(d, o), &P, &err);
+  h2b::PlanOptions po = to_plan_options(d, o);
+  // 8/16 right-hand sides on one GPU: the near field in the lean kernel
+  // (H2B_NEAR_SPLIT=0: the near field inside the dataflow kernel, round 1)
+  const int max_nrhs_req = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
+  const char* ns_env = std::getenv("H2B_NEAR_SPLIT");
+  po.near_split = po.world_size <= 1 && max_nrhs_req >= 8 && !(ns_env && ns_env[0] == '0');
+  int rc = h2b::build_plan(d, po, &P, &err);
   if (rc != H2B_OK) return fail(rc, err);
   for (const auto& F : P.ph) {
     if (F.ntasks() >= INT32_MAX / kQueues) return fail(H2B_EINVAL, "too many work items");
@@ -1865,6 +1969,9 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->ph.resize(P.ph.size());
   for (size_t k = 0; k < P.ph.size(); ++k)
     if ((rc = upload_phase(P.ph[k], &op->ph[k]))) return rc;
+  op->ph_split.resize(P.ph_split.size());
+  for (size_t k = 0; k < P.ph_split.size(); ++k)
+    if ((rc = upload_phase(P.ph_split[k], &op->ph_split[k]))) return rc;
   if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
   if ((rc = upload(&op->d_rank_lo, P.rank_lo.data(), P.rank_lo.size()))) return rc;
   if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
@@ -1876,6 +1983,23 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[2]))) return rc;
   if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[3]))) return rc;
   if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[4]))) return rc;
+  if (!op->ph_split.empty()) {
+    const char* st_env = std::getenv("H2B_NEAR_STAGE");
+    op->near_stage = (st_env && std::atoi(st_env) == 4096) ? 4096 : 8192;
+    const size_t sm = (size_t)op->wpc * sizeof(WarpSmem) + (size_t)op->wpc * ring_bytes(op->near_stage);
+    int per_sm = 0, dev = 0, nsm = 0;
+    if (op->near_stage == 4096) {
+      H2B_CUDA(cudaFuncSetAttribute(h2b_near_kernel<16, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_near_kernel<16, 4096>, op->wpc * 32, sm));
+    } else {
+      H2B_CUDA(cudaFuncSetAttribute(h2b_near_kernel<16, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_near_kernel<16, 8192>, op->wpc * 32, sm));
+    }
+    H2B_CUDA(cudaGetDevice(&dev));
+    H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm < 1) return fail(H2B_EINVAL, "near kernel does not fit an SM");
+    op->near_grid = per_sm * nsm;
+  }
   if (op->world > 1 && o && o->nccl_unique_id) {
     ncclUniqueId id;
     std::memcpy(&id, o->nccl_unique_id, sizeof(id));
@@ -1904,7 +2028,8 @@ int check_nrhs(const h2b_op* op, int nrhs) {
 int reset_locked(h2b_op* op) {
   H2B_CUDA(cudaSetDevice(op->device));
   H2B_CUDA(cudaDeviceSynchronize());
-  for (auto& F : op->ph) {
+  for (auto* list : {&op->ph, &op->ph_split})
+  for (auto& F : *list) {
     const size_t T1 = (size_t)std::max<int64_t>(1, F.ntasks);
     H2B_CUDA(cudaMemset(F.d_arrived, 0, sizeof(unsigned long long) * T1));
     H2B_CUDA(cudaMemset(F.d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));

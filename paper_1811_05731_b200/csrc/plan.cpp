@@ -446,7 +446,18 @@ int Builder::run(std::string* err) {
     P.ph.resize(1);
     P.local_bytes = P.stream_bytes;
     assign_bases(std::vector<char>(T, 1));
-    return finalize(&P.ph[0], all, std::vector<char>(T, 1), err);
+    rc = finalize(&P.ph[0], all, std::vector<char>(T, 1), err);
+    if (rc != H2B_OK || !opt_.near_split) return rc;
+    std::vector<char> is_near(T, 0), not_near(T, 0);
+    std::vector<int32_t> near_ids, rest_ids;
+    for (int32_t i = 0; i < T; ++i) {
+      if (tasks_[i].kind == kNear) { is_near[i] = 1; near_ids.push_back(i); }
+      else { not_near[i] = 1; rest_ids.push_back(i); }
+    }
+    P.ph_split.resize(2);
+    rc = finalize(&P.ph_split[0], near_ids, is_near, err);
+    if (rc != H2B_OK) return rc;
+    return finalize(&P.ph_split[1], rest_ids, not_near, err);
   }
 
   // ---- multi-GPU: byte-balanced contiguous leaf ranges (tree order is a

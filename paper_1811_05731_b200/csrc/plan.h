@@ -106,6 +106,10 @@ struct Plan {
   int32_t rank = 0, world_size = 1;
   int64_t local_bytes = 0;  // matrix bytes streamed by this rank
   std::vector<Phase> ph;
+  // Single GPU, PlanOptions::near_split: the same items in two launches --
+  // the near field alone (no dependencies: the lean multi-RHS kernel), then
+  // everything else (its near-field dependencies satisfied by the first).
+  std::vector<Phase> ph_split;
   int64_t exch_off = 0, exch_count = 0;
   std::vector<int64_t> rank_lo, rank_hi;  // tree-position range of each rank's leaves
 };
@@ -117,6 +121,7 @@ struct PlanOptions {
   int32_t final_class = 0;        // queue class of the final items (0: chain, 2: slack)
   int32_t near_phase0_pct = 90;   // multi-GPU: percent of the rank's near bytes in phase 0 (0: none)
   bool interleave = true;
+  bool near_split = false;        // also plan Plan::ph_split (single GPU)
   int32_t rank = 0;
   int32_t world_size = 1;
 };

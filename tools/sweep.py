@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--flush", action="store_true", help="flush L2 before each timed step")
     ap.add_argument("--nrhs", default="1", help="comma list of right-hand-side counts")
     ap.add_argument("--ablate", default="", help="comma list of: far (near=[]), near (coupling=[])")
+    ap.add_argument("--env", default="[{}]", help='JSON list of environment settings read at create, '
+                                                  'e.g. [{"H2B_NEAR_SPLIT":"0"},{}]')
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -44,10 +46,19 @@ def main():
     from bench import DeviceTimer
     timer = DeviceTimer(s, flush=a.flush)
     refs = {}
-    for (name, opx), nrhs, vals in itertools.product(ops.items(), nrhs_list,
-                                                     itertools.product(*[grid[k] for k in keys])):
+    import os
+    envs = json.loads(a.env)
+    for (name, opx), nrhs, vals, env in itertools.product(ops.items(), nrhs_list,
+                                                          itertools.product(*[grid[k] for k in keys]), envs):
         opts = dict(zip(keys, vals))
+        old_env = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
         dev = DeviceOperator(opx, **opts)
+        for k, v in old_env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
         st = dev.stats()
         x = torch.from_numpy(np.ascontiguousarray(vector_for(a.config, op.n, nrhs))).cuda()
         y = torch.empty_like(x)
@@ -58,7 +69,7 @@ def main():
         ref = refs.setdefault((name, nrhs), yy)
         err = float(np.linalg.norm(yy - ref) / np.linalg.norm(ref))
         gbs = (st["stream_bytes"] + 16 * op.n * nrhs) / (ms * 1e-3) / 1e9
-        print(json.dumps({"op": name, "nrhs": nrhs, "opts": opts, "ms": round(ms, 4), "GB/s": round(gbs, 1),
+        print(json.dumps({"op": name, "nrhs": nrhs, "opts": opts, "env": env, "ms": round(ms, 4), "GB/s": round(gbs, 1),
                           "ms_per_vector": round(ms / nrhs, 4), "items": st["ntasks"],
                           "grid": st["grid"], "rel_vs_first": err}), flush=True)
         dev.close()
