@@ -109,7 +109,7 @@ def _is_jacobi(a, precond) -> bool:
     d = np.asarray(a.diagonal(), dtype=np.float64)
     probe = np.random.default_rng(0).standard_normal(d.shape[0])
     with np.errstate(divide="ignore", invalid="ignore"):
-        want = probe / d
+        want = (1.0 / d) * probe      # solver.py:27-37: inv = 1.0 / diag; inv * r
     got = np.asarray(precond(probe), dtype=np.float64)
     return got.shape == want.shape and np.array_equal(got, want)
 

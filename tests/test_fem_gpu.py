@@ -40,6 +40,11 @@ def test_precond_contract_cpu():
     a = diags([2.0, 3.0, 4.0]).tocsr()
     inv = 1.0 / a.diagonal()
     assert fem._is_jacobi(a, lambda r: inv * r)
+    from oracle.reference import available, strayfield
+    if available():   # the reference's own preconditioner object
+        strayfield()
+        from strayfield.solver import jacobi_preconditioner
+        assert fem._is_jacobi(a, jacobi_preconditioner(a))
     assert not fem._is_jacobi(a, lambda r: r)
     with pytest.raises(NotImplementedError):
         fem.cg_solve(a, np.ones(3), precond=lambda r: r)

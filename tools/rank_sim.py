@@ -9,7 +9,14 @@ coefficients phase 1 reads are stale -- the work and the bytes are the
 same, the values are not checked.  The max over ranks models the step time
 of an N-GPU run; ranks never wait on each other here.  Both scheduling
 modes are timed (plain, and the streaming defaults forced) to place the
-H2B_STREAM_DEFAULT_BYTES threshold."""
+H2B_STREAM_DEFAULT_BYTES threshold.
+
+The all-gather is added back as a modeled term: every rank's exchange
+region (x^ of the clusters it owns; h2b_exchange_region) is all-gathered,
+W * region * 8 bytes in total, costed at a fixed latency plus that volume
+over NVLink 5 (--ag-latency-us, --ag-gbs: NCCL all-gather of small messages
+on 8 GPUs behind NVSwitch; not measured here, only one GPU is available).
+``modeled_ms = max over ranks (phase 0 + phase 1) + all-gather``."""
 
 import argparse
 import json
@@ -33,6 +40,9 @@ def main():
     ap.add_argument("--cache-dir", default="/tmp/h2b_cache")
     ap.add_argument("--pct", default="0", help="comma list of near_phase0_pct values (0: default)")
     ap.add_argument("--modes", default="plain,streaming")
+    ap.add_argument("--defaults", action="store_true", help="also time the library defaults (no forced mode)")
+    ap.add_argument("--ag-latency-us", type=float, default=15.0)
+    ap.add_argument("--ag-gbs", type=float, default=300.0)
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -45,12 +55,16 @@ def main():
     s = torch.cuda.current_stream()
     for world in [int(w) for w in a.worlds.split(",")]:
         modes = [(m, dict(PLAIN if m == "plain" else STREAMING, near_phase0_pct=int(pc)))
-                 for m in a.modes.split(",") for pc in a.pct.split(",")]
+                 for m in filter(None, a.modes.split(",")) for pc in a.pct.split(",")]
+        if a.defaults:
+            modes.append(("defaults", dict(near_phase0_pct=0)))
         for mode, opts in modes:
             per_rank = []
+            exch = 0
             for r in range(world):
                 dev = DeviceOperator(op, world_size=world, rank=r, **opts)
                 st = dev.stats()
+                exch = dev.exchange_region(1)[1] if world > 1 else 0
                 phases = 1 if world == 1 else 2
                 run = lambda: [dev.matvec_phase(k, x.data_ptr(), y.data_ptr(), 1, s.cuda_stream)
                                for k in range(phases)]
@@ -65,8 +79,13 @@ def main():
                 per_rank.append((e0.elapsed_time(e1) / a.steps, int(st["local_bytes"])))
                 dev.close()
             t = max(p[0] for p in per_rank)
+            ag_bytes = 8 * exch * world
+            ag_ms = 0.0 if world == 1 else (a.ag_latency_us + ag_bytes / (a.ag_gbs * 1e3)) / 1e3
             print(json.dumps({"config": a.config, "world": world, "mode": mode,
                               "near_phase0_pct": opts["near_phase0_pct"], "max_rank_ms": round(t, 4),
+                              "allgather_bytes": ag_bytes, "allgather_ms_modeled": round(ag_ms, 4),
+                              "modeled_ms": round(t + ag_ms, 4),
+                              "modeled_DOF_per_s_with_allgather": op.n / ((t + ag_ms) * 1e-3),
                               "rank_ms": [round(p[0], 4) for p in per_rank],
                               "rank_bytes": [p[1] for p in per_rank],
                               "modeled_DOF_per_s": op.n / (t * 1e-3)}), flush=True)
