@@ -123,6 +123,10 @@ typedef struct h2b_desc {
    continuations): the leaf-level downward items, which become ready
    together, then do not pull every warp off the near-field stream */
 #define H2B_SCHED_PRIO_NO_CHAIN (1 << 30)
+/* sched_flags bit 31: the near-priority warps' mix (H2B_SCHED_LEAF_MIX)
+   serves the coupling rows of inner clusters (they gate the downward chain)
+   before the leaf coupling rows */
+#define H2B_SCHED_MIX_INNER ((int)(1u << 31))
 /* sched_flags bits 26-29: the top k warps of each CTA take near-field items
    before the up-leaf items and the coupling queues (0: none) */
 #define H2B_SCHED_NEAR_PRIO(k) (((k) & 0xf) << 26)

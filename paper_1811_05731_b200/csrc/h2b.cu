@@ -131,6 +131,7 @@ constexpr int kFlagSlackFirst = 1;  // inner coupling rows before the claimed-ah
 constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming instead of the TMA ring
 constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, acquire fence on completion
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
+constexpr int kFlagMixInner = (int)(1u << 31);  // near-priority warps' mix serves inner coupling rows too
 constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
@@ -1173,6 +1174,13 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         if (nprio) {
           // near-priority warps apply the leaf mix too: otherwise the leaf
           // coupling rows wait for the other warps and trail the near field
+          // (with kFlagMixInner the coupling rows of inner clusters first:
+          // they gate the downward chain)
+          if (leaf_mix && near_run >= leaf_thr && owed < 0 && (p.flags & kFlagMixInner) && h[1] < t[1] &&
+              (item = claim(1)) >= 0) {
+            near_run = 0;
+            break;
+          }
           if (leaf_mix && near_run >= leaf_thr && owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) {
             near_run = 0;
             break;
@@ -1394,6 +1402,127 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   }
 }
 
+// mbarrier expecting `bytes` from the bulk copies issued next (one arrival).
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// Near-field stage of the multi-RHS near kernel: kNearCols columns of the
+// item's matrix (<= 64 rows, column-major) and the same columns' sources
+// (rows of xp, NRHS doubles each) -- both moved by TMA bulk copies into one
+// stage, completing one mbarrier.
+constexpr int kNearCols = 16;
+template <int NRHS>
+struct NearStage {
+  static constexpr int kA = kNearCols * 64 * 8 + 32;          // matrix chunk (+ 16-byte rounding)
+  static constexpr int kX = kNearCols * NRHS * 8;             // source rows
+  static constexpr int kBytes = (kA + kX + 127) / 128 * 128;
+};
+template <int NRHS>
+__host__ __device__ constexpr int near_warp_smem(int nst) {
+  return (int)((sizeof(WarpSmem) + 127) / 128 * 128) + nst * NearStage<NRHS>::kBytes + 128;
+}
+
+// One near item (ld == m <= 64, x segments only) with NRHS = 8 or 16: per
+// stage one bulk copy of the matrix chunk and one per source segment piece
+// (a near segment is a contiguous range of xp: the nodes of a source leaf,
+// node-major), NST stages in flight, DMMA tiles over the staged operands.
+// The k-steps group columns exactly like run_item_mma(_ring): same bits.
+template <int NRHS, int NST>
+__device__ __forceinline__ void run_near_tma(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
+                                             unsigned char* stages, uint64_t* bars, unsigned& par, int lane,
+                                             uint64_t pol) {
+  using S = NearStage<NRHS>;
+  constexpr int NT = NRHS / 8;
+  constexpr int MT = 4;
+  const int m = T.m;
+  const int mtiles = (m + 15) >> 4;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = (T.ncols + kNearCols - 1) / kNearCols;
+  const double* g0 = p.mat + T.data;
+  int kseg = 0;  // lane 0: segment cursor (chunks are issued in column order)
+  auto issue = [&](int j) {  // lane 0
+    unsigned char* st = stages + (j % NST) * S::kBytes;
+    uint64_t* bar = bars + (j % NST);
+    const int col = j * kNearCols;
+    const int cc = min(kNearCols, T.ncols - col);
+    const double* src = g0 + (int64_t)col * m;
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of this stage are done
+    mbar_expect(bar, (unsigned)(a1 - a0) + (unsigned)(cc * NRHS * 8));
+    bulk_copy_hint(st, (const void*)a0, (unsigned)(a1 - a0), bar, pol);
+    double* xs = reinterpret_cast<double*>(st + S::kA);
+    int c = col;
+    while (c < col + cc) {
+      while (w.seg_off[kseg + 1] <= c) ++kseg;
+      const int hi = min(col + cc, w.seg_off[kseg + 1]);
+      const int64_t e = (w.seg_src[kseg] + (c - w.seg_off[kseg])) * NRHS;
+      bulk_copy(xs + (c - col) * NRHS, p.xp + e, (unsigned)((hi - c) * NRHS * 8), bar);
+      c = hi;
+    }
+  };
+  load_segtable(p, T, sin, w, lane);
+  if (lane == 0)
+    for (int j = 0; j < NST && j < nch; ++j) issue(j);
+
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  for (int jc = 0; jc < nch; ++jc) {
+    const int s = jc % NST;
+    const int col = jc * kNearCols;
+    const int cc = min(kNearCols, T.ncols - col);
+    mbar_wait(bars + s, (par >> s) & 1u);
+    par ^= 1u << s;
+    const unsigned char* st = stages + s * S::kBytes;
+    const double* A = reinterpret_cast<const double*>(st) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
+    const double* xs = reinterpret_cast<const double*>(st + S::kA);
+    for (int c = 0; c < cc; c += 4) {
+      const bool okc = c + t < cc;
+      double a[MT][2];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = 16 * i + g;
+        const bool ok = okc && i < mtiles;
+        a[i][0] = (ok && r < m) ? A[(c + t) * m + r] : 0.0;
+        a[i][1] = (ok && r + 8 < m) ? A[(c + t) * m + r + 8] : 0.0;
+      }
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = okc ? xs[(c + t) * NRHS + 8 * j + g] : 0.0;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+        if (i < mtiles)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+    }
+    __syncwarp();  // every lane is done with stage s
+    if (lane == 0 && jc + NST < nch) issue(jc + NST);
+  }
+  mma_epilogue<NRHS>(p, T, acc, lane);
+}
+
 // The near field of a multi-RHS product (8 or 16 right-hand sides) on its
 // own: near items have no inputs but x, so this lean kernel needs none of
 // the dataflow kernel's scheduling -- warps claim items (longest first) from
@@ -1433,6 +1562,47 @@ __global__ void __launch_bounds__(256, STAGE <= 4096 ? 2 : 1) h2b_near_kernel(KP
     if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
     if (T.ld == T.m && T.m <= 64 && T.ncols > 0) {
       run_item_mma_ring<NRHS, STAGE>(p, T, sin, w, ring, rpar, lane, t_gath);
+    } else {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(&w.bar);
+      run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, 0u, t_gath);
+    }
+    __syncwarp();
+  }
+}
+
+// The same work with both operands moved by TMA (run_near_tma): no source
+// gathers through registers, so the L2 round trip of the sources is off the
+// per-chunk critical path.  NST stages of (matrix chunk + sources) per warp.
+template <int NRHS, int NST>
+__global__ void __launch_bounds__(256, 1) h2b_near_tma_kernel(KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* mine = smem_raw + (size_t)wib * near_warp_smem<NRHS>(NST);
+  WarpSmem& w = *reinterpret_cast<WarpSmem*>(mine);
+  unsigned char* stages = mine + (sizeof(WarpSmem) + 127) / 128 * 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NST * NearStage<NRHS>::kBytes);
+  if (lane == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(bars + s);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t pol = evict_first_policy();
+  unsigned par = 0;
+  unsigned long long t_gath = 0;
+  for (;;) {
+    int item = -1;
+    if (lane == 0) {
+      const unsigned s = atomicAdd(&p.ctl->near_head, 1u);
+      if (s < (unsigned)p.nready0) item = __ldg(p.ready0 + s);
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item < 0) break;
+    const DTask T = p.tasks[item];
+    DSeg sin{0, 0, 0, 0, 0};
+    if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
+    if (T.ld == T.m && T.m <= 64 && T.ncols > 0) {
+      run_near_tma<NRHS, NST>(p, T, sin, w, stages, bars, par, lane, pol);
     } else {
       uint64_t* bar = reinterpret_cast<uint64_t*>(&w.bar);
       run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, 0u, t_gath);
@@ -1486,6 +1656,10 @@ struct h2b_op {
   std::vector<PhaseDev> ph_split;
   int near_stage = 8192;    // lean near kernel ring stage (H2B_NEAR_STAGE=4096: 16 warps per SM)
   int near_grid = 0;
+  int near_impl = 1;        // 1: both operands by TMA (h2b_near_tma_kernel), 0: ring + register gathers
+  int near_nst = 2;         // TMA stages per warp (2: 8 warps per CTA, 3: 6 warps)
+  int near_warps = 8;
+  int split_only = 0;       // diagnostics (H2B_SPLIT_ONLY=near|rest): time one part; y is then wrong
   // multi-GPU
   int rank = 0, world = 1;
   int64_t exch_off = 0, exch_count = 0;
@@ -1698,6 +1872,39 @@ int launch_near(h2b_op* op, cudaStream_t st) {
   return H2B_OK;
 }
 
+template <int NRHS, int NST>
+int launch_near_tma(h2b_op* op, cudaStream_t st) {
+  const PhaseDev& F = op->ph_split[0];
+  if (F.ntasks == 0) return H2B_OK;
+  KParams p{};
+  p.tasks = F.d_tasks;
+  p.segs = F.d_segs;
+  p.seg_inline = F.d_seg_inline;
+  p.ready0 = F.d_ready0;
+  p.nready0 = F.nready0;
+  p.ctl = F.d_ctl;
+  p.ntasks = (int32_t)F.ntasks;
+  p.mat = op->d_mat;
+  p.coef = op->d_coef;
+  p.perm = op->d_perm;
+  p.xp = op->d_xp;
+  p.flags = op->flags;
+  const size_t smem = (size_t)op->near_warps * near_warp_smem<NRHS>(NST);
+  H2B_CUDA(cudaMemsetAsync(&F.d_ctl->near_head, 0, sizeof(unsigned), st));
+  H2B_CUDA(cudaFuncSetAttribute(h2b_near_tma_kernel<NRHS, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int per_sm = 0, dev = 0, nsm = 0;
+  H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_near_tma_kernel<NRHS, NST>,
+                                                         op->near_warps * 32, smem));
+  H2B_CUDA(cudaGetDevice(&dev));
+  H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (per_sm < 1) return fail(H2B_EINVAL, "near TMA kernel does not fit an SM");
+  h2b_near_tma_kernel<NRHS, NST><<<per_sm * nsm, op->near_warps * 32, smem, st>>>(p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(H2B_ECUDA, std::string("near TMA kernel launch: ") + cudaGetErrorString(e));
+  return H2B_OK;
+}
+
 // 8/16 right-hand sides on one GPU: xp, the near field (lean kernel), then
 // the rest of the product (dataflow kernel, near dependencies satisfied).
 template <int NRHS>
@@ -1705,8 +1912,11 @@ int launch_split(h2b_op* op, const double* x, double* y, cudaStream_t st) {
   const int64_t total = op->n * NRHS;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
   h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
-  int rc = op->near_stage == 4096 ? launch_near<NRHS, 4096>(op, st) : launch_near<NRHS, 8192>(op, st);
-  if (rc != H2B_OK) return rc;
+  int rc = H2B_OK;
+  if (op->split_only != 2)
+    rc = op->near_impl == 1 ? (op->near_nst == 3 ? launch_near_tma<NRHS, 3>(op, st) : launch_near_tma<NRHS, 2>(op, st))
+         : op->near_stage == 4096 ? launch_near<NRHS, 4096>(op, st) : launch_near<NRHS, 8192>(op, st);
+  if (rc != H2B_OK || op->split_only == 1) return rc;
   return launch_phase_dev<NRHS>(op, op->ph_split[1], x, y, st, false);
 }
 
@@ -1948,7 +2158,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     sf |= H2B_SCHED_STREAM_EVICT_FIRST;
   }
   op->sched = sf;
-  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (sf & 0x7ff3ff04);
+  op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (int)((unsigned)sf & 0xfff3ff04u);
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
     const int sel = (sf >> 18) & 3;
@@ -1986,6 +2196,13 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (!op->ph_split.empty()) {
     const char* st_env = std::getenv("H2B_NEAR_STAGE");
     op->near_stage = (st_env && std::atoi(st_env) == 4096) ? 4096 : 8192;
+    const char* im_env = std::getenv("H2B_NEAR_IMPL");
+    op->near_impl = (im_env && std::string(im_env) == "ring") ? 0 : 1;
+    const char* ns_env2 = std::getenv("H2B_NEAR_NST");
+    op->near_nst = (ns_env2 && std::atoi(ns_env2) == 3) ? 3 : 2;
+    op->near_warps = op->near_nst == 3 ? 6 : 8;
+    const char* so = std::getenv("H2B_SPLIT_ONLY");
+    op->split_only = !so ? 0 : std::string(so) == "near" ? 1 : std::string(so) == "rest" ? 2 : 0;
     const size_t sm = (size_t)op->wpc * sizeof(WarpSmem) + (size_t)op->wpc * ring_bytes(op->near_stage);
     int per_sm = 0, dev = 0, nsm = 0;
     if (op->near_stage == 4096) {

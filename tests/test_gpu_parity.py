@@ -291,9 +291,9 @@ def test_reference_test_patterns_against_dense(golden):
 @pytest.mark.parametrize("name", ["config1_sphere4", "prism_20_40_2_default", "random"])
 @pytest.mark.parametrize("nrhs", [8, 16])
 def test_multi_rhs_near_split_bit_identical(name, nrhs, monkeypatch):
-    """8/16 right-hand sides run the near field in the lean kernel
-    (h2b_near_kernel, both ring stage sizes) and the rest in the dataflow
-    kernel: the same per-item DMMA k-steps and the same fixed-order slot
+    """8/16 right-hand sides run the near field in a lean kernel (TMA for
+    both operands, 2 or 3 stages; or the ring + register-gather variant with
+    both stage sizes) and the rest in the dataflow kernel: the same per-item DMMA k-steps and the same fixed-order slot
     sums as the single dataflow launch (H2B_NEAR_SPLIT=0), so the same bits;
     all match the oracle.  "random": leaves above 64 nodes (row tiles whose
     near items take the register-staged fallback)."""
@@ -305,15 +305,21 @@ def test_multi_rhs_near_split_bit_identical(name, nrhs, monkeypatch):
     h2 = _gpu()
     X = np.random.default_rng(17).standard_normal((op.n, nrhs))
     ys = {}
-    for split, stage in (("0", "8192"), ("1", "8192"), ("1", "4096")):
-        monkeypatch.setenv("H2B_NEAR_SPLIT", split)
-        monkeypatch.setenv("H2B_NEAR_STAGE", stage)
+    variants = {"fused": {"H2B_NEAR_SPLIT": "0"},
+                "ring8k": {"H2B_NEAR_IMPL": "ring", "H2B_NEAR_STAGE": "8192"},
+                "ring4k": {"H2B_NEAR_IMPL": "ring", "H2B_NEAR_STAGE": "4096"},
+                "tma2": {}, "tma3": {"H2B_NEAR_NST": "3"}}
+    for name_v, env in variants.items():
+        for k in ("H2B_NEAR_SPLIT", "H2B_NEAR_IMPL", "H2B_NEAR_STAGE", "H2B_NEAR_NST"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         dev = h2.DeviceOperator(op)
         try:
-            ys[split, stage] = dev.matvec(X)
+            ys[name_v] = dev.matvec(X)
         finally:
             dev.close()
-    assert np.array_equal(ys["0", "8192"], ys["1", "8192"])
-    assert np.array_equal(ys["1", "8192"], ys["1", "4096"])
+    for name_v in variants:
+        assert np.array_equal(ys["fused"], ys[name_v]), name_v
     for i in range(nrhs):
-        assert rel(ys["1", "8192"][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+        assert rel(ys["tma2"][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
