@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define H2B_ABI_VERSION 2
+#define H2B_ABI_VERSION 3
 
 #define H2B_OK 0
 #define H2B_EINVAL (-1)
@@ -151,8 +151,20 @@ typedef struct h2b_options {
                               the rank's near field run in phase 0, beside the
                               latency-bound upward pass; 0 = default (90),
                               -1 = none (all in phase 1)                    */
-  int32_t pad_;
+  int32_t plan_flags;   /* H2B_PLAN_* bits; 0 = defaults                      */
 } h2b_options;
+
+/* plan_flags: the level-skipping far-field chain: upward
+   coefficients of even-height clusters from their grandchildren through
+   transfer products, downward coefficients of every other level from the
+   grandparent -- half the dependency links, one extra product matrix per
+   skipped link (h2b_stats.extra_bytes).  SKIP forces it on, NO_SKIP off. */
+#define H2B_PLAN_SKIP_LEVELS 1
+#define H2B_PLAN_NO_SKIP 2
+/* plan_flags (h2b_plan_create only): also plan the split multi-RHS product
+   (the near field alone, then the rest), exposed as phases 1 and 2 of a
+   single-GPU plan; h2b_create plans it whenever max_nrhs >= 8. */
+#define H2B_PLAN_NEAR_SPLIT 4
 
 typedef struct h2b_op h2b_op;      /* device-resident operator             */
 typedef struct h2b_plan h2b_plan;  /* host-only execution plan (no device) */
@@ -173,6 +185,8 @@ typedef struct h2b_stats {
   int64_t local_bytes;      /* bytes this rank streams                     */
   int32_t sched_flags;      /* effective scheduling (defaults applied)     */
   int32_t ring_warps;       /* single-vector TMA-ring warps per CTA        */
+  int64_t extra_bytes;      /* pool bytes beyond stream_bytes (transfer
+                               products of the level-skipping chain)       */
 } h2b_stats;
 
 /* Plan arrays for host-side inspection (tests execute them with a numpy
@@ -209,7 +223,8 @@ const char* h2b_last_error(void);
 int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out);
 int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* out);
 int h2b_plan_stats(const h2b_plan* p, h2b_stats* out);
-/* Multi-GPU plans have two phases; single-GPU plans one. */
+/* Multi-GPU plans have two phases; single-GPU plans one
+   (three with H2B_PLAN_NEAR_SPLIT: the whole product, the near field, the rest). */
 int h2b_plan_phases(const h2b_plan* p);
 int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* out);
 /* rank_lo_hi[2*world]: tree-position range of each rank's leaves;

@@ -142,7 +142,7 @@ def check_plan_invariants(plan: dict) -> None:
         seg = slice(plan["t_seg0"][t], plan["t_seg0"][t + 1])
         assert plan["s_ncols"][seg].sum() == plan["t_ncols"][t]
     assert plan["mat"].size * 8 == sum(plan["stats"]["bytes_by_kind"].values())
-    assert plan["mat"].size * 8 <= plan["stats"]["stream_bytes"]
+    assert plan["mat"].size * 8 <= plan["stats"]["stream_bytes"] + plan["stats"]["extra_bytes"]
     # every y row written exactly once
     fin = np.flatnonzero(plan["t_kind"] == 4)
     rows = np.concatenate([plan["t_out"][t] + np.arange(plan["t_m"][t]) for t in fin])

@@ -19,7 +19,7 @@ __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
 # H2B_LIB: an alternative build of the library (A/B timing of kernel variants)
 LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
-ABI_VERSION = 2  # include/h2b.h H2B_ABI_VERSION
+ABI_VERSION = 3  # include/h2b.h H2B_ABI_VERSION
 H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO, H2B_ECONV = 0, -1, -2, -3, -4, -5, -6, -7
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")
 
@@ -45,7 +45,7 @@ class Options(C.Structure):
         ("task_bytes", C.c_int64), ("far_task_bytes", C.c_int64), ("warps_per_cta", C.c_int32), ("ctas_per_sm", C.c_int32),
         ("max_nrhs", C.c_int32), ("sched_flags", C.c_int32), ("band_depth", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
-        ("near_phase0_pct", C.c_int32), ("pad_", C.c_int32),
+        ("near_phase0_pct", C.c_int32), ("plan_flags", C.c_int32),
     ]
 
 
@@ -56,7 +56,7 @@ class Stats(C.Structure):
         ("ndeps", C.c_int64), ("tasks_by_kind", C.c_int64 * 5), ("bytes_by_kind", C.c_int64 * 5),
         ("grid", C.c_int32), ("warps_per_cta", C.c_int32), ("rank", C.c_int32),
         ("world_size", C.c_int32), ("local_bytes", C.c_int64),
-        ("sched_flags", C.c_int32), ("ring_warps", C.c_int32),
+        ("sched_flags", C.c_int32), ("ring_warps", C.c_int32), ("extra_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

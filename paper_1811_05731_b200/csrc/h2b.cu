@@ -1660,6 +1660,7 @@ struct h2b_op {
   int near_nst = 2;         // TMA stages per warp (2: 8 warps per CTA, 3: 6 warps)
   int near_warps = 8;
   int split_only = 0;       // diagnostics (H2B_SPLIT_ONLY=near|rest): time one part; y is then wrong
+  int trace_split = 0;      // diagnostics (H2B_TRACE_SPLIT=1): trace the split product's dataflow part
   // multi-GPU
   int rank = 0, world = 1;
   int64_t exch_off = 0, exch_count = 0;
@@ -1743,6 +1744,8 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     else if (o->near_phase0_pct > 0) po.near_phase0_pct = std::min(100, o->near_phase0_pct);
     po.rank = o->rank;
     po.world_size = o->world_size > 0 ? o->world_size : 1;
+    if (o->plan_flags & H2B_PLAN_SKIP_LEVELS) po.skip_levels = true;
+    if (o->plan_flags & H2B_PLAN_NO_SKIP) po.skip_levels = false;
   }
   return po;
 }
@@ -1763,6 +1766,7 @@ void fill_stats(const h2b::Plan& P, h2b_stats* s) {
   s->rank = P.rank;
   s->world_size = P.world_size;
   s->local_bytes = P.local_bytes;
+  s->extra_bytes = P.extra_bytes;
 }
 
 int nrhs_index(int nrhs) {
@@ -2203,6 +2207,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     op->near_warps = op->near_nst == 3 ? 6 : 8;
     const char* so = std::getenv("H2B_SPLIT_ONLY");
     op->split_only = !so ? 0 : std::string(so) == "near" ? 1 : std::string(so) == "rest" ? 2 : 0;
+    const char* ts = std::getenv("H2B_TRACE_SPLIT");
+    op->trace_split = ts && ts[0] == '1';
     const size_t sm = (size_t)op->wpc * sizeof(WarpSmem) + (size_t)op->wpc * ring_bytes(op->near_stage);
     int per_sm = 0, dev = 0, nsm = 0;
     if (op->near_stage == 4096) {
@@ -2340,7 +2346,9 @@ int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
   try {
     std::unique_ptr<h2b_plan> p(new h2b_plan());
     std::string err;
-    int rc = h2b::build_plan(d, to_plan_options(d, opt), &p->plan, &err);
+    h2b::PlanOptions po = to_plan_options(d, opt);
+    po.near_split = po.world_size <= 1 && opt && (opt->plan_flags & H2B_PLAN_NEAR_SPLIT);
+    int rc = h2b::build_plan(d, po, &p->plan, &err);
     if (rc != H2B_OK) return fail(rc, err);
     h2b::pack_pool(&p->plan, host_threads());
     fill_stats(p->plan, &p->stats);
@@ -2353,11 +2361,12 @@ int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out) {
 
 int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* v) { return h2b_plan_phase_view(p, 0, v); }
 
-int h2b_plan_phases(const h2b_plan* p) { return p ? (int)p->plan.ph.size() : -1; }
+int h2b_plan_phases(const h2b_plan* p) { return p ? (int)(p->plan.ph.size() + p->plan.ph_split.size()) : -1; }
 
 int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* v) {
-  if (!p || !v || phase < 0 || phase >= (int)p->plan.ph.size()) return fail(H2B_EINVAL, "bad plan or phase");
-  fill_view(p->plan, p->plan.ph[phase], v);
+  const int n0 = p ? (int)p->plan.ph.size() : 0;
+  if (!p || !v || phase < 0 || phase >= n0 + (int)p->plan.ph_split.size()) return fail(H2B_EINVAL, "bad plan or phase");
+  fill_view(p->plan, phase < n0 ? p->plan.ph[phase] : p->plan.ph_split[phase - n0], v);
   return H2B_OK;
 }
 
@@ -2476,10 +2485,17 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
 
 int64_t h2b_stream_bytes(const h2b_op* op) { return op ? op->stats.stream_bytes : -1; }
 
+// The phase the trace covers: the single-GPU product's, or (H2B_TRACE_SPLIT=1
+// at create, 8/16 right-hand sides) the dataflow part of the split product.
+static PhaseDev& traced_phase(const h2b_op* op) {
+  h2b_op* o = const_cast<h2b_op*>(op);
+  return (o->trace_split && !o->ph_split.empty()) ? o->ph_split[1] : o->ph[0];
+}
+
 int h2b_trace_enable(h2b_op* op, int on) {
   if (!op) return fail(H2B_EINVAL, "null operator");
   H2B_CUDA(cudaSetDevice(op->device));
-  PhaseDev& F = op->ph[0];
+  PhaseDev& F = traced_phase(op);
   const size_t cnt = 8 * (size_t)std::max<int64_t>(1, F.ntasks);
   if (on && !F.d_trace) {
     H2B_CUDA(cudaMalloc(&F.d_trace, sizeof(unsigned long long) * cnt));
@@ -2492,16 +2508,16 @@ int h2b_trace_enable(h2b_op* op, int on) {
 }
 
 int h2b_trace_read(const h2b_op* op, uint64_t* out, int64_t nitems) {
-  if (!op || !out || nitems != op->ph[0].ntasks || !op->ph[0].d_trace)
+  if (!op || !out || nitems != traced_phase(op).ntasks || !traced_phase(op).d_trace)
     return fail(H2B_EINVAL, "trace not enabled or wrong size");
-  H2B_CUDA(cudaMemcpy(out, op->ph[0].d_trace, sizeof(uint64_t) * 8 * nitems, cudaMemcpyDeviceToHost));
+  H2B_CUDA(cudaMemcpy(out, traced_phase(op).d_trace, sizeof(uint64_t) * 8 * nitems, cudaMemcpyDeviceToHost));
   return H2B_OK;
 }
 
 int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems) {
-  if (!op || !out || nitems != op->ph[0].ntasks) return fail(H2B_EINVAL, "wrong size");
+  if (!op || !out || nitems != traced_phase(op).ntasks) return fail(H2B_EINVAL, "wrong size");
   std::vector<DTask> t(nitems);
-  H2B_CUDA(cudaMemcpy(t.data(), op->ph[0].d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
+  H2B_CUDA(cudaMemcpy(t.data(), traced_phase(op).d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < nitems; ++i) out[i] = t[i].kind;
   return H2B_OK;
 }

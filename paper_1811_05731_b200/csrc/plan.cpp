@@ -87,6 +87,19 @@ class Builder {
   bool is_leaf(int32_t c) const { return d_->cl_child[2 * c] < 0; }
 
   int validate(std::string* err);
+  // a (r x q) row-major times b (q x c) row-major -> owned (r x c) row-major
+  const double* product(const double* a, const double* b, int64_t r, int64_t q, int64_t c) {
+    auto buf = std::make_unique<std::vector<double>>((size_t)(r * c), 0.0);
+    double* o = buf->data();
+    for (int64_t i = 0; i < r; ++i)
+      for (int64_t k = 0; k < q; ++k) {
+        const double v = a[i * q + k];
+        for (int64_t j = 0; j < c; ++j) o[i * c + j] += v * b[k * c + j];
+      }
+    plan_->extra_bytes += 8 * r * c;
+    plan_->owned.push_back(std::move(buf));
+    return plan_->owned.back()->data();
+  }
   // pool offsets of the groups used by the selected tasks (in group order)
   void assign_bases(const std::vector<char>& sel);
   void alloc_vec(Vec* v, int32_t len, int32_t nslots) {
@@ -356,8 +369,22 @@ int Builder::run(std::string* err) {
       int32_t k = (int32_t)d->k_col[p];
       if (k == 0) continue;
       std::vector<SegSpec> segs;
+      const bool skip = opt_.skip_levels && height_[p] >= 2 && height_[p] % 2 == 0;
       for (int j = 0; j < 2; ++j) {
         int32_t ch = (int32_t)d->cl_child[2 * p + j];
+        if (skip && !is_leaf(ch)) {
+          // x^_p += (F_g F_ch)^T x^_g over the grandchildren g (h2.py:201-205 expanded)
+          const int64_t kc = d->k_col[ch];
+          if (kc == 0) continue;
+          for (int jj = 0; jj < 2; ++jj) {
+            const int32_t g = (int32_t)d->cl_child[2 * ch + jj];
+            if (!xhat_[g].exists()) continue;
+            const int64_t kg = d->k_col[g];
+            const double* fg = product(d->col_transfer[g], d->col_transfer[ch], kg, kc, k);
+            segs.push_back({kSegCoef, 0, (int32_t)kg, &xhat_[g], fg, false, 0});
+          }
+          continue;
+        }
         if (!xhat_[ch].exists()) continue;
         segs.push_back({kSegCoef, 0, (int32_t)d->k_col[ch], &xhat_[ch], d->col_transfer[ch], false, 0});
       }
@@ -396,14 +423,38 @@ int Builder::run(std::string* err) {
     std::vector<int32_t> order(nc);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return depth_[a] < depth_[b]; });
+    // Level skipping: an "own" cluster (inner, child of a full one) only sums
+    // its coupling rows; its children take the grandparent's coefficient
+    // through E_c E_p plus E_c times that own sum:
+    //   y^_c = E_c (E_p y^_gp + y^_p,own) + y^_c,own       (h2.py:220-235)
+    std::vector<char> own_only(nc, 0);
     for (int32_t t : order) {
       int32_t k = (int32_t)d->k_row[t];
+      // odd heights (counted from the leaves, so the leaves skip their
+      // parent's level), never two "own" levels in a row
+      if (t != 0 && opt_.skip_levels && !is_leaf(t) && height_[t] % 2 == 1 && !own_only[parent_[t]]) own_only[t] = 1;
       if (k == 0) continue;
       std::vector<SegSpec> segs;
-      if (t != 0) {
-        int32_t p = parent_[t];
-        if (yhat_[p].exists())
-          segs.push_back({kSegCoef, 0, (int32_t)d->k_row[p], &yhat_[p], d->row_transfer[t], true, d->k_row[p]});
+      bool transfer = false;
+      if (t != 0 && !own_only[t]) {
+        const int32_t p = parent_[t];
+        if (!own_only[p]) {
+          if (yhat_[p].exists()) {
+            segs.push_back({kSegCoef, 0, (int32_t)d->k_row[p], &yhat_[p], d->row_transfer[t], true, d->k_row[p]});
+            transfer = true;
+          }
+        } else if (d->k_row[p] > 0) {
+          const int32_t gp = parent_[p];
+          const int64_t kp = d->k_row[p];
+          if (yhat_[gp].exists()) {  // the chain link: E_t E_p y^_gp
+            const int64_t kg = d->k_row[gp];
+            const double* ep = product(d->row_transfer[t], d->row_transfer[p], k, kp, kg);
+            segs.push_back({kSegCoef, 0, (int32_t)kg, &yhat_[gp], ep, true, kg});
+            transfer = true;
+          }
+          if (yhat_[p].exists())   // the parent's own coupling sum (slack)
+            segs.push_back({kSegCoef, 0, (int32_t)kp, &yhat_[p], d->row_transfer[t], true, kp});
+        }
       }
       for (int64_t b : cp_by_row[t]) {
         int32_t s = (int32_t)d->cp_col[b];
@@ -412,7 +463,6 @@ int Builder::run(std::string* err) {
         segs.push_back({kSegCoef, 0, (int32_t)ks, &xhat_[s], d->cp_data[b], true, ks});
       }
       if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
-      const bool transfer = t != 0 && yhat_[parent_[t]].exists();
       cur_cl_ = t;
       emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 2 : 1, transfer);
     }
@@ -431,7 +481,7 @@ int Builder::run(std::string* err) {
   {
     int64_t all = 0;
     for (const auto& g : P.groups) all += g.size();
-    if (all > entries) {
+    if (all > entries + P.extra_bytes / 8) {
       *err = "internal: packed pool larger than storage_bytes";
       return H2B_EINVAL;
     }

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -97,7 +98,11 @@ struct Group {
 struct Plan {
   int64_t n = 0;
   std::vector<int64_t> perm;
-  std::vector<Group> groups;  // the pool's matrices (pointers into the descriptor)
+  std::vector<Group> groups;  // the pool's matrices (pointers into the descriptor or `owned`)
+  // transfer products of the level-skipping chain (PlanOptions::skip_levels),
+  // computed at planning time; groups point into them
+  std::vector<std::unique_ptr<std::vector<double>>> owned;
+  int64_t extra_bytes = 0;    // pool bytes beyond storage_bytes (the products)
   int64_t mat_len = 0;        // doubles of this rank's pool
   std::vector<double> mat;    // host copy of the pool (pack_pool; empty after a streamed upload)
   int64_t coef_len = 0;     // doubles per right-hand side
@@ -122,6 +127,13 @@ struct PlanOptions {
   int32_t near_phase0_pct = 90;   // multi-GPU: percent of the rank's near bytes in phase 0 (0: none)
   bool interleave = true;
   bool near_split = false;        // also plan Plan::ph_split (single GPU)
+  // Level-skipping far-field chain: the upward coefficients of clusters of
+  // even height come from their grandchildren through transfer products
+  // (F_g F_c)^T, and the downward coefficients of every other level from
+  // their grandparent through E_c E_p (the level between contributes only its
+  // own coupling sum), so the dependency chain through the tree has half the
+  // links.  Extra pool bytes: one product per skipped link.
+  bool skip_levels = false;
   int32_t rank = 0;
   int32_t world_size = 1;
 };

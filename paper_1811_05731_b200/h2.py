@@ -206,8 +206,14 @@ def SCHED_NEAR_PRIO(k: int) -> int:
     return (int(k) & 0xF) << 26
 
 
+PLAN_SKIP_LEVELS = 1
+PLAN_NO_SKIP = 2
+PLAN_NEAR_SPLIT = 4
+
+
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
-             band_depth=0, rank=0, world_size=1, nccl_unique_id=None, near_phase0_pct=0) -> nat.Options:
+             band_depth=0, rank=0, world_size=1, nccl_unique_id=None, near_phase0_pct=0,
+             plan_flags=0) -> nat.Options:
     o = nat.Options()
     o.task_bytes = int(task_bytes)
     o.far_task_bytes = int(far_task_bytes)
@@ -219,6 +225,7 @@ def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max
     o.rank = int(rank)
     o.world_size = int(world_size)
     o.near_phase0_pct = int(near_phase0_pct)
+    o.plan_flags = int(plan_flags)
     if nccl_unique_id is not None:
         buf = C.create_string_buffer(bytes(nccl_unique_id), 128)
         o._keep_id = buf

@@ -323,3 +323,24 @@ def test_multi_rhs_near_split_bit_identical(name, nrhs, monkeypatch):
         assert np.array_equal(ys["fused"], ys[name_v]), name_v
     for i in range(nrhs):
         assert rel(ys["tma2"][:, i], h2_matvec_ref(op, X[:, i])) <= TOL
+
+
+@pytest.mark.parametrize("nrhs", [1, 16])
+def test_level_skipping_chain_on_gpu(golden, nrhs):
+    """The level-skipping far-field chain (H2B_PLAN_SKIP_LEVELS) on the GPU:
+    the same product to rounding (1e-12), the far field checked on its own."""
+    name, op, ex = golden
+    h2 = _gpu()
+    X = np.random.default_rng(23).standard_normal((op.n, nrhs))
+    for o in (op, dataclasses.replace(op, near=[])):
+        dev = h2.DeviceOperator(o, plan_flags=h2.PLAN_SKIP_LEVELS)
+        try:
+            Y = dev.matvec(X[:, 0] if nrhs == 1 else X).reshape(op.n, nrhs)
+            Y2 = dev.matvec(X[:, 0] if nrhs == 1 else X).reshape(op.n, nrhs)
+        finally:
+            dev.close()
+        assert np.array_equal(Y, Y2)
+        for i in range(nrhs):
+            ref = h2_matvec_ref(o, X[:, i])
+            if np.linalg.norm(ref) > 0:
+                assert rel(Y[:, i], ref) <= TOL, (name, i)

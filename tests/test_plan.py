@@ -25,7 +25,7 @@ def test_abi_exports_every_declared_symbol():
     lib = ctypes.CDLL(str(nat.LIB_PATH))
     for nm in names:
         assert hasattr(lib, nm), nm
-    assert nat.lib().h2b_abi_version() == 2
+    assert nat.lib().h2b_abi_version() == 3
 
 
 @pytest.mark.parametrize("task_bytes", [0, 4096, 512])
@@ -133,3 +133,35 @@ def test_fused_runs_random_structures(seed):
         x = np.random.default_rng(seed).standard_normal(op.n)
         y = run_plan(P, x, rng=np.random.default_rng(seed + 10))
         assert rel(y, h2_matvec_ref(op, x)) <= 1e-13
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_level_skipping_chain(golden, world):
+    """The level-skipping far-field chain (H2B_PLAN_SKIP_LEVELS): even-height
+    clusters' x^ from the grandchildren through (F_g F_c)^T, every other
+    level's y^ from the grandparent through E_c E_p -- the same product to
+    rounding, with a chain of about half the links."""
+    from oracle.flat_matvec import run_ranks
+    from paper_1811_05731_b200.h2 import PLAN_SKIP_LEVELS, plan_view
+    name, op, ex = golden
+    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_SKIP_LEVELS) for r in range(world)]
+    for i in (0, 3):
+        y = run_ranks(plans, ex["X"][:, i]) if world > 1 else run_plan(plans[0], ex["X"][:, i])
+        assert rel(y, ex["y_full"][:, i]) <= 1e-13, (name, world, i)
+    if world == 1:
+        check_plan_invariants(plans[0])
+        base = plan_view(op)
+        assert plans[0]["stats"]["extra_bytes"] >= 0
+        assert chain_length(plans[0]) <= chain_length(base)
+        if chain_length(base) >= 8:   # deep enough for skipped links (config 1: 9 -> 7 items)
+            assert chain_length(plans[0]) < chain_length(base), (chain_length(plans[0]), chain_length(base))
+
+
+def chain_length(plan):
+    """Longest dependency path (items) of a single-GPU plan."""
+    T = len(plan["t_m"])
+    depth = np.zeros(T, np.int64)
+    for t in range(T):
+        d = plan["deps"][plan["t_dep0"][t]:plan["t_dep0"][t + 1]]
+        depth[t] = 1 + (depth[d].max() if d.size else 0)
+    return int(depth.max())

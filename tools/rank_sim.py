@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--defaults", action="store_true", help="also time the library defaults (no forced mode)")
     ap.add_argument("--ag-latency-us", type=float, default=15.0)
     ap.add_argument("--ag-gbs", type=float, default=300.0)
+    ap.add_argument("--plan-flags", default="0", help="comma list of h2b_options.plan_flags values")
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -54,10 +55,11 @@ def main():
     y = torch.zeros_like(x)
     s = torch.cuda.current_stream()
     for world in [int(w) for w in a.worlds.split(",")]:
-        modes = [(m, dict(PLAIN if m == "plain" else STREAMING, near_phase0_pct=int(pc)))
-                 for m in filter(None, a.modes.split(",")) for pc in a.pct.split(",")]
+        modes = [(m, dict(PLAIN if m == "plain" else STREAMING, near_phase0_pct=int(pc), plan_flags=int(pf)))
+                 for m in filter(None, a.modes.split(",")) for pc in a.pct.split(",")
+                 for pf in a.plan_flags.split(",")]
         if a.defaults:
-            modes.append(("defaults", dict(near_phase0_pct=0)))
+            modes += [("defaults", dict(near_phase0_pct=0, plan_flags=int(pf))) for pf in a.plan_flags.split(",")]
         for mode, opts in modes:
             per_rank = []
             exch = 0
@@ -82,7 +84,8 @@ def main():
             ag_bytes = 8 * exch * world
             ag_ms = 0.0 if world == 1 else (a.ag_latency_us + ag_bytes / (a.ag_gbs * 1e3)) / 1e3
             print(json.dumps({"config": a.config, "world": world, "mode": mode,
-                              "near_phase0_pct": opts["near_phase0_pct"], "max_rank_ms": round(t, 4),
+                              "near_phase0_pct": opts["near_phase0_pct"], "plan_flags": opts.get("plan_flags", 0),
+                              "max_rank_ms": round(t, 4),
                               "allgather_bytes": ag_bytes, "allgather_ms_modeled": round(ag_ms, 4),
                               "modeled_ms": round(t + ag_ms, 4),
                               "modeled_DOF_per_s_with_allgather": op.n / ((t + ag_ms) * 1e-3),

@@ -11,6 +11,7 @@ import argparse
 import ctypes as C
 import dataclasses
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -45,7 +46,14 @@ def main():
     elif a.ablate == "chain":  # bases and transfers only: the bare tree chain
         op = dataclasses.replace(op, near=[], coupling=[])
     opts = json.loads(a.opts)
-    plan = plan_view(op, **opts)
+    split = a.nrhs >= 8 and os.environ.get("H2B_NEAR_SPLIT", "1") != "0"
+    if split:   # trace the dataflow part of the split multi-RHS product
+        os.environ["H2B_TRACE_SPLIT"] = "1"
+        pv = plan_view(op, **dict(opts, plan_flags=opts.get("plan_flags", 0) | 4))
+        plan = pv["phases"][2]
+        plan["stats"] = pv["stats"]
+    else:
+        plan = plan_view(op, **opts)
     dev = DeviceOperator(op, **opts)
     lib = nat.lib()
     lib.h2b_trace_enable.argtypes = [C.c_void_p, C.c_int]
