@@ -165,6 +165,9 @@ typedef struct h2b_options {
    (the near field alone, then the rest), exposed as phases 1 and 2 of a
    single-GPU plan; h2b_create plans it whenever max_nrhs >= 8. */
 #define H2B_PLAN_NEAR_SPLIT 4
+/* plan_flags bits 4-7 (v > 0): leaf coupling rows cut into pieces of at
+   most 1 KB << v (default: task_bytes, the near-field piece size) */
+#define H2B_PLAN_COUPLING_PIECE(v) (((v) & 0xf) << 4)
 
 typedef struct h2b_op h2b_op;      /* device-resident operator             */
 typedef struct h2b_plan h2b_plan;  /* host-only execution plan (no device) */

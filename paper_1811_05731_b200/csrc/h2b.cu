@@ -717,6 +717,38 @@ __device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, d
   const int m = T.m;
   const int mtiles = (m + 15) >> 4;
   const int g = lane >> 2, t = lane & 3;
+  // bias slots (the final items' near-field partials): two slots of every
+  // row this lane holds in flight at once, added in slot order
+  if (T.bias >= 0) {
+    for (int s = 0; s < T.bias_nslots; s += 2) {
+      double2 q[2][MT][2][NT];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 16 * i + g + 8 * h;
+            const bool ok = s + u < T.bias_nslots && i < mtiles && r < m;
+            const double* bp = p.coef + (T.bias + (int64_t)(s + u) * T.bias_stride + r) * NRHS + 2 * t;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+              q[u][i][h][j] = ok ? __ldcg(reinterpret_cast<const double2*>(bp + 8 * j)) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (s + u < T.bias_nslots)
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) {
+                acc[i][j][2 * h] += q[u][i][h][j].x;
+                acc[i][j][2 * h + 1] += q[u][i][h][j].y;
+              }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     if (i >= mtiles) break;
@@ -727,16 +759,6 @@ __device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, d
       double2 v[NT];
 #pragma unroll
       for (int j = 0; j < NT; ++j) v[j] = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
-      if (T.bias >= 0)
-        for (int s = 0; s < T.bias_nslots; ++s) {
-          const double* bp = p.coef + (T.bias + (int64_t)s * T.bias_stride + r) * NRHS + 2 * t;
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const double2 q = __ldcg(reinterpret_cast<const double2*>(bp + 8 * j));
-            v[j].x += q.x;
-            v[j].y += q.y;
-          }
-        }
       double* dst = T.kind == h2b::kFinal ? p.y + __ldg(p.perm + T.out + r) * NRHS : p.coef + (T.out + r) * NRHS;
 #pragma unroll
       for (int j = 0; j < NT; ++j) *reinterpret_cast<double2*>(dst + 8 * j + 2 * t) = v[j];
@@ -1746,6 +1768,7 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     po.world_size = o->world_size > 0 ? o->world_size : 1;
     if (o->plan_flags & H2B_PLAN_SKIP_LEVELS) po.skip_levels = true;
     if (o->plan_flags & H2B_PLAN_NO_SKIP) po.skip_levels = false;
+    if ((o->plan_flags >> 4) & 0xf) po.coupling_task_bytes = (int64_t)1024 << ((o->plan_flags >> 4) & 0xf);
   }
   return po;
 }

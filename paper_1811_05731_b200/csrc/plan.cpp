@@ -239,9 +239,10 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
   // blocks after it are slack and streamed in large pieces.
   const bool bulk = kind == kNear || kind == kDown;
   // (coupling rows of inner clusters sit close to the chain: medium pieces)
+  const int64_t leaf_cp = opt_.coupling_task_bytes > 0 ? opt_.coupling_task_bytes : opt_.task_bytes;
   const int64_t big = kind == kNear ? std::max<int64_t>(opt_.task_bytes, (8 * (int64_t)m_total * C + kMaxNearPieces - 1) /
                                                                              kMaxNearPieces)
-                                    : (qclass == 1 ? std::min<int64_t>(opt_.task_bytes, 16384) : opt_.task_bytes);
+                                    : (qclass == 1 ? std::min<int64_t>(opt_.task_bytes, 16384) : leaf_cp);
   const int64_t cap = bulk ? big : opt_.far_task_bytes;
   const int64_t maxc = allow_split ? std::max<int64_t>(1, cap / (8 * (int64_t)m_total)) : INT64_MAX;
   Piece cur;

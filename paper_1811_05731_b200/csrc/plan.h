@@ -134,6 +134,9 @@ struct PlanOptions {
   // own coupling sum), so the dependency chain through the tree has half the
   // links.  Extra pool bytes: one product per skipped link.
   bool skip_levels = false;
+  // pieces of the leaf clusters' coupling rows (0: task_bytes); a heavy row
+  // cut finer runs on more warps at once instead of forming the tail
+  int64_t coupling_task_bytes = 0;
   int32_t rank = 0;
   int32_t world_size = 1;
 };
