@@ -132,6 +132,7 @@ constexpr int kFlagNoRing = 1 << 24; // multi-RHS: register-staged streaming ins
 constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, acquire fence on completion
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
 constexpr int kFlagMixInner = (int)(1u << 31);  // near-priority warps' mix serves inner coupling rows too
+constexpr int kFlagMrhsRingAll = 2;  // 8/16 RHS: far items through the ring too (TMA sources), not staged whole
 constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
@@ -256,6 +257,26 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 __device__ __forceinline__ void ring_load(const KParams& p, void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   if (p.flags & kFlagStreamEvictFirst) bulk_load_hint(dst, src, bytes, bar, evict_first_policy());
   else bulk_load(dst, src, bytes, bar);
+}
+
+// mbarrier expecting `bytes` from the bulk copies issued next (one arrival).
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
 // xp = x[perm] (h2.py:192-193), node-major with NRHS columns.
@@ -835,18 +856,50 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   const int cs = min(kHalf, STAGE / (8 * m)) & ~3;  // multi-RHS rings: 8 KB stages (4 KB: lean kernel option)
   const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
+  load_segtable(p, T, sin, w, lane);
+  // Sources by TMA too when every segment is one contiguous range: x (a
+  // node range of xp) or a coefficient vector with a single slot (the x^ of
+  // a source cluster): each chunk's sources are bulk-copied into the source
+  // half of its stage with the matrix chunk, no register gathers.
+  const int nseg = T.seg1 - T.seg0;
+  const bool tma_src = __all_sync(0xffffffffu, lane >= nseg || w.seg_kind[lane] == h2b::kSegX ||
+                                                   w.seg_nslots[lane] == 1);
+  int kseg_tma = 0;  // lane 0: segment cursor of the TMA source copies
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
     const double* src = g0 + (int64_t)j * cs * m;
     const int cc = min(cs, T.ncols - j * cs);
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)(src + (int64_t)cc * m) + 15) & ~(uintptr_t)15;
-    ring_load(p, R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+    if (!tma_src) {
+      ring_load(p, R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+      return;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(R.bar(j), (unsigned)(a1 - a0) + (unsigned)(cc * NRHS * 8));
+    if (p.flags & kFlagStreamEvictFirst) bulk_copy_hint(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j),
+                                                        evict_first_policy());
+    else bulk_copy(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
+    double* xs = w.xs + (j & 1) * kHalf * NRHS;
+    const int col = j * cs;
+    int c = col;
+    while (c < col + cc) {
+      while (w.seg_off[kseg_tma + 1] <= c) ++kseg_tma;
+      const int hi = min(col + cc, w.seg_off[kseg_tma + 1]);
+      const int64_t e = (w.seg_src[kseg_tma] + (c - w.seg_off[kseg_tma])) * NRHS;
+      const double* sp = (w.seg_kind[kseg_tma] == h2b::kSegX ? p.xp : p.coef) + e;
+      bulk_copy(xs + (c - col) * NRHS, sp, (unsigned)((hi - c) * NRHS * 8), R.bar(j));
+      c = hi;
+    }
   };
+  if (tma_src && lane == 0) {
+    // the coefficients were written by other warps (generic proxy) and
+    // acquired by this warp: order them before the async-proxy reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
   if (lane == 0) {
     issue(0);
     if (nch > 1) issue(1);
   }
-  load_segtable(p, T, sin, w, lane);
 
   double acc[MT][NT][4];
 #pragma unroll
@@ -858,15 +911,17 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
 
   GatherBatch<NRHS> gb;
   int kseg = 0;
-  gather_issue<NRHS>(p, w, lane, 0, min(cs, T.ncols), gb, kseg);
-  gather_commit<NRHS>(gb, lane, min(cs, T.ncols), w.xs);
-  __syncwarp();
+  if (!tma_src) {
+    gather_issue<NRHS>(p, w, lane, 0, min(cs, T.ncols), gb, kseg);
+    gather_commit<NRHS>(gb, lane, min(cs, T.ncols), w.xs);
+    __syncwarp();
+  }
   for (int jc = 0; jc < nch; ++jc) {
     const int col = jc * cs;
     const int cc = min(cs, T.ncols - col);
     const bool more = jc + 1 < nch;
     const int cc1 = more ? min(cs, T.ncols - col - cs) : 0;
-    if (more) gather_issue<NRHS>(p, w, lane, col + cs, cc1, gb, kseg);
+    if (more && !tma_src) gather_issue<NRHS>(p, w, lane, col + cs, cc1, gb, kseg);
     const int s = jc & 1;
     mbar_wait(R.bar(s), (rpar >> s) & 1u);
     rpar ^= 1u << s;
@@ -885,7 +940,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
       }
       double b[NT];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = xs[(c + t) * NRHS + 8 * j + g];
+      for (int j = 0; j < NT; ++j) b[j] = okc ? xs[(c + t) * NRHS + 8 * j + g] : 0.0;
 #pragma unroll
       for (int i = 0; i < MT; ++i)
         if (i < mtiles)
@@ -894,7 +949,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     }
     __syncwarp();  // every lane is done with stage s and with this source half
     if (lane == 0 && jc + 2 < nch) issue(jc + 2);
-    if (more) {
+    if (more && !tma_src) {
       gather_commit<NRHS>(gb, lane, cc1, w.xs + ((jc + 1) & 1) * kHalf * NRHS);
       __syncwarp();
     }
@@ -1278,7 +1333,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     // shared memory by one TMA bulk copy, overlapping the source gather;
     // near-field items stream from global memory.
     int off = -1;
-    if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0) {
+    if (T.kind != h2b::kNear && T.ld == T.m && T.ncols > 0 &&
+        !(NRHS >= 8 && (p.flags & kFlagMrhsRingAll) && T.m <= 64)) {
       const double* g0 = p.mat + T.data;
       const uintptr_t a0 = (uintptr_t)g0 & ~(uintptr_t)15;
       const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
@@ -1422,26 +1478,6 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       atomicAdd(&ctl->epoch, 1u);
     }
   }
-}
-
-// mbarrier expecting `bytes` from the bulk copies issued next (one arrival).
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
-                                               uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
 }
 
 // Near-field stage of the multi-RHS near kernel: kNearCols columns of the
@@ -2186,6 +2222,10 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   }
   op->sched = sf;
   op->flags = ((sf & H2B_SCHED_NEAR_FIRST) ? 0 : kFlagSlackFirst) | (int)((unsigned)sf & 0xfff3ff04u);
+  {
+    const char* ra = std::getenv("H2B_MRHS_RING_ALL");
+    if (ra && ra[0] == '1') op->flags |= kFlagMrhsRingAll;
+  }
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
     const int sel = (sf >> 18) & 3;
