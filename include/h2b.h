@@ -94,6 +94,10 @@ typedef struct h2b_desc {
    being an acquire (which invalidates the SM's L1) */
 #define H2B_SCHED_RELEASE_ARRIVALS 4
 #define H2B_STREAM_DEFAULT_BYTES (1LL << 30)
+/* Below this many near-field and coupling bytes per rank the plan uses the
+   level-skipping chain by default (plan_flags H2B_PLAN_NO_SKIP: off), and
+   plain scheduling (below H2B_STREAM_DEFAULT_BYTES) gets leaf mix 2. */
+#define H2B_SKIP_DEFAULT_BYTES (4LL << 30)
 /* sched_flags: run the near item a warp claimed ahead before the coupling
    rows of inner clusters (default: inner coupling rows first). */
 #define H2B_SCHED_NEAR_FIRST 1

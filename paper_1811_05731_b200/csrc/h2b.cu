@@ -1785,6 +1785,11 @@ bool streaming_defaults(const h2b_desc* d, const h2b_options* o) {
 
 h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
   h2b::PlanOptions po;
+  // the level-skipping chain where the product is chain-bound: operators
+  // (or rank shards) below 4 GiB of near-field and coupling bytes
+  // (config 1 -6 %, config 2 -3.5 %, config 3 at 8 ranks -7 %; config 3 on
+  // one GPU, near-field bound, +2.7 %: off)
+  po.skip_levels = desc_stream_bytes_per_rank(d, o) < H2B_SKIP_DEFAULT_BYTES;
   // streaming operators: 8 KB chain pieces (a ring warp stages both ring
   // stages at once), halving the latency-bound up-leaf items
   // and 128 KB near-field pieces (a ring warp keeps streaming across the
@@ -2213,6 +2218,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (op->wpc > 8) return fail(H2B_EINVAL, "warps_per_cta must be <= 8");
   const int cps = o ? o->ctas_per_sm : 0;
   int sf = o ? o->sched_flags : 0;
+  if (!(sf & H2B_SCHED_EXPLICIT) && !streaming_defaults(d, o) && ((sf >> 20) & 0xf) == 0)
+    sf |= H2B_SCHED_LEAF_MIX(2);   // plain scheduling: config 2 0.2085 -> 0.2026 ms with the skipping chain
   if (streaming_defaults(d, o)) {
     // streaming defaults (measured on config 3)
     if (((sf >> 4) & 0xf) == 0) sf |= H2B_SCHED_RING_WARPS(8) | H2B_SCHED_RING_STAGE(2);
