@@ -308,7 +308,7 @@ def test_multi_rhs_near_split_bit_identical(name, nrhs, monkeypatch):
     variants = {"fused": {"H2B_NEAR_SPLIT": "0"},
                 "ring8k": {"H2B_NEAR_IMPL": "ring", "H2B_NEAR_STAGE": "8192"},
                 "ring4k": {"H2B_NEAR_IMPL": "ring", "H2B_NEAR_STAGE": "4096"},
-                "tma2": {}, "tma3": {"H2B_NEAR_NST": "3"}, "ringall": {"H2B_MRHS_RING_ALL": "1"}}
+                "tma2": {}, "tma3": {"H2B_NEAR_NST": "3"}, "staged": {"H2B_MRHS_RING_ALL": "0"}}
     for name_v, env in variants.items():
         for k in ("H2B_NEAR_SPLIT", "H2B_NEAR_IMPL", "H2B_NEAR_STAGE", "H2B_NEAR_NST", "H2B_MRHS_RING_ALL"):
             monkeypatch.delenv(k, raising=False)
