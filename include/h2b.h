@@ -172,6 +172,12 @@ typedef struct h2b_options {
 /* plan_flags bits 4-7 (v > 0): leaf coupling rows cut into pieces of at
    most 1 KB << v (default: task_bytes, the near-field piece size) */
 #define H2B_PLAN_COUPLING_PIECE(v) (((v) & 0xf) << 4)
+/* plan_flags bit 8: coupling rows whose inputs are all upward coefficients
+   drop their per-source dependencies and are released together once every
+   upward item has finished (one counter instead of one arrival per edge);
+   bit 9 forces it off */
+#define H2B_PLAN_GATE (1 << 8)
+#define H2B_PLAN_NO_GATE (1 << 9)
 
 typedef struct h2b_op h2b_op;      /* device-resident operator             */
 typedef struct h2b_plan h2b_plan;  /* host-only execution plan (no device) */
@@ -221,6 +227,12 @@ typedef struct h2b_plan_view {
   const int32_t* deps;      /* [ndeps] task indices, all < dependent        */
   const int32_t* t_mlen;    /* [ntasks] fused run length at its first item,
                                0 for the run's other items (1: unfused)     */
+  const int32_t* gated;     /* [ngated] gated coupling rows (H2B_PLAN_GATE):
+                               no dependencies listed, released once all
+                               n_up upward items have finished              */
+  int64_t ngated;
+  int32_t n_gated1;         /* gated[0:n_gated1) are inner clusters' rows   */
+  int32_t n_up;
 } h2b_plan_view;
 
 int h2b_abi_version(void);

@@ -111,8 +111,15 @@ def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray, rng=No
 
     units = [t for t in range(T) if mlen[t] > 0]
     assert sum(int(mlen[t]) for t in units) == T, "fused runs must tile the queue"
+    # gated coupling rows: no listed dependencies, released once every
+    # upward item (kinds 0, 1) of the phase has finished
+    gated = set(int(g) for g in plan.get("gated", []))
+    up_units = [t for t in units if plan["t_kind"][t] <= 1]
+    assert len(up_units) == plan.get("n_up", len(up_units)) or not gated
     if rng is None:
         for t in units:
+            if t in gated:
+                assert all(done[u] for u in up_units), "gated item before the upward pass finished"
             run_unit(t)
         return
     remaining = {t: int(t_dep0[t + 1] - t_dep0[t]) for t in units}
@@ -120,10 +127,17 @@ def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray, rng=No
     for t in units:
         for d in plan["deps"][t_dep0[t]:t_dep0[t + 1]]:
             succ[int(d)].append(t)
-    ready = [t for t in units if remaining[t] == 0]
+    ready = [t for t in units if remaining[t] == 0 and t not in gated]
+    up_left = len(up_units)
+    if up_left == 0:
+        ready.extend(sorted(gated))
     while ready:
         t = ready.pop(int(rng.integers(len(ready))))
         run_unit(t)
+        if plan["t_kind"][t] <= 1:
+            up_left -= 1
+            if up_left == 0:
+                ready.extend(sorted(gated))
         for s2 in succ[t]:
             remaining[s2] -= 1
             if remaining[s2] == 0:

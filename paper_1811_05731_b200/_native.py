@@ -76,6 +76,7 @@ class PlanView(C.Structure):
         ("t_seg0", _p32), ("t_dep0", _p32), ("t_bias_nslots", _p32), ("t_bias_stride", _p32),
         ("s_src", _p64), ("s_ncols", _p32), ("s_kind", _p32), ("s_nslots", _p32),
         ("s_stride", _p32), ("deps", _p32), ("t_mlen", _p32),
+        ("gated", _p32), ("ngated", C.c_int64), ("n_gated1", C.c_int32), ("n_up", C.c_int32),
     ]
 
 

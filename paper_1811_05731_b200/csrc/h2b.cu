@@ -98,6 +98,8 @@ struct Ctl {
   unsigned exited;       // warps that left the scheduler loop
   unsigned epoch;        // launches completed so far
   unsigned pad3[30];
+  Line gate;             // upward items finished (gated coupling rows wait for n_up)
+  Line g_head[2];        // gated lists: next item to claim (inner rows, leaf rows)
 };
 
 struct KParams {
@@ -124,6 +126,8 @@ struct KParams {
   int32_t ring_warps;                   // NRHS < 8: warps per CTA (the top ones) with a TMA ring
   int32_t ring_stage;                   // NRHS < 8: ring stage payload bytes (8192, 6144, 4096)
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
+  const int32_t* __restrict__ gated;    // gated coupling rows (Phase::gated)
+  int32_t ngated, ngated1, nup_gate;
 };
 
 // scheduling switches
@@ -1158,13 +1162,16 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   //  2. a static item (up-leaf first, then the near field).
   Ctl* ctl = p.ctl;
   const unsigned e1 = ld_relaxed(&ctl->epoch) + 1u;
-  const unsigned n_dynamic = (unsigned)(p.nnodes - p.nready0);
+  const unsigned n_dynamic = (unsigned)(p.nnodes - p.nready0 - p.ngated);
   // lane-0 state below.  The initially-ready items are two static lists
   // claimed through separate heads: up-leaf items ready0[0, nready0_hi) and
   // the near field ready0[nready0_hi, nready0).
   const unsigned n_up = (unsigned)p.nready0_hi, n_near = (unsigned)(p.nready0 - p.nready0_hi);
   bool up_done = n_up == 0;
   bool near_done = n_near == 0;
+  // gated coupling rows: claimable once all nup_gate upward items are done
+  bool gate_open = p.nup_gate == 0;
+  bool g_done1 = p.ngated1 == 0, g_done2 = p.ngated == p.ngated1;
   int owed = -1;             // claimed dynamic slot whose push is still in flight
   int pend = -1;             // near item claimed ahead (slack work, no priority cost)
   int cont = -1;             // continuation (all lanes)
@@ -1220,6 +1227,20 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         }
         return __ldg(p.ready0 + s);
       };
+      auto take_g = [&](int q) -> int {  // gated list q (1: inner rows, 2: leaf rows)
+        if (q == 1 ? g_done1 : g_done2) return -1;
+        if (!gate_open) {
+          if (ld_acquire(&ctl->gate.v) < (unsigned)p.nup_gate) return -1;
+          gate_open = true;
+        }
+        const unsigned n = q == 1 ? (unsigned)p.ngated1 : (unsigned)(p.ngated - p.ngated1);
+        const unsigned s = atomicAdd(&ctl->g_head[q - 1].v, 1u);
+        if (s >= n) {
+          (q == 1 ? g_done1 : g_done2) = true;
+          return -1;
+        }
+        return __ldg(p.gated + (q == 1 ? 0 : p.ngated1) + s);
+      };
       auto take_near = [&]() -> int {
         const unsigned s = atomicAdd(&ctl->near_head, 1u);
         if (s >= n_near) {
@@ -1253,12 +1274,13 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
           // coupling rows wait for the other warps and trail the near field
           // (with kFlagMixInner the coupling rows of inner clusters first:
           // they gate the downward chain)
-          if (leaf_mix && near_run >= leaf_thr && owed < 0 && (p.flags & kFlagMixInner) && h[1] < t[1] &&
-              (item = claim(1)) >= 0) {
+          if (leaf_mix && near_run >= leaf_thr && owed < 0 && (p.flags & kFlagMixInner) &&
+              ((h[1] < t[1] && (item = claim(1)) >= 0) || (item = take_g(1)) >= 0)) {
             near_run = 0;
             break;
           }
-          if (leaf_mix && near_run >= leaf_thr && owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) {
+          if (leaf_mix && near_run >= leaf_thr && owed < 0 &&
+              ((h[2] < t[2] && (item = claim(2)) >= 0) || (item = take_g(2)) >= 0)) {
             near_run = 0;
             break;
           }
@@ -1276,8 +1298,10 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         // class-0 static items (up-leaf) before any slack work
         if (!up_done && near_ok && (item = take_up()) >= 0) break;
         // coupling rows of inner clusters feed the downward chain level by level
-        if ((p.flags & kFlagSlackFirst) && owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
-        if (leaf_mix && near_run >= leaf_thr && owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) {
+        if ((p.flags & kFlagSlackFirst) && owed < 0 &&
+            ((h[1] < t[1] && (item = claim(1)) >= 0) || (item = take_g(1)) >= 0)) break;
+        if (leaf_mix && near_run >= leaf_thr && owed < 0 &&
+            ((h[2] < t[2] && (item = claim(2)) >= 0) || (item = take_g(2)) >= 0)) {
           near_run = 0;
           break;
         }
@@ -1291,14 +1315,16 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
         }
         // coupling rows of inner clusters: the chain needs them level by level
         if (owed < 0 && h[1] < t[1] && (item = claim(1)) >= 0) break;
+        if ((item = take_g(1)) >= 0) break;
         if (owed < 0 && h[2] < t[2] && (item = claim(2)) >= 0) break;
+        if ((item = take_g(2)) >= 0) break;
         if (!near_done && near_ok && (item = take_near()) >= 0) {
           ++near_run;
           break;
         }
         // every dynamic item has started (continuations skip the queues, so
         // an over-claimed slot may never be pushed): nothing more will come
-        if (ld_relaxed(&ctl->dyn_started) >= n_dynamic) {
+        if (ld_relaxed(&ctl->dyn_started) >= n_dynamic && g_done1 && g_done2) {
           owed = -1;
           break;
         }
@@ -1370,6 +1396,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     // successor.  Of the successors whose count this warp completes, it runs
     // the first one itself next and pushes the others.
     __syncwarp();
+    if (p.ngated > 0 && T.kind <= h2b::kUpNode && lane == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->gate.v) : "memory");
     unsigned long long t_run = 0;
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_run));
     cont = -1;
@@ -1474,6 +1502,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
       ctl->near_head = 0;
       ctl->dyn_started = 0;
       ctl->exited = 0;
+      ctl->gate.v = 0;
+      ctl->g_head[0].v = ctl->g_head[1].v = 0;
       fence_acq_rel();
       atomicAdd(&ctl->epoch, 1u);
     }
@@ -1687,6 +1717,8 @@ struct PhaseDev {
   int32_t* d_ready0 = nullptr;
   int32_t nready0 = 0;
   int32_t nready0_hi = 0;
+  int32_t* d_gated = nullptr;
+  int32_t ngated = 0, ngated1 = 0, nup = 0;
   unsigned long long* d_arrived = nullptr;
   int32_t* d_ready_q = nullptr;
   unsigned* d_ready_flag = nullptr;
@@ -1810,6 +1842,8 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     if (o->plan_flags & H2B_PLAN_SKIP_LEVELS) po.skip_levels = true;
     if (o->plan_flags & H2B_PLAN_NO_SKIP) po.skip_levels = false;
     if ((o->plan_flags >> 4) & 0xf) po.coupling_task_bytes = (int64_t)1024 << ((o->plan_flags >> 4) & 0xf);
+    if (o->plan_flags & H2B_PLAN_GATE) po.gate_coupling = true;
+    if (o->plan_flags & H2B_PLAN_NO_GATE) po.gate_coupling = false;
   }
   return po;
 }
@@ -1871,6 +1905,10 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, const double* x, double* y, 
   p.ready0 = F.d_ready0;
   p.nready0 = F.nready0;
   p.nready0_hi = F.nready0_hi;
+  p.gated = F.d_gated;
+  p.ngated = F.ngated;
+  p.ngated1 = F.ngated1;
+  p.nup_gate = F.nup;
   p.arrived = F.d_arrived;
   p.ready_q = F.d_ready_q;
   p.ready_flag = F.d_ready_flag;
@@ -2023,6 +2061,7 @@ void free_phase(PhaseDev& F) {
   cudaFree(F.d_succ0);
   cudaFree(F.d_succ);
   cudaFree(F.d_ready0);
+  cudaFree(F.d_gated);
   cudaFree(F.d_arrived);
   cudaFree(F.d_ready_q);
   cudaFree(F.d_ready_flag);
@@ -2100,6 +2139,10 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   if ((rc = upload(&F->d_ready0, P.ready0.data(), P.ready0.size()))) return rc;
   F->nready0 = (int32_t)P.ready0.size();
   F->nready0_hi = P.n_ready0_hi;
+  if ((rc = upload(&F->d_gated, P.gated.data(), P.gated.size()))) return rc;
+  F->ngated = (int32_t)P.gated.size();
+  F->ngated1 = P.n_gated1;
+  F->nup = P.n_up;
   const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
   if ((rc = upload<unsigned long long>(&F->d_arrived, nullptr, T1))) return rc;
   if ((rc = upload<int32_t>(&F->d_ready_q, nullptr, kQueues * T1))) return rc;
@@ -2394,6 +2437,10 @@ void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
   v->t_seg0 = F.t_seg0.data();
   v->t_dep0 = F.t_dep0.data();
   v->t_mlen = F.t_mlen.data();
+  v->gated = F.gated.data();
+  v->ngated = (int64_t)F.gated.size();
+  v->n_gated1 = F.n_gated1;
+  v->n_up = F.n_up;
   v->t_bias_nslots = F.t_bias_nslots.data();
   v->t_bias_stride = F.t_bias_stride.data();
   v->s_src = F.s_src.data();

@@ -818,6 +818,44 @@ int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char
       F->tasks_by_kind[t.kind] += 1;
     }
   }
+  // gated coupling rows: their dependencies (all upward items) are dropped;
+  // the kernel releases them once every upward item of the phase is done
+  std::vector<char> gated(T, 0);
+  if (opt_.gate_coupling) {
+    bool any = false;
+    for (int32_t k = 0; k < T; ++k) {
+      if (F->t_kind[k] != kDown || F->t_qclass[k] == 0 || F->t_mlen[k] == 0) continue;
+      const int32_t e0 = F->t_dep0[k], e1 = F->t_dep0[k + 1];
+      if (e1 == e0) continue;
+      bool up_only = true;
+      for (int32_t e = e0; e < e1 && up_only; ++e) up_only = F->t_kind[F->deps[e]] <= kUpNode;
+      if (up_only) { gated[k] = 1; any = true; }
+    }
+    if (any) {
+      std::vector<int32_t> nd;
+      nd.reserve(F->deps.size());
+      std::vector<int32_t> d0(T + 1, 0);
+      for (int32_t k = 0; k < T; ++k) {
+        if (!gated[k])
+          for (int32_t e = F->t_dep0[k]; e < F->t_dep0[k + 1]; ++e) nd.push_back(F->deps[e]);
+        d0[k + 1] = (int32_t)nd.size();
+      }
+      F->deps.swap(nd);
+      F->t_dep0.swap(d0);
+    }
+    std::vector<int32_t> g2;
+    for (int32_t k = 0; k < T; ++k) {
+      if (!gated[k]) continue;
+      if (F->t_qclass[k] == 1) F->gated.push_back(k);
+      else g2.push_back(k);
+    }
+    F->n_gated1 = (int32_t)F->gated.size();
+    std::stable_sort(g2.begin(), g2.end(), [&](int32_t a, int32_t b) {
+      return (int64_t)F->t_m[a] * F->t_ncols[a] > (int64_t)F->t_m[b] * F->t_ncols[b];
+    });
+    F->gated.insert(F->gated.end(), g2.begin(), g2.end());
+    for (int32_t k = 0; k < T; ++k) F->n_up += (F->t_kind[k] <= kUpNode && F->t_mlen[k] > 0);
+  }
   // successor lists for the completion-driven scheduler
   F->succ0.assign(T + 1, 0);
   for (int32_t dp : F->deps) F->succ0[dp + 1] += 1;
@@ -832,12 +870,13 @@ int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char
   // chain), then the rest (the near field) longest first, so that heavy rows
   // start early and the end of the launch is made of short items
   for (int32_t k = 0; k < T; ++k)
-    if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] == 0) F->ready0.push_back(k);
+    if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] == 0 && !gated[k])
+      F->ready0.push_back(k);
   F->n_ready0_hi = (int32_t)F->ready0.size();
   {
     std::vector<int32_t> rest;
     for (int32_t k = 0; k < T; ++k)
-      if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] != 0) rest.push_back(k);
+      if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] != 0 && !gated[k]) rest.push_back(k);
     std::stable_sort(rest.begin(), rest.end(), [&](int32_t a, int32_t b) {
       return (int64_t)F->t_m[a] * F->t_ncols[a] > (int64_t)F->t_m[b] * F->t_ncols[b];
     });

@@ -63,6 +63,13 @@ struct Phase {
   std::vector<int32_t> succ0, succ;
   std::vector<int32_t> ready0;
   int32_t n_ready0_hi = 0;          // ready0[0:n_ready0_hi) are class 0
+  // Gated coupling rows (PlanOptions::gate_coupling): down items whose only
+  // inputs are upward coefficients carry no dependencies; they are claimed
+  // from these lists (inner clusters' rows first, then the leaves' rows,
+  // longest first) once all `n_up` upward items of the phase have finished.
+  std::vector<int32_t> gated;
+  int32_t n_gated1 = 0;             // gated[0:n_gated1) are class 1
+  int32_t n_up = 0;
   int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
 
   int64_t ntasks() const { return (int64_t)t_m.size(); }
@@ -137,6 +144,9 @@ struct PlanOptions {
   // pieces of the leaf clusters' coupling rows (0: task_bytes); a heavy row
   // cut finer runs on more warps at once instead of forming the tail
   int64_t coupling_task_bytes = 0;
+  // release coupling rows behind one counter of finished upward items
+  // instead of one arrival per (source, row) edge
+  bool gate_coupling = false;
   int32_t rank = 0;
   int32_t world_size = 1;
 };

@@ -209,6 +209,8 @@ def SCHED_NEAR_PRIO(k: int) -> int:
 PLAN_SKIP_LEVELS = 1
 PLAN_NO_SKIP = 2
 PLAN_NEAR_SPLIT = 4
+PLAN_GATE = 1 << 8
+PLAN_NO_GATE = 1 << 9
 
 
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
@@ -254,6 +256,7 @@ def _grab_view(v) -> dict:
         "s_kind": grab(v.s_kind, S, np.int32), "s_nslots": grab(v.s_nslots, S, np.int32),
         "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
         "t_mlen": grab(v.t_mlen, T, np.int32),
+        "gated": grab(v.gated, int(v.ngated), np.int32), "n_gated1": int(v.n_gated1), "n_up": int(v.n_up),
     }
 
 

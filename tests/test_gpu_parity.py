@@ -326,14 +326,18 @@ def test_multi_rhs_near_split_bit_identical(name, nrhs, monkeypatch):
 
 
 @pytest.mark.parametrize("nrhs", [1, 16])
-def test_level_skipping_chain_on_gpu(golden, nrhs):
-    """The level-skipping far-field chain (H2B_PLAN_SKIP_LEVELS) on the GPU:
-    the same product to rounding (1e-12), the far field checked on its own."""
+@pytest.mark.parametrize("flags", ["skip", "gate", "skip+gate", "none"])
+def test_level_skipping_chain_on_gpu(golden, nrhs, flags):
+    """The level-skipping far-field chain (H2B_PLAN_SKIP_LEVELS) and the gated
+    coupling rows (H2B_PLAN_GATE) on the GPU, alone and together: the same
+    product to rounding (1e-12), the far field checked on its own."""
     name, op, ex = golden
     h2 = _gpu()
+    pf = {"skip": h2.PLAN_SKIP_LEVELS, "gate": h2.PLAN_GATE | h2.PLAN_NO_SKIP,
+          "skip+gate": h2.PLAN_SKIP_LEVELS | h2.PLAN_GATE, "none": h2.PLAN_NO_SKIP | h2.PLAN_NO_GATE}[flags]
     X = np.random.default_rng(23).standard_normal((op.n, nrhs))
     for o in (op, dataclasses.replace(op, near=[])):
-        dev = h2.DeviceOperator(o, plan_flags=h2.PLAN_SKIP_LEVELS)
+        dev = h2.DeviceOperator(o, plan_flags=pf)
         try:
             Y = dev.matvec(X[:, 0] if nrhs == 1 else X).reshape(op.n, nrhs)
             Y2 = dev.matvec(X[:, 0] if nrhs == 1 else X).reshape(op.n, nrhs)

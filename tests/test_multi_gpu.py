@@ -136,7 +136,7 @@ STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20), f
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("opts", [{}, STREAMING])
+@pytest.mark.parametrize("opts", [{}, STREAMING, dict(plan_flags=1 << 8), dict(STREAMING, plan_flags=(1 << 8) | 1)])
 @pytest.mark.parametrize("world", [2, 4])
 def test_virtual_ranks_on_one_gpu(world, opts):
     torch = pytest.importorskip("torch")

@@ -170,3 +170,32 @@ def chain_length(plan):
         d = plan["deps"][plan["t_dep0"][t]:plan["t_dep0"][t + 1]]
         depth[t] = 1 + (depth[d].max() if d.size else 0)
     return int(depth.max())
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_gated_coupling_rows(golden, world):
+    """H2B_PLAN_GATE: coupling rows fed only by upward coefficients lose their
+    per-source dependencies and wait for the whole upward pass instead; the
+    interpreter releases them exactly so (random dependency orders too)."""
+    from oracle.flat_matvec import run_ranks
+    from paper_1811_05731_b200.h2 import PLAN_GATE, plan_view
+    name, op, ex = golden
+    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_GATE) for r in range(world)]
+    for i in (0, 2):
+        y = run_ranks(plans, ex["X"][:, i]) if world > 1 else run_plan(plans[0], ex["X"][:, i])
+        assert rel(y, ex["y_full"][:, i]) <= 1e-13, (name, world, i)
+    if world == 1:
+        p0 = plans[0]
+        base = plan_view(op, plan_flags=0x200)   # no gate
+        if len(op.coupling):
+            assert p0["gated"].size > 0 and p0["ndeps"] < base["ndeps"] if "ndeps" in p0 else p0["gated"].size > 0
+        assert np.all(p0["t_kind"][p0["gated"]] == 2)
+        for g in p0["gated"]:
+            assert p0["t_dep0"][g] == p0["t_dep0"][g + 1]
+        rng = np.random.default_rng(5)
+        for _ in range(2):
+            coef = np.full((max(1, p0["coef_len"]), 1), np.nan)
+            Y = np.full((op.n, 1), np.nan)
+            from oracle.flat_matvec import run_phase
+            run_phase(p0, ex["X"][:, 0], coef, Y, rng=rng)
+            assert rel(Y[:, 0], ex["y_full"][:, 0]) <= 1e-13
