@@ -122,14 +122,14 @@ def test_ring_warps_bit_identical(name):
 
 def test_effective_sched_flags_reported():
     """Small operators keep plain scheduling (the streaming defaults start
-    at H2B_STREAM_DEFAULT_BYTES per rank); explicit flags are used as given
-    and reported back through h2b_stats."""
+    at H2B_STREAM_DEFAULT_BYTES per rank) with leaf mix 2; explicit flags are
+    used as given and reported back through h2b_stats."""
     op, ex = load_golden("config1_sphere4")
     h2 = _gpu()
     dev = h2.DeviceOperator(op)
     try:
         st = dev.stats()
-        assert st["sched_flags"] == 0 and st["ring_warps"] == 0
+        assert st["sched_flags"] == h2.SCHED_LEAF_MIX(2) and st["ring_warps"] == 0
     finally:
         dev.close()
     flags = h2.SCHED_EXPLICIT | h2.SCHED_RING_WARPS(8) | (2 << 18) | h2.SCHED_NEAR_PRIO(6) | h2.SCHED_LEAF_MIX(2)
