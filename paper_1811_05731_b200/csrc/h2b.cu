@@ -137,6 +137,7 @@ constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, a
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
 constexpr int kFlagMixInner = (int)(1u << 31);  // near-priority warps' mix serves inner coupling rows too
 constexpr int kFlagMrhsRingAll = 2;  // 8/16 RHS: far items through the ring too (TMA sources), not staged whole
+constexpr int kFlagUpMix = 1 << 3;   // near-priority warps' mix takes up-leaf items first (H2B_UP_MIX=1)
 constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
 constexpr int kInlineSegs = 4;     // segments stored per item next to the task
@@ -1274,6 +1275,13 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
           // coupling rows wait for the other warps and trail the near field
           // (with kFlagMixInner the coupling rows of inner clusters first:
           // they gate the downward chain)
+          // (with kFlagUpMix the up-leaf items first: the upward pass gates
+          // every coupling row, and on large operators the few other warps
+          // drain it slowly)
+          if (leaf_mix && near_run >= leaf_thr && (p.flags & kFlagUpMix) && !up_done && (item = take_up()) >= 0) {
+            near_run = 0;
+            break;
+          }
           if (leaf_mix && near_run >= leaf_thr && owed < 0 && (p.flags & kFlagMixInner) &&
               ((h[1] < t[1] && (item = claim(1)) >= 0) || (item = take_g(1)) >= 0)) {
             near_run = 0;
@@ -2277,6 +2285,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     // TMA where contiguous (config 3, 16 RHS: 5.09 -> 4.52 ms; 8 RHS 3.63 -> 3.51)
     const char* ra = std::getenv("H2B_MRHS_RING_ALL");
     if (!(ra && ra[0] == '0')) op->flags |= kFlagMrhsRingAll;
+    const char* um = std::getenv("H2B_UP_MIX");
+    if (um && um[0] == '1') op->flags |= kFlagUpMix;
   }
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
