@@ -140,7 +140,9 @@ def main():
                for b0, b1 in zip(bins, bins[1:])]
         print(f"  MB/5% {name:10s}", " ".join(f"{r:6.0f}" for r in row))
     if a.save:
-        np.savez_compressed(a.save, start=start, end=end, kind=kind, tr=tr)
+        np.savez_compressed(a.save, start=start, end=end, kind=kind, tr=tr, t_m=plan["t_m"],
+                            t_ncols=plan["t_ncols"], dep0=dep0, deps=deps, t_out=plan["t_out"],
+                            t_bias=plan["t_bias"], t_bias_nslots=plan["t_bias_nslots"])
 
 
 if __name__ == "__main__":
