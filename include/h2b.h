@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define H2B_ABI_VERSION 3
+#define H2B_ABI_VERSION 4
 
 #define H2B_OK 0
 #define H2B_EINVAL (-1)
@@ -178,6 +178,19 @@ typedef struct h2b_options {
    bit 9 forces it off */
 #define H2B_PLAN_GATE (1 << 8)
 #define H2B_PLAN_NO_GATE (1 << 9)
+/* plan_flags bit 10: the staged product.  The clusters of at
+   most H2B_PLAN_SWEEP_NODES nodes root "bottom subtrees"; their upward items
+   run first in a sweep kernel (one CTA per subtree, block barriers between
+   tree levels, no arrival counters), one dataflow launch then runs the near
+   field, every coupling row and the short far-field chain of the clusters
+   above the subtrees, and a second sweep runs the subtrees' downward
+   transfers and the finals.  Bit 11 forces it off. */
+#define H2B_PLAN_STAGED (1 << 10)
+#define H2B_PLAN_NO_STAGED (1 << 11)
+/* plan_flags bits 12-15 (v > 0): bottom subtrees hold at most 64 << v nodes
+   (default 1024; multi-GPU plans shrink it until there are 8 subtrees per
+   rank, since ranks own whole subtrees) */
+#define H2B_PLAN_SWEEP_NODES(v) (((v) & 0xf) << 12)
 
 typedef struct h2b_op h2b_op;      /* device-resident operator             */
 typedef struct h2b_plan h2b_plan;  /* host-only execution plan (no device) */
@@ -233,6 +246,17 @@ typedef struct h2b_plan_view {
   int64_t ngated;
   int32_t n_gated1;         /* gated[0:n_gated1) are inner clusters' rows   */
   int32_t n_up;
+  /* the launch this phase is: mode 0 dataflow kernel, 1 sweep (units of
+     items run wave by wave by one CTA, a block barrier between waves), 2
+     near-field items only; group 0 before the x^ exchange of a multi-GPU
+     product, 1 after it */
+  int32_t mode, group;
+  int32_t split;            /* 1: a launch of the split multi-RHS product
+                               (H2B_PLAN_NEAR_SPLIT), 0: of the plain one    */
+  int32_t reserved_;
+  int64_t nunits, nwaves;
+  const int32_t* unit0;     /* [nunits+1] sweeps: unit u = waves [unit0[u], unit0[u+1]) */
+  const int32_t* wave0;     /* [nwaves+1] sweeps: wave w = items [wave0[w], wave0[w+1]) */
 } h2b_plan_view;
 
 int h2b_abi_version(void);
@@ -242,8 +266,11 @@ const char* h2b_last_error(void);
 int h2b_plan_create(const h2b_desc* d, const h2b_options* opt, h2b_plan** out);
 int h2b_plan_view_get(const h2b_plan* p, h2b_plan_view* out);
 int h2b_plan_stats(const h2b_plan* p, h2b_stats* out);
-/* Multi-GPU plans have two phases; single-GPU plans one
-   (three with H2B_PLAN_NEAR_SPLIT: the whole product, the near field, the rest). */
+/* The launches of the product in order (h2b_plan_view.mode / group): one
+   dataflow launch for a single-GPU plan, two (group 0, group 1) for a
+   multi-GPU rank plan; staged plans add an upward sweep before
+   and a downward sweep after.  With H2B_PLAN_NEAR_SPLIT the
+   launches of the split multi-RHS product follow those of the plain one. */
 int h2b_plan_phases(const h2b_plan* p);
 int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* out);
 /* rank_lo_hi[2*world]: tree-position range of each rank's leaves;
@@ -272,7 +299,8 @@ int h2b_reset(h2b_op* op);
 /* Synchronous host convenience (the drop-in path): copies x in, y out.
  * Multi-GPU rank operators return the full y on every rank. */
 int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int nrhs);
-/* One phase of a (multi-GPU) product and the exchange region between them
+/* One phase of a (multi-GPU) product -- 0: every launch before the x^
+ * exchange, 1: every launch after it -- and the exchange region between them
  * (for drivers that move the x^ regions themselves instead of NCCL). */
 int h2b_matvec_phase(h2b_op* op, int phase, const double* x_dev, double* y_dev, int nrhs, void* stream);
 int h2b_exchange_region(h2b_op* op, int nrhs, double** base, int64_t* count_per_rank);

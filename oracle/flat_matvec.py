@@ -15,16 +15,31 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["run_plan", "run_phase", "run_ranks", "check_plan_invariants"]
+__all__ = ["run_plan", "run_phase", "run_group", "run_ranks", "check_plan_invariants", "launches"]
 
 
-def run_plan(plan: dict, x: np.ndarray, rng=None) -> np.ndarray:
-    """Single-phase plan: y = M x (``rng``: random dependency-respecting order)."""
+def launches(plan: dict, group=None, split: bool = False) -> list:
+    """The launches of a plan in order (``h2b_plan_view.mode/group/split``):
+    those of the plain product, or of the split multi-RHS product."""
+    return [ph for ph in plan.get("phases", [plan])
+            if bool(ph.get("split", 0)) == split and (group is None or ph.get("group", 0) == group)]
+
+
+def run_group(plan: dict, group, x, coef, Y, rng=None, split: bool = False) -> None:
+    """Every launch of one group (0: before the x^ exchange, 1: after), in order."""
+    for ph in launches(plan, group, split):
+        run_phase(ph, x, coef, Y, rng=rng)
+
+
+def run_plan(plan: dict, x: np.ndarray, rng=None, split: bool = False) -> np.ndarray:
+    """Single-GPU plan: y = M x, launch after launch (``rng``: random
+    dependency-respecting order inside every launch; ``split``: the launches
+    of the split multi-RHS product)."""
     x = np.asarray(x, dtype=np.float64)
     nrhs = 1 if x.ndim == 1 else x.shape[1]
     coef = np.full((max(1, plan["coef_len"]), nrhs), np.nan)
     Y = np.full((plan["n"], nrhs), np.nan)
-    run_phase(plan, x, coef, Y, rng=rng)
+    run_group(plan, None, x, coef, Y, rng=rng, split=split)
     return Y[:, 0].copy() if x.ndim == 1 else Y
 
 
@@ -38,14 +53,14 @@ def run_ranks(rank_plans: list, x: np.ndarray) -> np.ndarray:
     coefs = [np.full((max(1, p["coef_len"]), nrhs), np.nan) for p in rank_plans]
     ys = [np.full((p["n"], nrhs), np.nan) for p in rank_plans]
     for r, p in enumerate(rank_plans):
-        run_phase(p["phases"][0], x, coefs[r], ys[r])
+        run_group(p, 0, x, coefs[r], ys[r])
     off, cnt = rank_plans[0]["exchange"]
     for r in range(W):
         region = coefs[r][off + r * cnt: off + (r + 1) * cnt].copy()
         for q in range(W):
             coefs[q][off + r * cnt: off + (r + 1) * cnt] = region
     for r, p in enumerate(rank_plans):
-        run_phase(p["phases"][1], x, coefs[r], ys[r])
+        run_group(p, 1, x, coefs[r], ys[r])
     Y = np.full_like(ys[0], np.nan)
     for r, p in enumerate(rank_plans):
         lo, hi = p["rank_lo_hi"][r]
@@ -111,6 +126,10 @@ def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray, rng=No
 
     units = [t for t in range(T) if mlen[t] > 0]
     assert sum(int(mlen[t]) for t in units) == T, "fused runs must tile the queue"
+    if plan.get("mode", 0) == 1:
+        _run_sweep(plan, units, mlen, execute, coef, rng)
+        assert all(done)
+        return
     # gated coupling rows: no listed dependencies, released once every
     # upward item (kinds 0, 1) of the phase has finished
     gated = set(int(g) for g in plan.get("gated", []))
@@ -145,19 +164,56 @@ def run_phase(plan: dict, x: np.ndarray, coef: np.ndarray, Y: np.ndarray, rng=No
     assert all(done), "some units never became ready"
 
 
+def _run_sweep(plan, units, mlen, execute, coef, rng) -> None:
+    """A sweep launch (csrc/h2b.cu h2b_sweep_kernel): every unit is run by
+    one CTA, wave after wave with a block barrier between waves; the items
+    of a wave run concurrently on the CTA's warps, so none may read what
+    another of the same wave writes -- each wave is executed against a
+    snapshot of the workspace taken at its start (and in a random order
+    with ``rng``); units run in any order."""
+    unit0, wave0 = plan["unit0"], plan["wave0"]
+    assert len(unit0) - 1 == len(units) and wave0[-1] == len(plan["t_m"]) and len(plan["deps"]) == 0
+    order = list(range(len(units)))
+    if rng is not None:
+        rng.shuffle(order)
+    for u in order:
+        assert wave0[unit0[u]] == units[u] and wave0[unit0[u + 1]] == units[u] + int(mlen[units[u]])
+        for w in range(unit0[u], unit0[u + 1]):
+            items = list(range(wave0[w], wave0[w + 1]))
+            assert items, "empty wave"
+            if rng is not None:
+                rng.shuffle(items)
+            before = coef.copy()
+            written = np.zeros(coef.shape[0], bool)
+            for t in items:
+                # inputs as they were when the wave started
+                mine = coef.copy()
+                coef[:] = before
+                execute(t)
+                o, m = int(plan["t_out"][t]), int(plan["t_m"][t])
+                if plan["t_kind"][t] != 4:
+                    mine[o:o + m] = coef[o:o + m]
+                    assert not written[o:o + m].any(), "two items of a wave write one slot"
+                    written[o:o + m] = True
+                coef[:] = mine
+
+
 def check_plan_invariants(plan: dict) -> None:
-    """Structural invariants the kernel relies on."""
-    T = len(plan["t_m"])
-    assert np.all(plan["t_m"] >= 1) and np.all(plan["t_m"] <= 64)
-    assert np.all(plan["t_ld"] >= plan["t_m"])
-    for t in range(T):
-        d = plan["deps"][plan["t_dep0"][t]:plan["t_dep0"][t + 1]]
-        assert np.all(d < t)
-        seg = slice(plan["t_seg0"][t], plan["t_seg0"][t + 1])
-        assert plan["s_ncols"][seg].sum() == plan["t_ncols"][t]
+    """Structural invariants the kernels rely on (every launch of the plain
+    product of a single-GPU plan)."""
+    rows = []
+    for ph in launches(plan):
+        T = len(ph["t_m"])
+        assert np.all(ph["t_m"] >= 1) and np.all(ph["t_m"] <= 64)
+        assert np.all(ph["t_ld"] >= ph["t_m"])
+        for t in range(T):
+            d = ph["deps"][ph["t_dep0"][t]:ph["t_dep0"][t + 1]]
+            assert np.all(d < t)
+            seg = slice(ph["t_seg0"][t], ph["t_seg0"][t + 1])
+            assert ph["s_ncols"][seg].sum() == ph["t_ncols"][t]
+        fin = np.flatnonzero(ph["t_kind"] == 4)
+        rows += [ph["t_out"][t] + np.arange(ph["t_m"][t]) for t in fin]
     assert plan["mat"].size * 8 == sum(plan["stats"]["bytes_by_kind"].values())
     assert plan["mat"].size * 8 <= plan["stats"]["stream_bytes"] + plan["stats"]["extra_bytes"]
     # every y row written exactly once
-    fin = np.flatnonzero(plan["t_kind"] == 4)
-    rows = np.concatenate([plan["t_out"][t] + np.arange(plan["t_m"][t]) for t in fin])
-    assert np.array_equal(np.sort(rows), np.arange(plan["n"]))
+    assert np.array_equal(np.sort(np.concatenate(rows)), np.arange(plan["n"]))

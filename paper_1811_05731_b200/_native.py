@@ -19,7 +19,7 @@ __all__ = ["lib", "Desc", "Options", "Stats", "PlanView", "check", "LIB_PATH",
 # H2B_LIB: an alternative build of the library (A/B timing of kernel variants)
 LIB_PATH = Path(os.environ.get("H2B_LIB") or Path(__file__).resolve().parent / "libh2b.so")
 
-ABI_VERSION = 3  # include/h2b.h H2B_ABI_VERSION
+ABI_VERSION = 4  # include/h2b.h H2B_ABI_VERSION
 H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENCCL, H2B_ENOMEM, H2B_ENODEV, H2B_EIO, H2B_ECONV = 0, -1, -2, -3, -4, -5, -6, -7
 KIND_NAMES = ("up_leaf", "up_node", "down", "near", "final")
 
@@ -77,6 +77,8 @@ class PlanView(C.Structure):
         ("s_src", _p64), ("s_ncols", _p32), ("s_kind", _p32), ("s_nslots", _p32),
         ("s_stride", _p32), ("deps", _p32), ("t_mlen", _p32),
         ("gated", _p32), ("ngated", C.c_int64), ("n_gated1", C.c_int32), ("n_up", C.c_int32),
+        ("mode", C.c_int32), ("group", C.c_int32), ("split", C.c_int32), ("reserved_", C.c_int32), ("nunits", C.c_int64), ("nwaves", C.c_int64),
+        ("unit0", _p32), ("wave0", _p32),
     ]
 
 

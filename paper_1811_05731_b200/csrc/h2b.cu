@@ -128,6 +128,10 @@ struct KParams {
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
   const int32_t* __restrict__ gated;    // gated coupling rows (Phase::gated)
   int32_t ngated, ngated1, nup_gate;
+  // sweeps (Phase::mode 1): units of waves of items
+  const int32_t* __restrict__ unit0;
+  const int32_t* __restrict__ wave0;
+  int32_t nunits;
 };
 
 // scheduling switches
@@ -149,6 +153,7 @@ constexpr int kStageBytes = 4096 + 128;  // TMA staging of one far-field item (+
 struct __align__(128) WarpSmem {
   double xs[kChunkBytes / 8];
   unsigned long long bar;
+  unsigned long long dbg[3];  // diagnostics (tracing): segment table, gather, multiply done
   double red[32];
   long long seg_src[h2b::kMaxSegs];
   int seg_off[h2b::kMaxSegs + 1];
@@ -537,6 +542,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
   const int m = T.m, ld = T.ld;
 
   load_segtable(p, T, sin, w, lane);
+  if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w.dbg[0])::"memory");
 
   const bool grouped = (NRHS == 1) && (m <= 16) && (ld == m) && (m > 0);
   double acc0[NRHS], acc1[NRHS];
@@ -552,6 +558,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
       const int cc = min(kCols, T.ncols - col);
       gather_chunk<NRHS>(p, w, lane, col, cc);
       __syncwarp();
+      if (p.trace && col == 0 && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w.dbg[1])::"memory");
       if (SMEM && col == 0) mbar_wait(bar, parity);
       if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
       const double* Ac = A + (int64_t)col * m;
@@ -594,6 +601,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
       }
       gather_chunk<NRHS>(p, w, lane, col, cc);
       __syncwarp();
+      if (p.trace && col == 0 && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w.dbg[1])::"memory");
       if (SMEM && col == 0) mbar_wait(bar, parity);
       if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
 #pragma unroll
@@ -638,6 +646,7 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
     }
   }
 
+  if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w.dbg[2])::"memory");
   store_rows<NRHS>(p, T, acc0, acc1, lane);
 }
 
@@ -1707,6 +1716,194 @@ __global__ void __launch_bounds__(256, 1) h2b_near_tma_kernel(KParams p) {
   }
 }
 
+
+// A sweep (Phase::mode 1): the far-field items of the bottom
+// subtrees of the cluster tree -- the leaf forward transforms and the upward
+// transfers below a subtree's root (h2.py:195-209), or the downward
+// transfers below it and the leaf back-transforms with the near-field
+// partial sums (h2.py:220-244).  One CTA runs a subtree: the items of a
+// tree level (a "wave") spread over its warps, a block barrier between
+// waves -- the links of the far-field chain inside a subtree cost a
+// __syncthreads instead of an arrival count, a queue push and a claim.
+// Every input from outside the subtree was written by an earlier launch.
+// A warp stages its items' matrices through two shared-memory buffers by TMA
+// bulk copies and prefetches its next item's matrix (same or next wave)
+// while the current one runs.
+constexpr int kSweepStage = 4096 + 32;  // one staged matrix (+ 16-byte alignment slack)
+inline size_t sweep_smem_bytes(int nw) { return (size_t)nw * (sizeof(WarpSmem) + ring_bytes(4096)) + 128; }
+
+__device__ __forceinline__ DTask load_task(const DTask* t) {
+  // read-only path: the line was prefetched to L1 while earlier items ran
+  union { DTask T; int4 q[4]; } u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u.q[i] = __ldg(reinterpret_cast<const int4*>(t) + i);
+  return u.T;
+}
+__device__ __forceinline__ void prefetch_l1(const void* q) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+}
+
+template <int NRHS>
+__global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
+  unsigned char* rb = smem_raw + (size_t)nw * sizeof(WarpSmem) + (size_t)wib * ring_bytes(4096);
+  double* buf[2] = {reinterpret_cast<double*>(rb), reinterpret_cast<double*>(rb + kSweepStage)};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rb + 2 * kSweepStage);
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(&w.bar);
+  int* next_unit = reinterpret_cast<int*>(smem_raw + (size_t)nw * (sizeof(WarpSmem) + ring_bytes(4096)));
+  if (lane == 0) {
+    mbar_init(bars);
+    mbar_init(bars + 1);
+    mbar_init(wbar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  Ctl* ctl = p.ctl;
+  // units are claimed from one counter (the next one while the current one
+  // runs); the last CTA to leave resets it for the next launch
+  if (threadIdx.x == 0) next_unit[0] = (int)atomicAdd(&ctl->static_head, 1u);
+  __syncthreads();
+  unsigned par = 0;   // parities of the two staging mbarriers (bit s)
+  int cur = 0;        // staging buffer of the next item
+  // bytes of an item's matrix rounded out to 16-byte boundaries, or 0 when
+  // it is not one contiguous block
+  auto span = [&](const DTask& T, uintptr_t& a0) -> unsigned {
+    if (T.ld != T.m || T.ncols <= 0) return 0u;
+    const double* g0 = p.mat + T.data;
+    a0 = (uintptr_t)g0 & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)(g0 + (size_t)T.m * T.ncols) + 15) & ~(uintptr_t)15;
+    return (unsigned)(a1 - a0);
+  };
+  unsigned long long t_gath = 0;
+  for (int k = 0;; ++k) {
+    const int u = next_unit[k & 1];
+    if (u >= p.nunits) break;
+    if (threadIdx.x == 0) next_unit[(k + 1) & 1] = (int)atomicAdd(&ctl->static_head, 1u);
+    const int wv0 = __ldg(p.unit0 + u), wv1 = __ldg(p.unit0 + u + 1);
+    // this warp's items in order: (wave, item), item = wave begin + warp, + nw, ...
+    auto first_from = [&](int wv, int& item) -> int {  // first wave >= wv holding an item of this warp
+      for (; wv < wv1; ++wv) {
+        item = __ldg(p.wave0 + wv) + wib;
+        if (item < __ldg(p.wave0 + wv + 1)) return wv;
+      }
+      item = -1;
+      return wv1;
+    };
+    auto advance = [&](int wv, int item, int& nitem) -> int {
+      nitem = item + nw;
+      if (nitem < __ldg(p.wave0 + wv + 1)) return wv;
+      return first_from(wv + 1, nitem);
+    };
+    int item, nx, nx2;
+    int wv_i = first_from(wv0, item);
+    int wv_n = wv1, wv_n2 = wv1;
+    nx = nx2 = -1;
+    if (item >= 0) wv_n = advance(wv_i, item, nx);
+    if (nx >= 0) wv_n2 = advance(wv_n, nx, nx2);
+    // prefetched matrix of `item`: staging mode (0: none yet) and offset
+    int pf_mode = 0, pf_off = 0;
+    if (nx >= 0) {
+      prefetch_l1(p.tasks + nx);
+      prefetch_l1(p.seg_inline + (int64_t)nx * kInlineSegs);
+    }
+    for (int wv = wv0; wv < wv1; ++wv) {
+      while (item >= 0 && wv_i == wv) {
+        unsigned long long t_start = 0;
+        if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        const DTask T = load_task(p.tasks + item);
+        DSeg sin{0, 0, 0, 0, 0};
+        if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
+        // this item's matrix: prefetched, staged now (one buffer, or both
+        // when it is larger), or streamed from global memory
+        int mode = pf_mode, off = pf_off;  // 1: staged in buf[cur], 2: across both buffers
+        if (mode == 0) {
+          uintptr_t a0 = 0;
+          const unsigned bytes = span(T, a0);
+          if (bytes > 0 && bytes <= 2u * kSweepStage) {
+            mode = bytes <= (unsigned)kSweepStage ? 1 : 2;
+            if (mode == 2) cur = 0;  // nothing is in flight: both buffers are free
+            if (lane == 0) bulk_load(buf[cur], (const void*)a0, bytes, bars + cur);
+            off = (int)(((uintptr_t)(p.mat + T.data) - a0) >> 3);
+          }
+        }
+        // the warp's next item: its matrix into the other buffer while this
+        // one runs (its descriptor was prefetched to L1 an item ago), and
+        // the descriptor after that towards L1
+        pf_mode = 0;
+        if (nx >= 0) {
+          if (mode == 1) {
+            const DTask N = load_task(p.tasks + nx);
+            uintptr_t n0 = 0;
+            const unsigned nb = span(N, n0);
+            if (nb > 0 && nb <= (unsigned)kSweepStage) {
+              if (lane == 0) bulk_load(buf[cur ^ 1], (const void*)n0, nb, bars + (cur ^ 1));
+              pf_mode = 1;
+              pf_off = (int)(((uintptr_t)(p.mat + N.data) - n0) >> 3);
+            }
+            // an up-leaf item's sources (a range of xp) towards L1 too
+            if (N.kind == h2b::kUpLeaf && lane < 8) {
+              const DSeg ns = p.seg_inline[(int64_t)nx * kInlineSegs];
+              const double* q = p.xp + ns.src * NRHS + lane * 16;
+              if (ns.kind == h2b::kSegX && lane * 16 < ns.ncols * NRHS) prefetch_l1(q);
+            }
+          }
+          if (nx2 >= 0) {
+            prefetch_l1(p.tasks + nx2);
+            prefetch_l1(p.seg_inline + (int64_t)nx2 * kInlineSegs);
+          }
+        }
+        const unsigned ph = (par >> cur) & 1u;
+        unsigned long long t_desc = 0;
+        if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_desc)::"memory");
+        if constexpr (NRHS >= 8) {
+          if (mode) run_item_mma<NRHS, true>(p, T, sin, w, lane, buf[cur] + off, bars + cur, ph, t_gath);
+          else run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, wbar, 0u, t_gath);
+        } else {
+          if (mode) run_item<NRHS, true, 16>(p, T, sin, w, lane, buf[cur] + off, bars + cur, ph, t_gath);
+          else run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, wbar, 0u, t_gath);
+        }
+        if (mode) par ^= 1u << cur;
+        if (mode == 1) cur ^= 1;
+        __syncwarp();
+        if (p.trace && lane == 0) {
+          unsigned long long t_end, smid;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&smid));
+          smid &= 0xffffffffull;
+          unsigned long long* tr = p.trace + 8 * (int64_t)item;
+          tr[0] = t_start;
+          tr[1] = t_end;
+          tr[2] = (smid << 32) | (unsigned)(blockIdx.x * nw + wib);
+          tr[3] = w.dbg[0];
+          tr[4] = w.dbg[2];
+          tr[5] = t_desc;
+          tr[6] = t_gath;
+          tr[7] = w.dbg[1];
+        }
+        item = nx;
+        wv_i = wv_n;
+        nx = nx2;
+        wv_n = wv_n2;
+        nx2 = -1;
+        wv_n2 = wv1;
+        if (nx >= 0) wv_n2 = advance(wv_n, nx, nx2);
+      }
+      __syncthreads();  // the wave's outputs are visible to the CTA's next wave
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
+      ctl->static_head = 0;
+      ctl->exited = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace
 
 namespace h2b_detail {
@@ -1732,6 +1929,10 @@ struct PhaseDev {
   unsigned* d_ready_flag = nullptr;
   Ctl* d_ctl = nullptr;
   unsigned long long* d_trace = nullptr;
+  int mode = 0, group = 0;        // Phase::mode, Phase::group
+  int32_t* d_unit0 = nullptr;     // sweeps
+  int32_t* d_wave0 = nullptr;
+  int32_t nunits = 0;
 };
 
 struct h2b_op {
@@ -1741,6 +1942,7 @@ struct h2b_op {
   int max_nrhs = 16;
   int wpc = 8;
   int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
+  int sweep_grid[5] = {0, 0, 0, 0, 0};
   double* d_mat = nullptr;
   double* d_coef = nullptr;
   int64_t* d_perm = nullptr;
@@ -1852,7 +2054,18 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     if ((o->plan_flags >> 4) & 0xf) po.coupling_task_bytes = (int64_t)1024 << ((o->plan_flags >> 4) & 0xf);
     if (o->plan_flags & H2B_PLAN_GATE) po.gate_coupling = true;
     if (o->plan_flags & H2B_PLAN_NO_GATE) po.gate_coupling = false;
+    if (o->plan_flags & H2B_PLAN_STAGED) po.staged = true;
+    if (o->plan_flags & H2B_PLAN_NO_STAGED) po.staged = false;
+    if ((o->plan_flags >> 12) & 0xf) po.sweep_nodes = (int64_t)64 << ((o->plan_flags >> 12) & 0xf);
   }
+  {
+    const char* sg = std::getenv("H2B_STAGED");  // A/B switch for tools and benches
+    if (sg && sg[0] == '1') po.staged = true;
+    if (sg && sg[0] == '0') po.staged = false;
+  }
+  // staged plans: the subtrees' items are staged one per 4 KB buffer and the
+  // next one prefetched, so they keep the small far-field pieces
+  if (po.staged && !(o && o->far_task_bytes > 0)) po.far_task_bytes = 4096;
   return po;
 }
 
@@ -1901,10 +2114,33 @@ int occupancy_grid(int wpc, int ring_warps, int ring_stage, int ctas_per_sm, int
   return H2B_OK;
 }
 
-// xp = x[perm] (when `permute`) then one phase of the plan.
 template <int NRHS>
-int launch_phase_dev(h2b_op* op, const PhaseDev& F, const double* x, double* y, cudaStream_t st, bool permute) {
-  KParams p;
+int sweep_grid(int wpc, int* grid) {
+  const size_t sm = sweep_smem_bytes(wpc);
+  H2B_CUDA(cudaFuncSetAttribute(h2b_sweep_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0, dev = 0, nsm = 0;
+  H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_sweep_kernel<NRHS>, wpc * 32, sm));
+  H2B_CUDA(cudaGetDevice(&dev));
+  H2B_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (per_sm < 1) return fail(H2B_EINVAL, "sweep kernel does not fit an SM: lower warps_per_cta");
+  *grid = per_sm * nsm;
+  return H2B_OK;
+}
+
+// xp = x[perm] (h2.py:192-193)
+template <int NRHS>
+int launch_permute(h2b_op* op, const double* x, cudaStream_t st) {
+  const int64_t total = op->n * NRHS;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(H2B_ECUDA, std::string("permute kernel launch: ") + cudaGetErrorString(e));
+  return H2B_OK;
+}
+
+template <int NRHS>
+KParams phase_params(h2b_op* op, const PhaseDev& F, double* y) {
+  KParams p{};
   p.tasks = F.d_tasks;
   p.segs = F.d_segs;
   p.seg_inline = F.d_seg_inline;
@@ -1932,20 +2168,24 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, const double* x, double* y, 
   p.flags = op->flags;
   p.ring_warps = op->ring_warps;
   p.ring_stage = op->ring_stage;
+  p.unit0 = F.d_unit0;
+  p.wave0 = F.d_wave0;
+  p.nunits = F.nunits;
+  return p;
+}
+
+// One dataflow launch (Phase::mode 0).
+template <int NRHS>
+int launch_phase_dev(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) {
+  if (F.ntasks == 0) return H2B_OK;
+  const KParams p = phase_params<NRHS>(op, F, y);
   const int gi = nrhs_index(NRHS);
   const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kRingStageBytes)
                                 : smem_bytes(op->wpc, op->ring_warps, op->ring_stage);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
-  if (permute) {
-    const int64_t total = op->n * NRHS;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-    h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
-  }
-  if (F.ntasks > 0) {
-    // the attribute is per function and shared by every operator of the process
-    H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
-  }
+  // the attribute is per function and shared by every operator of the process
+  H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
@@ -1955,28 +2195,25 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, const double* x, double* y, 
   return H2B_OK;
 }
 
+// One sweep launch (Phase::mode 1): a CTA per unit, round robin.
 template <int NRHS>
-int launch_phase(h2b_op* op, int k, const double* x, double* y, cudaStream_t st) {
-  return launch_phase_dev<NRHS>(op, op->ph[k], x, y, st, k == 0);
+int launch_sweep(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) {
+  if (F.ntasks == 0 || F.nunits == 0) return H2B_OK;
+  const KParams p = phase_params<NRHS>(op, F, y);
+  const size_t smem = sweep_smem_bytes(op->wpc);
+  H2B_CUDA(cudaFuncSetAttribute(h2b_sweep_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int gi = nrhs_index(NRHS);
+  const int grid = std::min<int>(op->sweep_grid[gi], F.nunits);
+  h2b_sweep_kernel<NRHS><<<grid, op->wpc * 32, smem, st>>>(p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(H2B_ECUDA, std::string("sweep kernel launch: ") + cudaGetErrorString(e));
+  return H2B_OK;
 }
 
 template <int NRHS, int STAGE>
-int launch_near(h2b_op* op, cudaStream_t st) {
-  const PhaseDev& F = op->ph_split[0];
+int launch_near(h2b_op* op, const PhaseDev& F, cudaStream_t st) {
   if (F.ntasks == 0) return H2B_OK;
-  KParams p{};
-  p.tasks = F.d_tasks;
-  p.segs = F.d_segs;
-  p.seg_inline = F.d_seg_inline;
-  p.ready0 = F.d_ready0;
-  p.nready0 = F.nready0;
-  p.ctl = F.d_ctl;
-  p.ntasks = (int32_t)F.ntasks;
-  p.mat = op->d_mat;
-  p.coef = op->d_coef;
-  p.perm = op->d_perm;
-  p.xp = op->d_xp;
-  p.flags = op->flags;
+  KParams p = phase_params<NRHS>(op, F, nullptr);
   const size_t smem = (size_t)op->wpc * sizeof(WarpSmem) + (size_t)op->wpc * ring_bytes(STAGE);
   H2B_CUDA(cudaMemsetAsync(&F.d_ctl->near_head, 0, sizeof(unsigned), st));
   H2B_CUDA(cudaFuncSetAttribute(h2b_near_kernel<NRHS, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1987,22 +2224,9 @@ int launch_near(h2b_op* op, cudaStream_t st) {
 }
 
 template <int NRHS, int NST>
-int launch_near_tma(h2b_op* op, cudaStream_t st) {
-  const PhaseDev& F = op->ph_split[0];
+int launch_near_tma(h2b_op* op, const PhaseDev& F, cudaStream_t st) {
   if (F.ntasks == 0) return H2B_OK;
-  KParams p{};
-  p.tasks = F.d_tasks;
-  p.segs = F.d_segs;
-  p.seg_inline = F.d_seg_inline;
-  p.ready0 = F.d_ready0;
-  p.nready0 = F.nready0;
-  p.ctl = F.d_ctl;
-  p.ntasks = (int32_t)F.ntasks;
-  p.mat = op->d_mat;
-  p.coef = op->d_coef;
-  p.perm = op->d_perm;
-  p.xp = op->d_xp;
-  p.flags = op->flags;
+  KParams p = phase_params<NRHS>(op, F, nullptr);
   const size_t smem = (size_t)op->near_warps * near_warp_smem<NRHS>(NST);
   H2B_CUDA(cudaMemsetAsync(&F.d_ctl->near_head, 0, sizeof(unsigned), st));
   H2B_CUDA(cudaFuncSetAttribute(h2b_near_tma_kernel<NRHS, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2019,39 +2243,46 @@ int launch_near_tma(h2b_op* op, cudaStream_t st) {
   return H2B_OK;
 }
 
-// 8/16 right-hand sides on one GPU: xp, the near field (lean kernel), then
-// the rest of the product (dataflow kernel, near dependencies satisfied).
+// One launch of the plan, by its mode.
 template <int NRHS>
-int launch_split(h2b_op* op, const double* x, double* y, cudaStream_t st) {
-  const int64_t total = op->n * NRHS;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  h2b_permute_kernel<NRHS><<<blocks, 256, 0, st>>>(x, op->d_perm, op->d_xp, op->n);
-  int rc = H2B_OK;
-  if (op->split_only != 2)
-    rc = op->near_impl == 1 ? (op->near_nst == 3 ? launch_near_tma<NRHS, 3>(op, st) : launch_near_tma<NRHS, 2>(op, st))
-         : op->near_stage == 4096 ? launch_near<NRHS, 4096>(op, st) : launch_near<NRHS, 8192>(op, st);
-  if (rc != H2B_OK || op->split_only == 1) return rc;
-  return launch_phase_dev<NRHS>(op, op->ph_split[1], x, y, st, false);
-}
-
-// The whole product: all phases, with the x^ all-gather between them.
-template <int NRHS>
-int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+int launch_one(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) {
+  if (F.mode == 1) return op->split_only == 1 ? H2B_OK : launch_sweep<NRHS>(op, F, y, st);
   if constexpr (NRHS >= 8) {
-    if (!op->ph_split.empty()) return launch_split<NRHS>(op, x, y, st);
-  }
-  for (int k = 0; k < (int)op->ph.size(); ++k) {
-    int rc = launch_phase<NRHS>(op, k, x, y, st);
-    if (rc != H2B_OK) return rc;
-    if (k == 0 && op->world > 1) {
-      if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
-      double* base = op->d_coef + op->exch_off * NRHS;
-      const size_t cnt = (size_t)op->exch_count * NRHS;
-      if (cnt > 0)
-        H2B_NCCL(ncclAllGather(base + (size_t)op->rank * cnt, base, cnt, ncclDouble, op->comm, st));
+    // the near field of a split multi-RHS product: the lean near kernel
+    if (F.mode == 2) {
+      if (op->split_only == 2) return H2B_OK;
+      return op->near_impl == 1 ? (op->near_nst == 3 ? launch_near_tma<NRHS, 3>(op, F, st)
+                                                     : launch_near_tma<NRHS, 2>(op, F, st))
+             : op->near_stage == 4096 ? launch_near<NRHS, 4096>(op, F, st) : launch_near<NRHS, 8192>(op, F, st);
     }
   }
+  if (op->split_only == 1) return H2B_OK;
+  return launch_phase_dev<NRHS>(op, F, y, st);
+}
+
+// The launches of one group (0: before the x^ exchange -- xp = x[perm]
+// first -- 1: after it).  8/16 right-hand sides on one GPU use the split
+// list (the near field in the lean kernel).
+template <int NRHS>
+int launch_group(h2b_op* op, int group, const double* x, double* y, cudaStream_t st) {
+  const std::vector<PhaseDev>& list = (NRHS >= 8 && !op->ph_split.empty()) ? op->ph_split : op->ph;
+  int rc = H2B_OK;
+  if (group == 0 && (rc = launch_permute<NRHS>(op, x, st)) != H2B_OK) return rc;
+  for (const PhaseDev& F : list)
+    if (F.group == group && (rc = launch_one<NRHS>(op, F, y, st)) != H2B_OK) return rc;
   return H2B_OK;
+}
+
+// The whole product: both groups, with the x^ all-gather between them.
+template <int NRHS>
+int launch(h2b_op* op, const double* x, double* y, cudaStream_t st) {
+  int rc = launch_group<NRHS>(op, 0, x, y, st);
+  if (rc != H2B_OK || op->world <= 1) return rc;
+  if (!op->comm) return fail(H2B_EINVAL, "multi-GPU operator without an NCCL communicator");
+  double* base = op->d_coef + op->exch_off * NRHS;
+  const size_t cnt = (size_t)op->exch_count * NRHS;
+  if (cnt > 0) H2B_NCCL(ncclAllGather(base + (size_t)op->rank * cnt, base, cnt, ncclDouble, op->comm, st));
+  return launch_group<NRHS>(op, 1, x, y, st);
 }
 
 template <typename T>
@@ -2075,6 +2306,8 @@ void free_phase(PhaseDev& F) {
   cudaFree(F.d_ready_flag);
   cudaFree(F.d_ctl);
   cudaFree(F.d_trace);
+  cudaFree(F.d_unit0);
+  cudaFree(F.d_wave0);
 }
 
 void free_op(h2b_op* op) {
@@ -2099,6 +2332,13 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   int rc;
   F->ntasks = P.ntasks();
   F->nnodes = P.nnodes;
+  F->mode = P.mode;
+  F->group = P.group;
+  if (P.mode == 1) {
+    if ((rc = upload(&F->d_unit0, P.unit0.data(), P.unit0.size()))) return rc;
+    if ((rc = upload(&F->d_wave0, P.wave0.data(), P.wave0.size()))) return rc;
+    F->nunits = (int32_t)P.unit0.size() - 1;
+  }
   std::vector<DTask> tasks(P.ntasks());
   for (int64_t i = 0; i < P.ntasks(); ++i) {
     DTask& t = tasks[i];
@@ -2151,7 +2391,8 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   F->ngated = (int32_t)P.gated.size();
   F->ngated1 = P.n_gated1;
   F->nup = P.n_up;
-  const size_t T1 = (size_t)std::max<int64_t>(1, P.ntasks());
+  // (a sweep has no scheduler state: one entry each)
+  const size_t T1 = P.mode == 1 ? 1 : (size_t)std::max<int64_t>(1, P.ntasks());
   if ((rc = upload<unsigned long long>(&F->d_arrived, nullptr, T1))) return rc;
   if ((rc = upload<int32_t>(&F->d_ready_q, nullptr, kQueues * T1))) return rc;
   if ((rc = upload<unsigned>(&F->d_ready_flag, nullptr, kQueues * T1))) return rc;
@@ -2254,7 +2495,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if (rc != H2B_OK) return fail(rc, err);
   for (const auto& F : P.ph) {
     if (F.ntasks() >= INT32_MAX / kQueues) return fail(H2B_EINVAL, "too many work items");
-    if (F.nnodes != F.ntasks())
+    if (F.mode != 1 && F.nnodes != F.ntasks())
       return fail(H2B_EINVAL, "band_depth > 1 (fused runs) is a planning option only: the kernel runs "
                               "single items (fused runs measured slower on B200, DESIGN.md)");
   }
@@ -2322,6 +2563,11 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[2]))) return rc;
   if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[3]))) return rc;
   if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[4]))) return rc;
+  if ((rc = sweep_grid<1>(op->wpc, &op->sweep_grid[0]))) return rc;
+  if ((rc = sweep_grid<2>(op->wpc, &op->sweep_grid[1]))) return rc;
+  if ((rc = sweep_grid<4>(op->wpc, &op->sweep_grid[2]))) return rc;
+  if ((rc = sweep_grid<8>(op->wpc, &op->sweep_grid[3]))) return rc;
+  if ((rc = sweep_grid<16>(op->wpc, &op->sweep_grid[4]))) return rc;
   if (!op->ph_split.empty()) {
     const char* st_env = std::getenv("H2B_NEAR_STAGE");
     op->near_stage = (st_env && std::atoi(st_env) == 4096) ? 4096 : 8192;
@@ -2378,7 +2624,7 @@ int reset_locked(h2b_op* op) {
   H2B_CUDA(cudaDeviceSynchronize());
   for (auto* list : {&op->ph, &op->ph_split})
   for (auto& F : *list) {
-    const size_t T1 = (size_t)std::max<int64_t>(1, F.ntasks);
+    const size_t T1 = F.mode == 1 ? 1 : (size_t)std::max<int64_t>(1, F.ntasks);
     H2B_CUDA(cudaMemset(F.d_arrived, 0, sizeof(unsigned long long) * T1));
     H2B_CUDA(cudaMemset(F.d_ready_flag, 0, sizeof(unsigned) * kQueues * T1));
     H2B_CUDA(cudaMemset(F.d_ctl, 0, sizeof(Ctl)));
@@ -2406,11 +2652,11 @@ int matvec_locked(h2b_op* op, int phase, const double* x, double* y, int nrhs, v
     }
   } else {
     switch (nrhs) {
-      case 1: rc = launch_phase<1>(op, phase, x, y, st); break;
-      case 2: rc = launch_phase<2>(op, phase, x, y, st); break;
-      case 4: rc = launch_phase<4>(op, phase, x, y, st); break;
-      case 8: rc = launch_phase<8>(op, phase, x, y, st); break;
-      default: rc = launch_phase<16>(op, phase, x, y, st); break;
+      case 1: rc = launch_group<1>(op, phase, x, y, st); break;
+      case 2: rc = launch_group<2>(op, phase, x, y, st); break;
+      case 4: rc = launch_group<4>(op, phase, x, y, st); break;
+      case 8: rc = launch_group<8>(op, phase, x, y, st); break;
+      default: rc = launch_group<16>(op, phase, x, y, st); break;
     }
   }
   if (rc != H2B_OK) {
@@ -2459,6 +2705,14 @@ void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
   v->s_nslots = F.s_nslots.data();
   v->s_stride = F.s_stride.data();
   v->deps = F.deps.data();
+  v->mode = F.mode;
+  v->group = F.group;
+  v->split = 0;
+  v->reserved_ = 0;
+  v->nunits = F.mode == 1 ? (int64_t)F.unit0.size() - 1 : 0;
+  v->nwaves = F.mode == 1 ? (int64_t)F.wave0.size() - 1 : 0;
+  v->unit0 = F.unit0.data();
+  v->wave0 = F.wave0.data();
 }
 
 }  // namespace
@@ -2496,6 +2750,7 @@ int h2b_plan_phase_view(const h2b_plan* p, int phase, h2b_plan_view* v) {
   const int n0 = p ? (int)p->plan.ph.size() : 0;
   if (!p || !v || phase < 0 || phase >= n0 + (int)p->plan.ph_split.size()) return fail(H2B_EINVAL, "bad plan or phase");
   fill_view(p->plan, phase < n0 ? p->plan.ph[phase] : p->plan.ph_split[phase - n0], v);
+  v->split = phase < n0 ? 0 : 1;
   return H2B_OK;
 }
 
@@ -2532,7 +2787,7 @@ int h2b_matvec_dev(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, voi
 }
 
 int h2b_matvec_phase(h2b_op* op, int phase, const double* x_dev, double* y_dev, int nrhs, void* stream) {
-  if (!op || phase < 0 || phase >= (int)op->ph.size()) return fail(H2B_EINVAL, "bad operator or phase");
+  if (!op || phase < 0 || phase > (op->world > 1 ? 1 : 0)) return fail(H2B_EINVAL, "bad operator or phase");
   std::lock_guard<std::mutex> lk(op->mu);
   return matvec_locked(op, phase, x_dev, y_dev, nrhs, stream);
 }
@@ -2618,7 +2873,13 @@ int64_t h2b_stream_bytes(const h2b_op* op) { return op ? op->stats.stream_bytes 
 // at create, 8/16 right-hand sides) the dataflow part of the split product.
 static PhaseDev& traced_phase(const h2b_op* op) {
   h2b_op* o = const_cast<h2b_op*>(op);
-  return (o->trace_split && !o->ph_split.empty()) ? o->ph_split[1] : o->ph[0];
+  std::vector<PhaseDev>& list = (o->trace_split && !o->ph_split.empty()) ? o->ph_split : o->ph;
+  // H2B_TRACE_PHASE=k: launch k of the list; default: its first dataflow launch
+  const char* tp = std::getenv("H2B_TRACE_PHASE");
+  if (tp && std::atoi(tp) >= 0 && std::atoi(tp) < (int)list.size()) return list[std::atoi(tp)];
+  for (auto& F : list)
+    if (F.mode == 0) return F;
+  return list[0];
 }
 
 int h2b_trace_enable(h2b_op* op, int on) {

@@ -56,6 +56,7 @@ struct TaskTmp {
   int32_t stage;
   int32_t qclass = 0;
   int32_t cl = 0;                // cluster (row cluster for down/near/final)
+  bool transfer = false;         // down item holding the parent-transfer segment (the chain link)
   std::vector<int32_t> seg_idx;  // into seg tables
   std::vector<int32_t> deps;     // provisional ids
 };
@@ -72,7 +73,16 @@ class Builder {
   Plan* plan_;
 
   std::vector<int32_t> parent_, depth_, height_;
+  std::vector<int32_t> order_;              // clusters in preorder
   std::vector<int32_t> leaves_;             // preorder == position order
+  // staged plans: root of the bottom subtree containing each cluster, or -1
+  // for the clusters above the subtrees ("top")
+  std::vector<int32_t> broot_;
+  bool top(int32_t c) const { return broot_.empty() || broot_[c] < 0; }
+  void mark_bottom_subtrees();
+  // a sweep phase from provisional task ids: units by bottom subtree (tree
+  // order), waves by dependency depth inside the unit
+  int finalize_sweep(Phase* F, const std::vector<int32_t>& ids, std::string* err);
   std::vector<Vec> xhat_, yhat_, nearv_;
   std::vector<TaskTmp> tasks_;
   int32_t cur_cl_ = 0;  // cluster of the group being emitted
@@ -180,6 +190,7 @@ int Builder::validate(std::string* err) {
     }
   }
   for (int32_t c : order) if (is_leaf(c)) leaves_.push_back(c);
+  order_ = order;
   // bases / transfers
   for (int64_t c = 0; c < nc; ++c) {
     if (is_leaf((int32_t)c)) {
@@ -317,7 +328,7 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       t.qclass = qclass;
       t.cl = cur_cl_;
       if (seg0_hi) {
-        for (auto& part : pc.parts) if (part[0] == 0) t.qclass = 0;
+        for (auto& part : pc.parts) if (part[0] == 0) { t.qclass = 0; t.transfer = true; }
       }
       if (outv) outv->producers.push_back((int32_t)tasks_.size());
       tasks_.push_back(std::move(t));
@@ -335,6 +346,7 @@ int Builder::run(std::string* err) {
   P.perm.assign(d->perm, d->perm + d->n);
   P.rank = opt_.rank;
   P.world_size = opt_.world_size;
+  if (opt_.staged) mark_bottom_subtrees();
 
   // Algorithmic byte count, H2Matrix.storage_bytes() (h2.py:77-83).
   int64_t entries = 0;
@@ -370,7 +382,9 @@ int Builder::run(std::string* err) {
       int32_t k = (int32_t)d->k_col[p];
       if (k == 0) continue;
       std::vector<SegSpec> segs;
-      const bool skip = opt_.skip_levels && height_[p] >= 2 && height_[p] % 2 == 0;
+      // (staged plans: only above the bottom subtrees, whose levels are
+      // separated by block barriers, not by scheduling links)
+      const bool skip = opt_.skip_levels && height_[p] >= 2 && height_[p] % 2 == 0 && top(p);
       for (int j = 0; j < 2; ++j) {
         int32_t ch = (int32_t)d->cl_child[2 * p + j];
         if (skip && !is_leaf(ch)) {
@@ -433,7 +447,8 @@ int Builder::run(std::string* err) {
       int32_t k = (int32_t)d->k_row[t];
       // odd heights (counted from the leaves, so the leaves skip their
       // parent's level), never two "own" levels in a row
-      if (t != 0 && opt_.skip_levels && !is_leaf(t) && height_[t] % 2 == 1 && !own_only[parent_[t]]) own_only[t] = 1;
+      if (t != 0 && opt_.skip_levels && !is_leaf(t) && height_[t] % 2 == 1 && !own_only[parent_[t]] && top(t))
+        own_only[t] = 1;
       if (k == 0) continue;
       std::vector<SegSpec> segs;
       bool transfer = false;
@@ -491,24 +506,60 @@ int Builder::run(std::string* err) {
   const int32_t T = (int32_t)tasks_.size();
   P.rank_lo.assign(1, 0);
   P.rank_hi.assign(1, d->n);
+  // staged plans: the sweeps' items
+  auto in_up_sweep = [&](const TaskTmp& t) {
+    return opt_.staged && (t.kind == kUpLeaf || t.kind == kUpNode) && !top(t.cl);
+  };
+  auto in_down_sweep = [&](const TaskTmp& t) {
+    return opt_.staged && (t.kind == kFinal || (t.kind == kDown && t.transfer && !top(t.cl)));
+  };
+  // the launches of one group of selected items: [up sweep] dataflow [down
+  // sweep]; with `split` the near field gets a launch of its own (mode 2)
+  auto emit_launches = [&](std::vector<Phase>* out, const std::vector<char>& in, int32_t group, bool split) -> int {
+    std::vector<int32_t> up, dn, near, rest;
+    std::vector<char> in_near(T, 0), in_rest(T, 0);
+    for (int32_t i = 0; i < T; ++i) {
+      if (!in[i]) continue;
+      const TaskTmp& t = tasks_[i];
+      if (in_up_sweep(t)) up.push_back(i);
+      else if (in_down_sweep(t)) dn.push_back(i);
+      else if (split && t.kind == kNear) { near.push_back(i); in_near[i] = 1; }
+      else { rest.push_back(i); in_rest[i] = 1; }
+    }
+    // closure: the dataflow launch must not wait for an item of the down sweep
+    for (int32_t i : rest)
+      for (int32_t dp : tasks_[i].deps)
+        if (in[dp] && in_down_sweep(tasks_[dp])) { *err = "internal: dataflow item depends on the down sweep"; return H2B_EINVAL; }
+    int rc2 = H2B_OK;
+    if (!up.empty()) {
+      out->emplace_back();
+      if ((rc2 = finalize_sweep(&out->back(), up, err)) != H2B_OK) return rc2;
+      out->back().group = group;
+    }
+    if (split) {
+      out->emplace_back();
+      if ((rc2 = finalize(&out->back(), near, in_near, err)) != H2B_OK) return rc2;
+      out->back().mode = 2;
+      out->back().group = group;
+    }
+    if (!rest.empty() || (!split && up.empty() && dn.empty())) {
+      out->emplace_back();
+      if ((rc2 = finalize(&out->back(), rest, in_rest, err)) != H2B_OK) return rc2;
+      out->back().group = group;
+    }
+    if (!dn.empty()) {
+      out->emplace_back();
+      if ((rc2 = finalize_sweep(&out->back(), dn, err)) != H2B_OK) return rc2;
+      out->back().group = group;
+    }
+    return H2B_OK;
+  };
   if (opt_.world_size <= 1) {
-    std::vector<int32_t> all(T);
-    std::iota(all.begin(), all.end(), 0);
-    P.ph.resize(1);
     P.local_bytes = P.stream_bytes;
     assign_bases(std::vector<char>(T, 1));
-    rc = finalize(&P.ph[0], all, std::vector<char>(T, 1), err);
+    rc = emit_launches(&P.ph, std::vector<char>(T, 1), 0, false);
     if (rc != H2B_OK || !opt_.near_split) return rc;
-    std::vector<char> is_near(T, 0), not_near(T, 0);
-    std::vector<int32_t> near_ids, rest_ids;
-    for (int32_t i = 0; i < T; ++i) {
-      if (tasks_[i].kind == kNear) { is_near[i] = 1; near_ids.push_back(i); }
-      else { not_near[i] = 1; rest_ids.push_back(i); }
-    }
-    P.ph_split.resize(2);
-    rc = finalize(&P.ph_split[0], near_ids, is_near, err);
-    if (rc != H2B_OK) return rc;
-    return finalize(&P.ph_split[1], rest_ids, not_near, err);
+    return emit_launches(&P.ph_split, std::vector<char>(T, 1), 0, true);
   }
 
   // ---- multi-GPU: byte-balanced contiguous leaf ranges (tree order is a
@@ -516,22 +567,30 @@ int Builder::run(std::string* err) {
   const int32_t W = opt_.world_size, R = opt_.rank;
   std::vector<double> leaf_w(nc, 0.0);
   for (auto& t : tasks_) leaf_w[t.cl] += 8.0 * t.m * t.ncols;
+  // granules of the partition: the leaves, or (staged) the bottom subtrees,
+  // so that a rank owns whole subtrees and sweeps them by itself
+  std::vector<std::pair<int64_t, double>> gran;  // (end position, weight)
+  for (size_t i = 0; i < leaves_.size(); ++i) {
+    const int32_t l = leaves_[i];
+    const bool same = opt_.staged && i > 0 && broot_[l] == broot_[leaves_[i - 1]];
+    if (same) { gran.back().first = d->cl_end[l]; gran.back().second += leaf_w[l] + 1.0; }
+    else gran.push_back({d->cl_end[l], leaf_w[l] + 1.0});
+  }
   double total = 0.0;
-  for (int32_t l : leaves_) total += leaf_w[l] + 1.0;
+  for (auto& g : gran) total += g.second;
   P.rank_lo.assign(W, 0);
   P.rank_hi.assign(W, 0);
   {
     double acc = 0.0;
     int32_t r = 0;
     P.rank_lo[0] = 0;
-    for (size_t i = 0; i < leaves_.size(); ++i) {
-      const int32_t l = leaves_[i];
-      acc += leaf_w[l] + 1.0;
-      const size_t left = leaves_.size() - i - 1;
+    for (size_t i = 0; i < gran.size(); ++i) {
+      acc += gran[i].second;
+      const size_t left = gran.size() - i - 1;
       if (r < W - 1 && (acc >= total * (r + 1) / W || left <= (size_t)(W - 1 - r))) {
-        P.rank_hi[r] = d->cl_end[l];
+        P.rank_hi[r] = gran[i].first;
         ++r;
-        P.rank_lo[r] = d->cl_end[l];
+        P.rank_lo[r] = gran[i].first;
       }
     }
     for (; r < W; ++r) {
@@ -625,30 +684,115 @@ int Builder::run(std::string* err) {
     P.exch_off = 0;
     P.exch_count = rsz;
   }
-  P.ph.resize(2);
-  std::vector<int32_t> ids0, ids1;
   P.local_bytes = 0;
-  for (int32_t i = 0; i < T; ++i) {
-    if (in0[i]) ids0.push_back(i);
-    if (in1[i]) ids1.push_back(i);
+  for (int32_t i = 0; i < T; ++i)
     if (sel[i]) P.local_bytes += 8 * (int64_t)tasks_[i].m * tasks_[i].ncols;
-  }
   // a phase-1 dependency on a phase-1 item of another rank would be a
   // missing exchange: check the selection is closed
-  for (int32_t i : ids1)
+  for (int32_t i = 0; i < T; ++i) {
+    if (!in1[i]) continue;
     for (int32_t dp : tasks_[i].deps)
       if (!in1[dp] && !(tasks_[dp].kind == kUpLeaf || tasks_[dp].kind == kUpNode ||
                         (tasks_[dp].kind == kNear && in0[dp]))) {
         *err = "internal: rank plan is missing a dependency";
         return H2B_EINVAL;
       }
+  }
   // this rank's pool: only the matrices of its selected items (the
   // replicated upper clusters plus its own rows), so per-rank host and
   // device memory scale as 1/world
   assign_bases(sel);
-  rc = finalize(&P.ph[0], ids0, in0, err);
+  // group 0 (before the exchange) always has a dataflow launch, possibly
+  // empty, so that classic plans keep their two phases
+  rc = emit_launches(&P.ph, in0, 0, false);
   if (rc != H2B_OK) return rc;
-  return finalize(&P.ph[1], ids1, in1, err);
+  return emit_launches(&P.ph, in1, 1, false);
+}
+
+void Builder::mark_bottom_subtrees() {
+  const h2b_desc* d = d_;
+  const int64_t nc = d->nclusters;
+  int64_t S = opt_.sweep_nodes > 0 ? opt_.sweep_nodes : 1024;
+  auto mark = [&](int64_t cap) -> int64_t {
+    broot_.assign(nc, -1);
+    int64_t roots = 0;
+    for (int32_t c : order_) {  // preorder: parents first
+      const int32_t p = parent_[c];
+      if (p >= 0 && broot_[p] >= 0) broot_[c] = broot_[p];
+      else if (size(c) <= cap || is_leaf(c)) { broot_[c] = c; ++roots; }
+    }
+    return roots;
+  };
+  int64_t roots = mark(S);
+  // multi-GPU: ranks own whole subtrees, so there must be enough of them to
+  // balance the ranks' bytes
+  const int64_t want = opt_.world_size > 1 ? std::min<int64_t>(8 * (int64_t)opt_.world_size, (int64_t)leaves_.size()) : 1;
+  while (roots < want && S > 1) {
+    S /= 2;
+    roots = mark(S);
+  }
+}
+
+int Builder::finalize_sweep(Phase* F, const std::vector<int32_t>& ids, std::string* err) {
+  const int32_t T = (int32_t)ids.size();
+  std::vector<int32_t> wave(tasks_.size(), -1);
+  // provisional ids grow along dependencies (a producer is emitted before
+  // its consumers), so one ascending pass gives the dependency depth
+  std::vector<int32_t> sorted(ids);
+  std::sort(sorted.begin(), sorted.end());
+  std::vector<char> in(tasks_.size(), 0);
+  for (int32_t i : sorted) in[i] = 1;
+  for (int32_t i : sorted) {
+    int32_t w = 0;
+    for (int32_t dp : tasks_[i].deps) {
+      if (!in[dp]) continue;  // produced by an earlier launch
+      if (dp >= i || wave[dp] < 0 || broot_[tasks_[dp].cl] != broot_[tasks_[i].cl]) {
+        *err = "internal: sweep dependency outside its subtree";
+        return H2B_EINVAL;
+      }
+      w = std::max(w, wave[dp] + 1);
+    }
+    wave[i] = w;
+  }
+  // units in tree order of their roots; items by wave, then emission order
+  std::stable_sort(sorted.begin(), sorted.end(), [&](int32_t a, int32_t b) {
+    const int32_t ra = broot_[tasks_[a].cl], rb = broot_[tasks_[b].cl];
+    if (ra != rb) return d_->cl_start[ra] < d_->cl_start[rb];
+    return wave[a] < wave[b];
+  });
+  F->mode = 1;
+  F->t_data.resize(T); F->t_out.resize(T); F->t_bias.resize(T);
+  F->t_m.resize(T); F->t_ld.resize(T); F->t_ncols.resize(T); F->t_kind.resize(T);
+  F->t_bias_nslots.resize(T); F->t_bias_stride.resize(T); F->t_qclass.assign(T, 0);
+  F->t_mlen.assign(T, 0);
+  F->t_seg0.assign(T + 1, 0); F->t_dep0.assign(T + 1, 0);
+  F->succ0.assign(T + 1, 0);
+  F->unit0.clear(); F->wave0.clear();
+  int32_t unit_first = 0;
+  for (int32_t k = 0; k < T; ++k) {
+    const TaskTmp& t = tasks_[sorted[k]];
+    const bool new_unit = k == 0 || broot_[t.cl] != broot_[tasks_[sorted[k - 1]].cl];
+    if (new_unit) {
+      if (k > 0) F->t_mlen[unit_first] = k - unit_first;
+      unit_first = k;
+      F->unit0.push_back((int32_t)F->wave0.size());
+    }
+    if (new_unit || wave[sorted[k]] != wave[sorted[k - 1]]) F->wave0.push_back(k);
+    F->t_data[k] = t.data; F->t_out[k] = t.out; F->t_bias[k] = t.bias;
+    F->t_m[k] = t.m; F->t_ld[k] = t.ld; F->t_ncols[k] = t.ncols; F->t_kind[k] = t.kind;
+    F->t_bias_nslots[k] = t.bias_nslots; F->t_bias_stride[k] = t.bias_stride;
+    for (int32_t si : t.seg_idx) {
+      F->s_src.push_back(s_src_[si]); F->s_ncols.push_back(s_ncols_[si]); F->s_kind.push_back(s_kind_[si]);
+      F->s_nslots.push_back(s_nslots_[si]); F->s_stride.push_back(s_stride_[si]);
+    }
+    F->t_seg0[k + 1] = (int32_t)F->s_ncols.size();
+    F->tasks_by_kind[t.kind] += 1;
+  }
+  if (T > 0) F->t_mlen[unit_first] = T - unit_first;
+  F->unit0.push_back((int32_t)F->wave0.size());
+  F->wave0.push_back(T);
+  F->nnodes = (int64_t)F->unit0.size() - 1;
+  return H2B_OK;
 }
 
 void Builder::assign_bases(const std::vector<char>& sel) {
@@ -877,9 +1021,31 @@ int Builder::finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char
     std::vector<int32_t> rest;
     for (int32_t k = 0; k < T; ++k)
       if (F->t_mlen[k] > 0 && F->t_dep0[k + 1] == F->t_dep0[k] && F->t_qclass[k] != 0 && !gated[k]) rest.push_back(k);
-    std::stable_sort(rest.begin(), rest.end(), [&](int32_t a, int32_t b) {
+    auto longer = [&](int32_t a, int32_t b) {
       return (int64_t)F->t_m[a] * F->t_ncols[a] > (int64_t)F->t_m[b] * F->t_ncols[b];
-    });
+    };
+    std::stable_sort(rest.begin(), rest.end(), longer);
+    // Staged plans: the coupling rows of the bottom clusters are static too.
+    // They are small and gather-bound: behind the near field they would form
+    // a slow tail, so the two lists (each longest first) are merged in
+    // proportion to their bytes and stream side by side.
+    std::vector<int32_t> nearl, cpl;
+    for (int32_t k : rest) (F->t_kind[k] == kNear ? nearl : cpl).push_back(k);
+    if (opt_.staged && !nearl.empty() && !cpl.empty()) {
+      auto bytes = [&](int32_t k) { return (double)F->t_m[k] * F->t_ncols[k]; };
+      double bn = 0.0, bc = 0.0;
+      for (int32_t k : nearl) bn += bytes(k);
+      for (int32_t k : cpl) bc += bytes(k);
+      rest.clear();
+      size_t i = 0, j = 0;
+      double dn = 0.0, dc = 0.0;
+      while (i < nearl.size() || j < cpl.size()) {
+        // take from the list that is behind its share
+        const bool take_near = j >= cpl.size() || (i < nearl.size() && dn * bc <= dc * bn);
+        if (take_near) { dn += bytes(nearl[i]); rest.push_back(nearl[i++]); }
+        else { dc += bytes(cpl[j]); rest.push_back(cpl[j++]); }
+      }
+    }
     F->ready0.insert(F->ready0.end(), rest.begin(), rest.end());
   }
   return H2B_OK;

@@ -71,6 +71,17 @@ struct Phase {
   int32_t n_gated1 = 0;             // gated[0:n_gated1) are class 1
   int32_t n_up = 0;
   int64_t tasks_by_kind[5] = {0, 0, 0, 0, 0};
+  // Launch kind and position in the product (staged plans).
+  // mode 0: the completion-driven dataflow kernel; 1: a sweep -- CTA-
+  // cooperative units (bottom subtrees of the cluster tree) whose items run
+  // wave by wave with a block barrier between waves, no arrival counters;
+  // 2: near-field items only (multi-RHS: the lean near kernel).
+  // group 0: before the x^ exchange of a multi-GPU product, 1: after it.
+  int32_t mode = 0, group = 0;
+  // sweeps: unit u is waves [unit0[u], unit0[u+1]); wave w is the items
+  // [wave0[w], wave0[w+1]) of the queue (a unit's items are contiguous and
+  // form one fused run: t_mlen = its length at its first item)
+  std::vector<int32_t> unit0, wave0;
 
   int64_t ntasks() const { return (int64_t)t_m.size(); }
   int64_t nsegs() const { return (int64_t)s_ncols.size(); }
@@ -147,6 +158,17 @@ struct PlanOptions {
   // release coupling rows behind one counter of finished upward items
   // instead of one arrival per (source, row) edge
   bool gate_coupling = false;
+  // Staged product: the clusters of at most `sweep_nodes`
+  // nodes whose parents are larger root "bottom subtrees".  Their upward
+  // items run first as a sweep (one CTA per subtree, block barriers between
+  // tree levels), then one dataflow launch runs the near field, every
+  // coupling row and the far-field chain of the clusters above the subtrees,
+  // then a second sweep runs the subtrees' downward transfers and the finals.
+  // Only the short top chain keeps arrival counters; near items and the
+  // coupling rows of bottom clusters have neither inputs to wait for nor
+  // successors to notify.  Multi-GPU: ranks own whole subtrees.
+  bool staged = false;
+  int64_t sweep_nodes = 0;        // 0: default (1024)
   int32_t rank = 0;
   int32_t world_size = 1;
 };

@@ -211,6 +211,13 @@ PLAN_NO_SKIP = 2
 PLAN_NEAR_SPLIT = 4
 PLAN_GATE = 1 << 8
 PLAN_NO_GATE = 1 << 9
+PLAN_STAGED = 1 << 10
+PLAN_NO_STAGED = 1 << 11
+
+
+def PLAN_SWEEP_NODES(v: int) -> int:
+    """Bottom subtrees of at most 64 << v nodes (plan_flags bits 12-15)."""
+    return (int(v) & 0xF) << 12
 
 
 def _options(task_bytes=0, far_task_bytes=0, warps_per_cta=0, ctas_per_sm=0, max_nrhs=0, sched_flags=0,
@@ -257,6 +264,9 @@ def _grab_view(v) -> dict:
         "s_stride": grab(v.s_stride, S, np.int32), "deps": grab(v.deps, D, np.int32),
         "t_mlen": grab(v.t_mlen, T, np.int32),
         "gated": grab(v.gated, int(v.ngated), np.int32), "n_gated1": int(v.n_gated1), "n_up": int(v.n_up),
+        "mode": int(v.mode), "group": int(v.group), "split": int(v.split),
+        "unit0": grab(v.unit0, int(v.nunits) + 1, np.int32) if v.mode == 1 else np.zeros(0, np.int32),
+        "wave0": grab(v.wave0, int(v.nwaves) + 1, np.int32) if v.mode == 1 else np.zeros(0, np.int32),
     }
 
 

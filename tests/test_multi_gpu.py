@@ -83,7 +83,7 @@ _GLOO_WORKER = textwrap.dedent("""
     import torch.distributed as dist
     sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
     from conftest import load_golden
-    from oracle.flat_matvec import run_phase
+    from oracle.flat_matvec import run_group
     from paper_1811_05731_b200.h2 import plan_view
     dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}",
                             rank=int(sys.argv[1]), world_size=2)
@@ -93,13 +93,13 @@ _GLOO_WORKER = textwrap.dedent("""
     x = ex["X"][:, 0]
     coef = np.full((p["coef_len"], 1), np.nan)
     y = np.zeros((op.n, 1))
-    run_phase(p["phases"][0], x, coef, y)
+    run_group(p, 0, x, coef, y)
     off, cnt = p["exchange"]
     parts = [torch.zeros(cnt, dtype=torch.float64) for _ in range(W)]
     dist.all_gather(parts, torch.from_numpy(coef[off + r * cnt: off + (r + 1) * cnt, 0].copy()))
     for q in range(W):
         coef[off + q * cnt: off + (q + 1) * cnt, 0] = parts[q].numpy()
-    run_phase(p["phases"][1], x, coef, y)
+    run_group(p, 1, x, coef, y)
     lo, hi = p["rank_lo_hi"][r]
     mine = np.zeros(op.n)
     mine[p["perm"][lo:hi]] = y[p["perm"][lo:hi], 0]

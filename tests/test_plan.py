@@ -25,7 +25,7 @@ def test_abi_exports_every_declared_symbol():
     lib = ctypes.CDLL(str(nat.LIB_PATH))
     for nm in names:
         assert hasattr(lib, nm), nm
-    assert nat.lib().h2b_abi_version() == 3
+    assert nat.lib().h2b_abi_version() == 4
 
 
 @pytest.mark.parametrize("task_bytes", [0, 4096, 512])

@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--opts", default="{}")
     ap.add_argument("--save", default="")
     ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--phase", type=int, default=-1,
+                    help="launch of the plan to trace (staged plans: 0 up sweep, 1 dataflow, 2 down sweep); "
+                         "default: the first dataflow launch")
     a = ap.parse_args()
     import torch
     import __graft_entry__
@@ -53,7 +56,12 @@ def main():
         plan = pv["phases"][2]
         plan["stats"] = pv["stats"]
     else:
-        plan = plan_view(op, **opts)
+        pv = plan_view(op, **opts)
+        k = a.phase if a.phase >= 0 else [ph["mode"] for ph in pv["phases"]].index(0)
+        os.environ["H2B_TRACE_PHASE"] = str(k)
+        plan = pv["phases"][k]
+        plan["stats"] = pv["stats"]
+        print(f"launches: {[(ph['mode'], len(ph['t_m'])) for ph in pv['phases']]}, tracing launch {k}")
     dev = DeviceOperator(op, **opts)
     lib = nat.lib()
     lib.h2b_trace_enable.argtypes = [C.c_void_p, C.c_int]
@@ -90,6 +98,16 @@ def main():
     t_succ = tr[:, 1].astype(np.int64) - tr_
     nbytes = 8 * plan["t_m"].astype(np.int64) * plan["t_ncols"]
     print(f"items {T}, span {end.max() / 1e3:.1f} us, bytes {nbytes.sum() / 1e6:.1f} MB")
+    if plan.get("mode", 0) == 1:
+        # sweeps record more stages: descriptors and prefetch issue, segment
+        # table, gather, wait for the staged matrix, multiply, store
+        seg, gat = tr[:, 3].astype(np.int64), tr[:, 7].astype(np.int64)
+        for k in range(5):
+            sel = (kind == k) & unit & (seg > 0)
+            if sel.any():
+                parts = [td - ts, seg - td, gat - seg, tg - gat, tr_ - tg, tr[:, 1].astype(np.int64) - tr_]
+                print(f"  {KINDS[k]:8s} stages us: " + " ".join(
+                    f"{nm} {v[sel].mean() / 1e3:5.2f}" for nm, v in zip(("desc", "segtab", "gather", "wait", "fma", "store"), parts)))
     mlen = plan.get("t_mlen", np.ones(T, np.int32))
     print(f"units {int(unit.sum())}, fused runs {int((mlen > 1).sum())} (mean length "
           f"{mlen[mlen > 1].mean() if (mlen > 1).any() else 0:.1f})")
