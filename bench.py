@@ -132,17 +132,20 @@ def _build(args, rank, ws, log):
 
 
 def _traffic(args):
-    """DRAM bytes per launch of the dataflow kernel from the committed ncu
-    capture of this workload (profiles/r01_traffic.json), or --traffic."""
+    """DRAM bytes per product (every launch of a step, summed) from the
+    committed ncu capture of this workload (profiles/r02_traffic.json, else
+    the round-1 file), or --traffic."""
     if args.traffic is not None:
         return args.traffic
     if args.nrhs != 1 or args.world > 1:
         return None
-    try:
-        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
-        return t[args.config]["bytes"]
-    except (OSError, KeyError, ValueError):
-        return None
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            t = json.loads((ROOT / "profiles" / name).read_text())
+            return t[args.config]["bytes"]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 L2_BYTES = 126 * 2**20
@@ -405,6 +408,23 @@ def run_b200(args):
         e2e["host_input"] = "pageable numpy array (as apply_operator / compute_demag pass it)"
         e2e_pinned = e2e_time(torch.from_numpy(np.ascontiguousarray(xh)).pin_memory().numpy())
         e2e_pinned["host_input"] = "pinned"
+    # per-launch device times (CUDA events around every launch, on the
+    # launching stream): the dominant kernel's own roofline beside the whole
+    # product's
+    kernels = None
+    dominant = None
+    if ws == 1:
+        kernels = dev.launch_times(x.data_ptr(), y.data_ptr(), nrhs, max(3, min(20, args.steps)), sp)
+        xy = 16 * n * nrhs
+        for kd in kernels:
+            kd["GB/s"] = round(kd["bytes"] / (kd["ms"] * 1e-3) / 1e9, 1) if kd["ms"] > 0 and kd["bytes"] else None
+        dominant = max(kernels, key=lambda kd: kd["ms"])
+        tot = sum(kd["ms"] for kd in kernels)
+        dominant = {"kernel": dominant["kernel"], "ms": dominant["ms"], "share_of_step": dominant["ms"] / tot,
+                    "algorithmic_bytes": dominant["bytes"],
+                    "achieved": dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9,
+                    "frac": dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    nlaunch = len(dev.launches(nrhs)) + (1 if ws > 1 else 0)   # multi-GPU: + the x^ all-gather (NCCL)
     cpu = None
     if rank == 0 and ws == 1 and not args.profile and not args.no_cpu_baseline:
         x0 = xh if nrhs == 1 else np.ascontiguousarray(xh[:, 0])
@@ -423,9 +443,11 @@ def run_b200(args):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"] * ws, "unit": "GB/s",
                              "frac": achieved / (peaks["hbm_gbs"] * ws), "traffic": _traffic(args),
                              "peak_kind": peak_kind, "aggregate_over_gpus": ws,
-                             "algorithmic_bytes_per_launch": b_alg},
+                             "algorithmic_bytes_per_launch": b_alg,
+                             "scope": "the whole product (every launch of a step)",
+                             "dominant_kernel": dominant, "kernels": kernels},
                 "cpu_baseline": cpu, "e2e": e2e, "e2e_pinned": e2e_pinned,
-                "gpu_launches": (2 if ws == 1 else 3) * args.steps, "clocks": clocks,
+                "gpu_launches": nlaunch * args.steps, "clocks": clocks,
                 "parity_rel_err_vs_oracle": max(parity.values()) if parity else None,
                 "parity": parity,
                 "build": {**{k: v for k, v in info.items() if k not in ("build_seconds", "coords")},

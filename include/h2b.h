@@ -188,7 +188,8 @@ typedef struct h2b_options {
 #define H2B_PLAN_STAGED (1 << 10)
 #define H2B_PLAN_NO_STAGED (1 << 11)
 /* plan_flags bits 12-15 (v > 0): bottom subtrees hold at most 64 << v nodes
-   (default 1024; multi-GPU plans shrink it until there are 8 subtrees per
+   (default: the power of two giving about 256 subtrees per rank, between 128
+   and 16384 nodes; multi-GPU plans shrink it until there are 8 subtrees per
    rank, since ranks own whole subtrees) */
 #define H2B_PLAN_SWEEP_NODES(v) (((v) & 0xf) << 12)
 
@@ -213,6 +214,10 @@ typedef struct h2b_stats {
   int32_t ring_warps;       /* single-vector TMA-ring warps per CTA        */
   int64_t extra_bytes;      /* pool bytes beyond stream_bytes (transfer
                                products of the level-skipping chain)       */
+  int32_t launches;         /* kernel launches per single-vector product (after xp = x[perm]) */
+  int32_t resident_mask;    /* bit i: the sweeps of a product with 1 << i
+                               right-hand sides run from shared memory
+                               (resident sweep kernel); operators only     */
 } h2b_stats;
 
 /* Plan arrays for host-side inspection (tests execute them with a numpy
@@ -253,10 +258,20 @@ typedef struct h2b_plan_view {
   int32_t mode, group;
   int32_t split;            /* 1: a launch of the split multi-RHS product
                                (H2B_PLAN_NEAR_SPLIT), 0: of the plain one    */
-  int32_t reserved_;
+  int32_t resident;         /* sweeps: every unit's inputs are contiguous
+                               ranges (u_range), so a CTA can run it from
+                               shared memory                                */
   int64_t nunits, nwaves;
   const int32_t* unit0;     /* [nunits+1] sweeps: unit u = waves [unit0[u], unit0[u+1]) */
   const int32_t* wave0;     /* [nwaves+1] sweeps: wave w = items [wave0[w], wave0[w+1]) */
+  const int64_t* u_range;   /* [8*nunits] sweeps, per unit (offset, doubles):
+                               matrices in the pool; the x^ (upward) or y^
+                               (downward) slots of its clusters; the near-field
+                               partial slots of its leaves (downward); its
+                               tree-position range of x (upward)            */
+  int64_t res_mat_max;      /* sweeps: the largest unit's matrix doubles ...  */
+  int64_t res_vec_max;      /* ... its coefficient + partial + x doubles ...  */
+  int64_t res_items_max;    /* ... and the most items of a unit               */
 } h2b_plan_view;
 
 int h2b_abi_version(void);
@@ -308,6 +323,17 @@ int h2b_exchange_region(h2b_op* op, int nrhs, double** base, int64_t* count_per_
 int h2b_exchange_copy(h2b_op* dst, const h2b_op* src, int nrhs, void* stream);
 int64_t h2b_stream_bytes(const h2b_op* op);
 int h2b_stats_get(const h2b_op* op, h2b_stats* out);
+/* The kernel launches of a product with `nrhs` right-hand sides, in order
+ * (launch 0 is xp = x[perm]): h2b_launch_count returns how many; per launch
+ * its kind (-1 permutation gather, 0 dataflow kernel, 1 sweep kernel, 2 lean
+ * near-field kernel), its work items and the matrix bytes they stream.
+ * h2b_launch_times runs `steps` products on `stream` with CUDA events around
+ * every launch and returns the mean milliseconds of each (measurement aid:
+ * bench.py reports the dominant kernel's roofline from it; single GPU). */
+int h2b_launch_count(const h2b_op* op, int nrhs);
+int h2b_launch_info(const h2b_op* op, int nrhs, int launch, int32_t* kind, int64_t* items, int64_t* bytes);
+int h2b_launch_times(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, int steps, void* stream,
+                     double* ms_per_launch);
 void h2b_destroy(h2b_op* op);
 
 /* ---- Operator files: the reference's "H2MS" v1 format (persist.py:22-199)

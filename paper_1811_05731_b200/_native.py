@@ -57,6 +57,7 @@ class Stats(C.Structure):
         ("grid", C.c_int32), ("warps_per_cta", C.c_int32), ("rank", C.c_int32),
         ("world_size", C.c_int32), ("local_bytes", C.c_int64),
         ("sched_flags", C.c_int32), ("ring_warps", C.c_int32), ("extra_bytes", C.c_int64),
+        ("launches", C.c_int32), ("resident_mask", C.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -77,8 +78,9 @@ class PlanView(C.Structure):
         ("s_src", _p64), ("s_ncols", _p32), ("s_kind", _p32), ("s_nslots", _p32),
         ("s_stride", _p32), ("deps", _p32), ("t_mlen", _p32),
         ("gated", _p32), ("ngated", C.c_int64), ("n_gated1", C.c_int32), ("n_up", C.c_int32),
-        ("mode", C.c_int32), ("group", C.c_int32), ("split", C.c_int32), ("reserved_", C.c_int32), ("nunits", C.c_int64), ("nwaves", C.c_int64),
-        ("unit0", _p32), ("wave0", _p32),
+        ("mode", C.c_int32), ("group", C.c_int32), ("split", C.c_int32), ("resident", C.c_int32), ("nunits", C.c_int64), ("nwaves", C.c_int64),
+        ("unit0", _p32), ("wave0", _p32), ("u_range", _p64),
+        ("res_mat_max", C.c_int64), ("res_vec_max", C.c_int64), ("res_items_max", C.c_int64),
     ]
 
 
@@ -119,6 +121,12 @@ def _load():
     lib.h2b_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]
     lib.h2b_destroy.argtypes = [C.c_void_p]
     lib.h2b_destroy.restype = None
+    lib.h2b_launch_count.argtypes = [C.c_void_p, C.c_int]
+    lib.h2b_launch_count.restype = C.c_int
+    lib.h2b_launch_info.argtypes = [C.c_void_p, C.c_int, C.c_int, _p32, _p64, _p64]
+    lib.h2b_launch_info.restype = C.c_int
+    lib.h2b_launch_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, _pd]
+    lib.h2b_launch_times.restype = C.c_int
     lib.h2b_nccl_unique_id.argtypes = [C.c_void_p]
     lib.h2b_plan_phases.argtypes = [C.c_void_p]
     lib.h2b_plan_phase_view.argtypes = [C.c_void_p, C.c_int, C.POINTER(PlanView)]

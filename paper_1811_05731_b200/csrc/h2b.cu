@@ -132,6 +132,10 @@ struct KParams {
   const int32_t* __restrict__ unit0;
   const int32_t* __restrict__ wave0;
   int32_t nunits;
+  // resident sweeps: per-unit ranges (Phase::u_range) and the shared-memory
+  // capacities (doubles; items) the launch was sized for
+  const int64_t* __restrict__ u_range;
+  int32_t cap_mat, cap_vec, cap_items;
 };
 
 // scheduling switches
@@ -1733,7 +1737,7 @@ constexpr int kSweepStage = 4096 + 32;  // one staged matrix (+ 16-byte alignmen
 inline size_t sweep_smem_bytes(int nw) { return (size_t)nw * (sizeof(WarpSmem) + ring_bytes(4096)) + 128; }
 
 __device__ __forceinline__ DTask load_task(const DTask* t) {
-  // read-only path: the line was prefetched to L1 while earlier items ran
+  // read-only path: the line was prefetched while earlier items ran
   union { DTask T; int4 q[4]; } u;
 #pragma unroll
   for (int i = 0; i < 4; ++i) u.q[i] = __ldg(reinterpret_cast<const int4*>(t) + i);
@@ -1743,6 +1747,11 @@ __device__ __forceinline__ void prefetch_l1(const void* q) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
 }
 
+// The generic sweep: units are claimed from one counter; a warp stages its
+// items' matrices through two shared-memory buffers by TMA bulk copies and
+// prefetches its next item's matrix (same or a later wave of the unit) while
+// the current one runs.  Used when a unit's inputs do not fit shared memory
+// (large subtrees, many right-hand sides); see the resident kernel below.
 template <int NRHS>
 __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1762,8 +1771,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KPara
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   Ctl* ctl = p.ctl;
-  // units are claimed from one counter (the next one while the current one
-  // runs); the last CTA to leave resets it for the next launch
+  // the next unit is claimed while the current one runs; the last CTA to
+  // leave resets the counter for the next launch
   if (threadIdx.x == 0) next_unit[0] = (int)atomicAdd(&ctl->static_head, 1u);
   __syncthreads();
   unsigned par = 0;   // parities of the two staging mbarriers (bit s)
@@ -1830,8 +1839,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KPara
           }
         }
         // the warp's next item: its matrix into the other buffer while this
-        // one runs (its descriptor was prefetched to L1 an item ago), and
-        // the descriptor after that towards L1
+        // one runs, and the descriptor after that towards L1
         pf_mode = 0;
         if (nx >= 0) {
           if (mode == 1) {
@@ -1842,12 +1850,6 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KPara
               if (lane == 0) bulk_load(buf[cur ^ 1], (const void*)n0, nb, bars + (cur ^ 1));
               pf_mode = 1;
               pf_off = (int)(((uintptr_t)(p.mat + N.data) - n0) >> 3);
-            }
-            // an up-leaf item's sources (a range of xp) towards L1 too
-            if (N.kind == h2b::kUpLeaf && lane < 8) {
-              const DSeg ns = p.seg_inline[(int64_t)nx * kInlineSegs];
-              const double* q = p.xp + ns.src * NRHS + lane * 16;
-              if (ns.kind == h2b::kSegX && lane * 16 < ns.ncols * NRHS) prefetch_l1(q);
             }
           }
           if (nx2 >= 0) {
@@ -1904,6 +1906,300 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KPara
   }
 }
 
+// ---- Resident sweep.  The planner lays a unit's inputs out
+// as a few contiguous ranges (Phase::u_range): its matrices in the pool, the
+// coefficient slots of its clusters, the near-field partial slots and the
+// permutation entries of its leaves (downward) or its range of x (upward),
+// and its item descriptors.  The CTA copies all of them into shared memory
+// with one batch of TMA bulk copies (one mbarrier), then runs the unit's
+// waves entirely from shared memory -- a wave costs a block barrier and
+// shared-memory latencies, not a chain of cold DRAM misses per item -- and
+// writes x^ (upward; the dataflow launch reads it) or y (finals) to global
+// memory.  With two or three CTAs per SM one unit's copies overlap another's
+// waves, so the sweep is bound by HBM bandwidth.
+constexpr int kSweepXs = 128;  // per-warp source scratch (columns)
+struct SweepGeom {
+  size_t off_v, off_dt, off_ds, off_xs, off_ctl, total;
+};
+__host__ __device__ inline SweepGeom sweep_geom(int nrhs, int nw, int cap_mat, int cap_vec, int cap_items) {
+  auto up = [](size_t v) { return (v + 127) / 128 * 128; };
+  SweepGeom g;
+  g.off_v = up((size_t)(cap_mat + 2) * 8);
+  g.off_dt = g.off_v + up((size_t)(cap_vec + 16) * 8 * nrhs);
+  g.off_ds = g.off_dt + up((size_t)cap_items * sizeof(DTask));
+  g.off_xs = g.off_ds + up((size_t)cap_items * kInlineSegs * sizeof(DSeg));
+  g.off_ctl = g.off_xs + up((size_t)nw * kSweepXs * 8 * nrhs);
+  g.total = g.off_ctl + 128 + 256;
+  return g;
+}
+
+template <int NRHS>
+__global__ void __launch_bounds__(256) h2b_sweep_resident_kernel(KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const SweepGeom G = sweep_geom(NRHS, nw, p.cap_mat, p.cap_vec, p.cap_items);
+  double* Msm = reinterpret_cast<double*>(smem_raw);
+  double* Vsm = reinterpret_cast<double*>(smem_raw + G.off_v);
+  const DTask* DT = reinterpret_cast<const DTask*>(smem_raw + G.off_dt);
+  const DSeg* DS = reinterpret_cast<const DSeg*>(smem_raw + G.off_ds);
+  double* xs = reinterpret_cast<double*>(smem_raw + G.off_xs) + (size_t)wib * kSweepXs * NRHS;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G.off_ctl);
+  // the unit's record (Phase::u_rec) and the next unit's, fetched while this one runs
+  int64_t* rec = reinterpret_cast<int64_t*>(smem_raw + G.off_ctl + 128);  // [2][16]
+  int* next_unit = reinterpret_cast<int*>(smem_raw + G.off_ctl + 16);
+  Ctl* ctl = p.ctl;
+  // first unit: the CTA's index; further units from a counter (starting
+  // behind the grid), the last CTA to leave resets it
+  if (threadIdx.x == 0) {
+    mbar_init(bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    next_unit[0] = (int)blockIdx.x;
+  }
+  if (threadIdx.x < 16 && (int)blockIdx.x < p.nunits) rec[threadIdx.x] = __ldg(p.u_range + 16 * (int64_t)blockIdx.x + threadIdx.x);
+  __syncthreads();
+  unsigned parity = 0;
+  for (int k = 0;; ++k) {
+    const int u = next_unit[k & 1];
+    if (u >= p.nunits) break;
+    const int64_t* R = rec + 16 * (k & 1);
+    const int k0 = (int)(R[8] & 0xffffffff), nit = (int)(R[8] >> 32);
+    const int nwv = (int)R[9];
+    const int32_t* wend = reinterpret_cast<const int32_t*>(R + 10);
+    // ranges, rounded out to 16-byte boundaries (even element offsets)
+    const int64_t m0 = R[0] & ~(int64_t)1, m1 = (R[0] + R[1] + 1) & ~(int64_t)1;
+    const int64_t c0 = (R[2] * NRHS) & ~(int64_t)1, c1 = ((R[2] + R[3]) * NRHS + 1) & ~(int64_t)1;
+    const int64_t b0 = (R[4] * NRHS) & ~(int64_t)1, b1 = ((R[4] + R[5]) * NRHS + 1) & ~(int64_t)1;
+    const int64_t x0 = R[6], xn = R[7];
+    // the V area: [C | B | X or perm]
+    double* Csm = Vsm;
+    double* Bsm = Csm + (c1 - c0) + 2;
+    double* Xsm = Bsm + (b1 - b0) + 2;
+    const bool up_sweep = (R[9] >> 32) != 0;   // planner: 1 in the high word for an upward unit
+    const int64_t xa0 = up_sweep ? (x0 * NRHS) & ~(int64_t)1 : x0 & ~(int64_t)1;
+    // diagnostics: unit timeline in the trace slots of its first item
+    unsigned long long* tr = p.trace ? p.trace + 8 * (int64_t)k0 : nullptr;
+    auto stamp = [&](int j) {
+      if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        tr[j] = t;
+      }
+    };
+    stamp(0);
+    if (threadIdx.x == 0) {
+      const int64_t xa1 = up_sweep ? ((x0 + xn) * NRHS + 1) & ~(int64_t)1 : (x0 + xn + 1) & ~(int64_t)1;
+      const unsigned bm = (unsigned)((m1 - m0) * 8), bc = (unsigned)((c1 - c0) * 8), bb = (unsigned)((b1 - b0) * 8);
+      const unsigned bx = (unsigned)((xa1 - xa0) * 8);
+      const unsigned bt = (unsigned)(nit * sizeof(DTask)), bs = (unsigned)(nit * kInlineSegs * sizeof(DSeg));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(bar, bm + bc + bb + bx + bt + bs);
+      if (bm) bulk_copy(Msm, p.mat + m0, bm, bar);
+      if (bc) bulk_copy(Csm, p.coef + c0, bc, bar);
+      if (bb) bulk_copy(Bsm, p.coef + b0, bb, bar);
+      if (bx) bulk_copy(Xsm, up_sweep ? (const void*)(p.xp + xa0) : (const void*)(p.perm + xa0), bx, bar);
+      bulk_copy(const_cast<DTask*>(DT), p.tasks + k0, bt, bar);
+      bulk_copy(const_cast<DSeg*>(DS), p.seg_inline + (int64_t)k0 * kInlineSegs, bs, bar);
+      // claim the next unit and fetch its record while this one runs
+      const int nu = (int)(atomicAdd(&ctl->static_head, 1u) + gridDim.x);
+      next_unit[(k + 1) & 1] = nu;
+      if (nu < p.nunits) {
+        int64_t* Rn = rec + 16 * ((k + 1) & 1);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) Rn[j] = __ldg(p.u_range + 16 * (int64_t)nu + j);
+      }
+    }
+    stamp(3);
+    mbar_wait(bar, parity);
+    parity ^= 1u;
+    stamp(4);
+    // element (scaled by NRHS) -> pointer: shared memory inside the unit's
+    // ranges, global memory (L2) outside
+    auto coef_ptr = [&](int64_t e, int64_t span) -> const double* {  // e: scaled offset, span: scaled extent read from it
+      if (e >= c0 && e + span <= c1) return Csm + (e - c0);
+      if (e >= b0 && e + span <= b1) return Bsm + (e - b0);
+      return nullptr;
+    };
+    int t0 = 0;
+    for (int wv = 0; wv < nwv; ++wv) {
+      const int t1 = wend[wv];
+      for (int it = t0 + wib; it < t1; it += nw) {
+        const DTask& T = DT[it];
+        const int m = T.m, ld = T.ld, ncols = T.ncols;
+        const int nseg = T.seg1 - T.seg0;
+        const double* A = Msm + (T.data - m0);
+        // lanes: rows rr (and rr + 32 when m > 32); for m <= 16 the columns
+        // are split over 32 / m' lane groups and reduced at the end
+        int mp = 32;
+        if (m <= 16) { mp = 1; while (mp < m) mp <<= 1; }
+        const int Gn = 32 / mp, g = lane / mp, rr = lane - g * mp;
+        double acc0[NRHS], acc1[NRHS];
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) acc0[r] = acc1[r] = 0.0;
+        const bool v0 = rr < m, v1 = (mp == 32) && (rr + 32 < m);
+        for (int col = 0; col < ncols; col += kSweepXs) {
+          const int cc = min(kSweepXs, ncols - col);
+          // sources of columns [col, col + cc): slot sums, through the segments
+          for (int j = lane; j < cc * NRHS; j += 32) {
+            const int c = col + j / NRHS, r = j - (j / NRHS) * NRHS;
+            int sbase = 0, sj = 0;
+            DSeg S = nseg <= kInlineSegs ? DS[it * kInlineSegs] : p.segs[T.seg0];
+            while (sbase + S.ncols <= c) {
+              sbase += S.ncols;
+              ++sj;
+              S = nseg <= kInlineSegs ? DS[it * kInlineSegs + sj] : p.segs[T.seg0 + sj];
+            }
+            const int64_t e = (S.src + (c - sbase)) * NRHS + r;
+            double v = 0.0;
+            if (S.kind == h2b::kSegX) {
+              v = (up_sweep && S.src >= x0 && S.src + S.ncols <= x0 + xn) ? Xsm[e - xa0] : __ldg(p.xp + e);
+            } else {
+              const int64_t st = (int64_t)S.stride * NRHS;
+              const double* q = coef_ptr(e, (int64_t)(S.nslots - 1) * st + 1);
+              if (q) {
+                for (int s2 = 0; s2 < S.nslots; ++s2) v += q[(int64_t)s2 * st];
+              } else {
+                // global (L2): eight slots in flight at a time, added in slot order
+                const double* gq = p.coef + e;
+                int s2 = 0;
+                for (; s2 + 8 <= S.nslots; s2 += 8) {
+                  double t8[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) t8[i] = __ldcg(gq + (int64_t)(s2 + i) * st);
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v += t8[i];
+                }
+                double t8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) t8[i] = (s2 + i < S.nslots) ? __ldcg(gq + (int64_t)(s2 + i) * st) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v += t8[i];
+              }
+            }
+            xs[j] = v;
+          }
+          __syncwarp();
+          // four independent partial sums per row (columns c, c+Gn, c+2Gn,
+          // c+3Gn): the loads of a step are in flight together and the FMA
+          // chains are a quarter as long
+          const double* Ar = A + (int64_t)col * ld + (v0 ? rr : 0);
+          const int step = Gn * ld;
+          double q0[4][NRHS], q1[4][NRHS];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) q0[i][r] = q1[i][r] = 0.0;
+          int c = g;
+          const double* Ap = Ar + (int64_t)g * ld;
+          for (; c + 3 * Gn < cc; c += 4 * Gn, Ap += 4 * step) {
+            double a0[4], a1[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              a0[i] = Ap[i * step];
+              a1[i] = v1 ? Ap[i * step + 32] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int r = 0; r < NRHS; ++r) {
+                const double xv = xs[(c + i * Gn) * NRHS + r];
+                q0[i][r] = fma(a0[i], xv, q0[i][r]);
+                q1[i][r] = fma(a1[i], xv, q1[i][r]);
+              }
+          }
+          for (; c < cc; c += Gn, Ap += step) {
+            const double a0 = Ap[0];
+            const double a1 = v1 ? Ap[32] : 0.0;
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) {
+              const double xv = xs[c * NRHS + r];
+              q0[0][r] = fma(a0, xv, q0[0][r]);
+              q1[0][r] = fma(a1, xv, q1[0][r]);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            acc0[r] += (q0[0][r] + q0[1][r]) + (q0[2][r] + q0[3][r]);
+            acc1[r] += (q1[0][r] + q1[1][r]) + (q1[2][r] + q1[3][r]);
+          }
+          __syncwarp();
+        }
+        if (!v0) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) acc0[r] = 0.0;
+        }
+        if (Gn > 1) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r)
+            for (int o = mp; o < 32; o <<= 1) acc0[r] += __shfl_xor_sync(0xffffffffu, acc0[r], o);
+        }
+        // bias slots (the finals' near-field partial sums), in slot order
+        if (T.bias >= 0) {
+          for (int s2 = 0; s2 < T.bias_nslots; ++s2) {
+            const int64_t e = (T.bias + (int64_t)s2 * T.bias_stride) * NRHS;
+            const double* q = coef_ptr(e, (int64_t)m * NRHS);
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) {
+              if (v0) acc0[r] += q ? q[(int64_t)rr * NRHS + r] : __ldcg(p.coef + e + (int64_t)rr * NRHS + r);
+              if (v1) acc1[r] += q ? q[(int64_t)(rr + 32) * NRHS + r] : __ldcg(p.coef + e + (int64_t)(rr + 32) * NRHS + r);
+            }
+          }
+        }
+        // outputs: y (finals), or the coefficient slot -- in shared memory for
+        // the unit's later waves, and in global memory when a later launch
+        // reads it (x^) or it lies outside the unit's range
+        if (g == 0) {
+          if (T.kind == h2b::kFinal) {
+            const int64_t* pm = reinterpret_cast<const int64_t*>(Xsm) + (T.out - xa0);
+            const bool in = !up_sweep && T.out >= x0 && T.out + m <= x0 + xn;
+            if (v0) {
+              const int64_t node = in ? pm[rr] : __ldg(p.perm + T.out + rr);
+#pragma unroll
+              for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc0[r];
+            }
+            if (v1) {
+              const int64_t node = in ? pm[rr + 32] : __ldg(p.perm + T.out + rr + 32);
+#pragma unroll
+              for (int r = 0; r < NRHS; ++r) p.y[node * NRHS + r] = acc1[r];
+            }
+          } else {
+            const int64_t e = T.out * NRHS;
+            double* q = const_cast<double*>(coef_ptr(e, (int64_t)m * NRHS));
+            const bool glob = q == nullptr || T.kind <= h2b::kUpNode;
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) {
+              if (v0) {
+                if (q) q[(int64_t)rr * NRHS + r] = acc0[r];
+                if (glob) p.coef[e + (int64_t)rr * NRHS + r] = acc0[r];
+              }
+              if (v1) {
+                if (q) q[(int64_t)(rr + 32) * NRHS + r] = acc1[r];
+                if (glob) p.coef[e + (int64_t)(rr + 32) * NRHS + r] = acc1[r];
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();  // the wave's outputs are visible to the CTA's next wave
+      t0 = t1;
+      if (wv < 2) stamp(5 + wv);
+      if (wv == nwv - 2) stamp(7);
+    }
+    stamp(1);
+    if (tr && threadIdx.x == 0) tr[2] = ((unsigned long long)nwv << 32) | blockIdx.x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
+      ctl->static_head = 0;
+      ctl->exited = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace
 
 namespace h2b_detail {
@@ -1933,6 +2229,10 @@ struct PhaseDev {
   int32_t* d_unit0 = nullptr;     // sweeps
   int32_t* d_wave0 = nullptr;
   int32_t nunits = 0;
+  int64_t bytes = 0;              // matrix bytes its items stream
+  int64_t* d_u_range = nullptr;   // resident sweeps
+  bool resident = false;
+  int cap_mat = 0, cap_vec = 0, cap_items = 0;
 };
 
 struct h2b_op {
@@ -1943,6 +2243,8 @@ struct h2b_op {
   int wpc = 8;
   int grid[5] = {0, 0, 0, 0, 0};  // per NRHS template 1,2,4,8,16
   int sweep_grid[5] = {0, 0, 0, 0, 0};
+  int sweep_resident = 1;   // H2B_SWEEP_RESIDENT=0: always the generic sweep kernel (A/B switch)
+  int smem_optin = 0, nsm = 0;
   double* d_mat = nullptr;
   double* d_coef = nullptr;
   int64_t* d_perm = nullptr;
@@ -1981,6 +2283,8 @@ struct h2b_op {
   // stream either ran on; `mu` serialises the host side.
   cudaEvent_t done = nullptr;
   std::mutex mu;
+  std::vector<cudaEvent_t>* tev = nullptr;  // h2b_launch_times: events of the product being timed
+  int tev_n = 0;
   h2b_stats stats{};
 };
 
@@ -2027,6 +2331,10 @@ bool streaming_defaults(const h2b_desc* d, const h2b_options* o) {
 
 h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
   h2b::PlanOptions po;
+  // the staged product (sweeps over the bottom subtrees around one dataflow
+  // launch) by default: config 1 60 -> 52 us, config 2 0.209 -> 0.177 ms,
+  // config 3 2.366 -> 2.295 ms, 2 / 4 right-hand sides -8..-15 %
+  po.staged = true;
   // the level-skipping chain where the product is chain-bound: operators
   // (or rank shards) below 4 GiB of near-field and coupling bytes
   // (config 1 -6 %, config 2 -3.5 %, config 3 at 8 ranks -7 %; config 3 on
@@ -2086,6 +2394,8 @@ void fill_stats(const h2b::Plan& P, h2b_stats* s) {
   s->world_size = P.world_size;
   s->local_bytes = P.local_bytes;
   s->extra_bytes = P.extra_bytes;
+  s->launches = (int32_t)P.ph.size();
+  s->resident_mask = 0;
 }
 
 int nrhs_index(int nrhs) {
@@ -2171,6 +2481,10 @@ KParams phase_params(h2b_op* op, const PhaseDev& F, double* y) {
   p.unit0 = F.d_unit0;
   p.wave0 = F.d_wave0;
   p.nunits = F.nunits;
+  p.u_range = F.d_u_range;
+  p.cap_mat = F.cap_mat;
+  p.cap_vec = F.cap_vec;
+  p.cap_items = F.cap_items;
   return p;
 }
 
@@ -2195,11 +2509,32 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) 
   return H2B_OK;
 }
 
-// One sweep launch (Phase::mode 1): a CTA per unit, round robin.
+// One sweep launch (Phase::mode 1): CTAs claim units from a counter.  The
+// resident kernel when every unit's inputs are contiguous ranges that fit a
+// CTA's shared memory at this NRHS (at least two CTAs per SM preferred),
+// else the generic one.
 template <int NRHS>
 int launch_sweep(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) {
   if (F.ntasks == 0 || F.nunits == 0) return H2B_OK;
   const KParams p = phase_params<NRHS>(op, F, y);
+  if (F.resident && op->sweep_resident) {
+    const size_t smem = sweep_geom(NRHS, op->wpc, F.cap_mat, F.cap_vec, F.cap_items).total;
+    if (smem <= (size_t)op->smem_optin) {
+      H2B_CUDA(cudaFuncSetAttribute(h2b_sweep_resident_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      int per_sm = 0;
+      H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_sweep_resident_kernel<NRHS>, op->wpc * 32,
+                                                             smem));
+      if (per_sm >= 1) {
+        const int grid = std::min<int>(per_sm * op->nsm, F.nunits);
+        h2b_sweep_resident_kernel<NRHS><<<grid, op->wpc * 32, smem, st>>>(p);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+          return fail(H2B_ECUDA, std::string("resident sweep kernel launch: ") + cudaGetErrorString(e));
+        return H2B_OK;
+      }
+    }
+  }
   const size_t smem = sweep_smem_bytes(op->wpc);
   H2B_CUDA(cudaFuncSetAttribute(h2b_sweep_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int gi = nrhs_index(NRHS);
@@ -2267,9 +2602,20 @@ template <int NRHS>
 int launch_group(h2b_op* op, int group, const double* x, double* y, cudaStream_t st) {
   const std::vector<PhaseDev>& list = (NRHS >= 8 && !op->ph_split.empty()) ? op->ph_split : op->ph;
   int rc = H2B_OK;
-  if (group == 0 && (rc = launch_permute<NRHS>(op, x, st)) != H2B_OK) return rc;
+  // (h2b_launch_times: an event before every launch and after the last)
+  auto mark = [&]() {
+    if (op->tev && op->tev_n < (int)op->tev->size()) cudaEventRecord((*op->tev)[op->tev_n++], st);
+  };
+  if (group == 0) {
+    mark();
+    if ((rc = launch_permute<NRHS>(op, x, st)) != H2B_OK) return rc;
+  }
   for (const PhaseDev& F : list)
-    if (F.group == group && (rc = launch_one<NRHS>(op, F, y, st)) != H2B_OK) return rc;
+    if (F.group == group) {
+      mark();
+      if ((rc = launch_one<NRHS>(op, F, y, st)) != H2B_OK) return rc;
+    }
+  mark();
   return H2B_OK;
 }
 
@@ -2308,6 +2654,7 @@ void free_phase(PhaseDev& F) {
   cudaFree(F.d_trace);
   cudaFree(F.d_unit0);
   cudaFree(F.d_wave0);
+  cudaFree(F.d_u_range);
 }
 
 void free_op(h2b_op* op) {
@@ -2334,10 +2681,16 @@ int upload_phase(const h2b::Phase& P, PhaseDev* F) {
   F->nnodes = P.nnodes;
   F->mode = P.mode;
   F->group = P.group;
+  for (int64_t i = 0; i < P.ntasks(); ++i) F->bytes += 8 * (int64_t)P.t_m[i] * P.t_ncols[i];
   if (P.mode == 1) {
     if ((rc = upload(&F->d_unit0, P.unit0.data(), P.unit0.size()))) return rc;
     if ((rc = upload(&F->d_wave0, P.wave0.data(), P.wave0.size()))) return rc;
     F->nunits = (int32_t)P.unit0.size() - 1;
+    if ((rc = upload(&F->d_u_range, P.u_rec.data(), P.u_rec.size()))) return rc;
+    F->resident = P.resident && P.res_mat_max < (1 << 20) && P.res_vec_max < (1 << 20);
+    F->cap_mat = (int)P.res_mat_max;
+    F->cap_vec = (int)P.res_vec_max;
+    F->cap_items = P.res_items_max;
   }
   std::vector<DTask> tasks(P.ntasks());
   for (int64_t i = 0; i < P.ntasks(); ++i) {
@@ -2552,10 +2905,14 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->ph_split.resize(P.ph_split.size());
   for (size_t k = 0; k < P.ph_split.size(); ++k)
     if ((rc = upload_phase(P.ph_split[k], &op->ph_split[k]))) return rc;
-  if ((rc = upload(&op->d_perm, P.perm.data(), P.perm.size()))) return rc;
+  // (+2 entries: the resident sweeps' bulk copies round ranges out to 16 bytes)
+  if ((rc = upload<int64_t>(&op->d_perm, nullptr, P.perm.size() + 2))) return rc;
+  H2B_CUDA(cudaMemset(op->d_perm, 0, sizeof(int64_t) * (P.perm.size() + 2)));
+  H2B_CUDA(cudaMemcpy(op->d_perm, P.perm.data(), sizeof(int64_t) * P.perm.size(), cudaMemcpyHostToDevice));
   if ((rc = upload(&op->d_rank_lo, P.rank_lo.data(), P.rank_lo.size()))) return rc;
-  if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs))) return rc;
-  if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs))) return rc;
+  if ((rc = upload<double>(&op->d_coef, nullptr, (size_t)std::max<int64_t>(1, P.coef_len) * op->max_nrhs + 2))) return rc;
+  if ((rc = upload<double>(&op->d_xp, nullptr, (size_t)P.n * op->max_nrhs + 2))) return rc;
+  H2B_CUDA(cudaMemset(op->d_xp, 0, sizeof(double) * ((size_t)P.n * op->max_nrhs + 2)));
   H2B_CUDA(cudaMemset(op->d_coef, 0, sizeof(double) * std::max<int64_t>(1, P.coef_len) * op->max_nrhs));
 
   if ((rc = occupancy_grid<1>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[0]))) return rc;
@@ -2563,6 +2920,12 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[2]))) return rc;
   if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[3]))) return rc;
   if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[4]))) return rc;
+  H2B_CUDA(cudaDeviceGetAttribute(&op->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
+  H2B_CUDA(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, op->device));
+  {
+    const char* sr = std::getenv("H2B_SWEEP_RESIDENT");
+    op->sweep_resident = !(sr && sr[0] == '0');
+  }
   if ((rc = sweep_grid<1>(op->wpc, &op->sweep_grid[0]))) return rc;
   if ((rc = sweep_grid<2>(op->wpc, &op->sweep_grid[1]))) return rc;
   if ((rc = sweep_grid<4>(op->wpc, &op->sweep_grid[2]))) return rc;
@@ -2607,6 +2970,15 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   op->stats.warps_per_cta = op->wpc;
   op->stats.sched_flags = op->sched;
   op->stats.ring_warps = op->ring_warps;
+  for (int i = 0; i < 5 && op->sweep_resident; ++i) {
+    bool all = false;
+    for (const auto& F : ((1 << i) >= 8 && !op->ph_split.empty()) ? op->ph_split : op->ph) {
+      if (F.mode != 1 || F.nunits == 0) continue;
+      all = F.resident && sweep_geom(1 << i, op->wpc, F.cap_mat, F.cap_vec, F.cap_items).total <= (size_t)op->smem_optin;
+      if (!all) break;
+    }
+    if (all) op->stats.resident_mask |= 1 << i;
+  }
   *out = op.release();
   return H2B_OK;
 }
@@ -2708,7 +3080,11 @@ void fill_view(const h2b::Plan& P, const h2b::Phase& F, h2b_plan_view* v) {
   v->mode = F.mode;
   v->group = F.group;
   v->split = 0;
-  v->reserved_ = 0;
+  v->resident = F.resident ? 1 : 0;
+  v->u_range = F.u_range.data();
+  v->res_mat_max = F.res_mat_max;
+  v->res_vec_max = F.res_vec_max;
+  v->res_items_max = F.res_items_max;
   v->nunits = F.mode == 1 ? (int64_t)F.unit0.size() - 1 : 0;
   v->nwaves = F.mode == 1 ? (int64_t)F.wave0.size() - 1 : 0;
   v->unit0 = F.unit0.data();
@@ -2909,6 +3285,60 @@ int h2b_item_kinds(const h2b_op* op, int32_t* out, int64_t nitems) {
   std::vector<DTask> t(nitems);
   H2B_CUDA(cudaMemcpy(t.data(), traced_phase(op).d_tasks, sizeof(DTask) * nitems, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < nitems; ++i) out[i] = t[i].kind;
+  return H2B_OK;
+}
+
+int h2b_launch_count(const h2b_op* op, int nrhs) {
+  if (!op || nrhs_index(nrhs) < 0) return -1;
+  const auto& list = (nrhs >= 8 && !op->ph_split.empty()) ? op->ph_split : op->ph;
+  return 1 + (int)list.size();
+}
+
+int h2b_launch_info(const h2b_op* op, int nrhs, int launch, int32_t* kind, int64_t* items, int64_t* bytes) {
+  const int n = h2b_launch_count(op, nrhs);
+  if (n < 0 || launch < 0 || launch >= n || !kind || !items || !bytes) return fail(H2B_EINVAL, "bad launch index");
+  if (launch == 0) {
+    *kind = -1;
+    *items = op->n;
+    *bytes = 0;
+    return H2B_OK;
+  }
+  const auto& list = (nrhs >= 8 && !op->ph_split.empty()) ? op->ph_split : op->ph;
+  const PhaseDev& F = list[launch - 1];
+  *kind = F.mode;
+  *items = F.ntasks;
+  *bytes = F.bytes;
+  return H2B_OK;
+}
+
+int h2b_launch_times(h2b_op* op, const double* x_dev, double* y_dev, int nrhs, int steps, void* stream,
+                     double* ms_per_launch) {
+  if (!op || !ms_per_launch || steps < 1) return fail(H2B_EINVAL, "bad argument");
+  if (op->world > 1) return fail(H2B_EINVAL, "h2b_launch_times: single-GPU operators only");
+  const int n = h2b_launch_count(op, nrhs);
+  if (n < 0) return fail(H2B_EINVAL, "nrhs must be 1, 2, 4, 8 or 16");
+  std::lock_guard<std::mutex> lk(op->mu);
+  H2B_CUDA(cudaSetDevice(op->device));
+  std::vector<cudaEvent_t> ev((size_t)n + 1, nullptr);
+  for (auto& e : ev) H2B_CUDA(cudaEventCreate(&e));
+  std::vector<double> acc((size_t)n, 0.0);
+  int rc = H2B_OK;
+  for (int s = 0; s < steps && rc == H2B_OK; ++s) {
+    op->tev = &ev;
+    op->tev_n = 0;
+    rc = matvec_locked(op, -1, x_dev, y_dev, nrhs, stream);
+    op->tev = nullptr;
+    if (rc != H2B_OK) break;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) { rc = fail(H2B_ECUDA, "synchronize"); break; }
+    for (int k = 0; k < n; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      acc[k] += ms;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != H2B_OK) return rc;
+  for (int k = 0; k < n; ++k) ms_per_launch[k] = acc[k] / steps;
   return H2B_OK;
 }
 

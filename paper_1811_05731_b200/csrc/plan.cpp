@@ -15,6 +15,8 @@
 #include <queue>
 #include <unordered_map>
 #include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -78,6 +80,7 @@ class Builder {
   // staged plans: root of the bottom subtree containing each cluster, or -1
   // for the clusters above the subtrees ("top")
   std::vector<int32_t> broot_;
+  std::vector<std::vector<int32_t>> units_;  // clusters of every bottom subtree (preorder), roots in tree order
   bool top(int32_t c) const { return broot_.empty() || broot_[c] < 0; }
   void mark_bottom_subtrees();
   // a sweep phase from provisional task ids: units by bottom subtree (tree
@@ -86,6 +89,8 @@ class Builder {
   std::vector<Vec> xhat_, yhat_, nearv_;
   std::vector<TaskTmp> tasks_;
   int32_t cur_cl_ = 0;  // cluster of the group being emitted
+  int32_t cur_region_ = 0;  // Group::region / unit of the group being emitted
+  int64_t cur_unit_ = 0;
   // finish one phase from provisional task ids (any order); deps outside
   // `in_phase` are dropped (satisfied before the phase starts)
   int finalize(Phase* F, std::vector<int32_t> ids, const std::vector<char>& in_phase, std::string* err);
@@ -121,7 +126,7 @@ class Builder {
   // Packs the group's matrix, splits it into pieces, emits tasks.
   void emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
                   Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split, int32_t qclass = 0,
-                  bool seg0_hi = false);
+                  bool seg0_hi = false, bool append = false);
   void collect_leaves(int32_t c, std::vector<int32_t>* out) const {
     if (is_leaf(c)) { out->push_back(c); return; }
     collect_leaves((int32_t)d_->cl_child[2 * c], out);
@@ -223,7 +228,7 @@ int Builder::validate(std::string* err) {
 
 void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vector<SegSpec>& segs,
                          Vec* outv, int64_t y_pos, const Vec* bias, bool allow_split, int32_t qclass,
-                         bool seg0_hi) {
+                         bool seg0_hi, bool append) {
   Plan& P = *plan_;
   if (m_total <= 0) return;
   // 1. the group matrix (m_total x C, column-major, ld = m_total): recorded,
@@ -235,6 +240,8 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
     Group g;
     g.m = m_total;
     g.ncols = C;
+    g.region = cur_region_;
+    g.unit = cur_unit_;
     for (auto& s : segs) g.segs.push_back({s.a, s.ncols, s.transpose, s.a_ld});
     P.groups.push_back(std::move(g));
   }
@@ -274,8 +281,18 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
     }
   }
   if (cur.ncols > 0 || pieces.empty()) pieces.push_back(cur);
-  // 3. output vector
-  if (outv) alloc_vec(outv, m_total, (int32_t)pieces.size());
+  // 3. output vector (`append`: further slots right behind the ones it has)
+  int32_t slot0 = 0;
+  if (outv) {
+    if (append && outv->exists() && outv->len == m_total &&
+        outv->off + (int64_t)outv->len * outv->nslots == plan_->coef_len) {
+      slot0 = outv->nslots;
+      outv->nslots += (int32_t)pieces.size();
+      plan_->coef_len += (int64_t)m_total * (int64_t)pieces.size();
+    } else {
+      alloc_vec(outv, m_total, (int32_t)pieces.size());
+    }
+  }
   // 4. tasks: one per (piece, row tile)
   for (size_t pi = 0; pi < pieces.size(); ++pi) {
     const Piece& pc = pieces[pi];
@@ -311,7 +328,7 @@ void Builder::emit_group(int32_t kind, int32_t stage, int32_t m_total, std::vect
       t.ncols = (int32_t)pc.ncols;
       t.kind = kind;
       t.stage = stage;
-      t.out = outv ? outv->off + (int64_t)pi * m_total + r0 : y_pos + r0;
+      t.out = outv ? outv->off + (int64_t)(slot0 + (int32_t)pi) * m_total + r0 : y_pos + r0;
       if (bias && bias->exists()) {
         t.bias = bias->off + r0;
         t.bias_nslots = bias->nslots;
@@ -365,47 +382,70 @@ int Builder::run(std::string* err) {
   yhat_.assign(nc, Vec());
   nearv_.assign(nc, Vec());
 
-  // ---- forward, leaves: x^_t = W_t^T x|_t (h2.py:199-200)
-  for (int32_t c : leaves_) {
+  // ---- forward (h2.py:195-209).  Staged plans emit the bottom subtrees one
+  // after another (leaves, then inner clusters by height), so that a unit's
+  // matrices and x^ vectors are contiguous; then the clusters above them.
+  auto emit_up_leaf = [&](int32_t c) {   // x^_t = W_t^T x|_t (h2.py:199-200)
     int32_t k = (int32_t)d->k_col[c];
-    if (k == 0) continue;
+    if (k == 0) return;
     std::vector<SegSpec> segs{{kSegX, d->cl_start[c], (int32_t)size(c), nullptr, d->col_basis[c], false, 0}};
     cur_cl_ = c;
     emit_group(kUpLeaf, 0, k, segs, &xhat_[c], 0, nullptr, true);
+  };
+  auto emit_up_node = [&](int32_t p) {   // x^_p = sum_c F_c^T x^_c (h2.py:201-205)
+    int32_t k = (int32_t)d->k_col[p];
+    if (k == 0) return;
+    std::vector<SegSpec> segs;
+    // (staged plans: only above the bottom subtrees, whose levels are
+    // separated by block barriers, not by scheduling links)
+    const bool skip = opt_.skip_levels && height_[p] >= 2 && height_[p] % 2 == 0 && top(p);
+    for (int j = 0; j < 2; ++j) {
+      int32_t ch = (int32_t)d->cl_child[2 * p + j];
+      if (skip && !is_leaf(ch)) {
+        // x^_p += (F_g F_ch)^T x^_g over the grandchildren g (h2.py:201-205 expanded)
+        const int64_t kc = d->k_col[ch];
+        if (kc == 0) continue;
+        for (int jj = 0; jj < 2; ++jj) {
+          const int32_t g = (int32_t)d->cl_child[2 * ch + jj];
+          if (!xhat_[g].exists()) continue;
+          const int64_t kg = d->k_col[g];
+          const double* fg = product(d->col_transfer[g], d->col_transfer[ch], kg, kc, k);
+          segs.push_back({kSegCoef, 0, (int32_t)kg, &xhat_[g], fg, false, 0});
+        }
+        continue;
+      }
+      if (!xhat_[ch].exists()) continue;
+      segs.push_back({kSegCoef, 0, (int32_t)d->k_col[ch], &xhat_[ch], d->col_transfer[ch], false, 0});
+    }
+    cur_cl_ = p;
+    emit_group(kUpNode, height_[p], k, segs, &xhat_[p], 0, nullptr, true);
+  };
+  // the clusters of every bottom subtree (preorder), in tree order of the roots
+  std::vector<std::vector<int32_t>>& units = units_;
+  if (opt_.staged)
+    for (int32_t c : order_) {
+      if (broot_[c] == c) units.emplace_back();
+      if (broot_[c] >= 0) units.back().push_back(c);
+    }
+  for (auto& sub : units) {
+    cur_region_ = 1;
+    cur_unit_ = d->cl_start[sub[0]];
+    std::vector<int32_t> inner;
+    for (int32_t c : sub) {
+      if (is_leaf(c)) emit_up_leaf(c);
+      else inner.push_back(c);
+    }
+    std::stable_sort(inner.begin(), inner.end(), [&](int32_t a, int32_t b) { return height_[a] < height_[b]; });
+    for (int32_t p : inner) emit_up_node(p);
   }
-  // ---- forward, inner clusters bottom-up: x^_p = sum_c F_c^T x^_c (h2.py:201-205)
+  cur_region_ = 0;
+  cur_unit_ = 0;
+  for (int32_t c : leaves_) if (top(c)) emit_up_leaf(c);
   {
     std::vector<int32_t> inner;
-    for (int32_t c = 0; c < nc; ++c) if (!is_leaf(c)) inner.push_back(c);
+    for (int32_t c = 0; c < nc; ++c) if (!is_leaf(c) && top(c)) inner.push_back(c);
     std::stable_sort(inner.begin(), inner.end(), [&](int32_t a, int32_t b) { return height_[a] < height_[b]; });
-    for (int32_t p : inner) {
-      int32_t k = (int32_t)d->k_col[p];
-      if (k == 0) continue;
-      std::vector<SegSpec> segs;
-      // (staged plans: only above the bottom subtrees, whose levels are
-      // separated by block barriers, not by scheduling links)
-      const bool skip = opt_.skip_levels && height_[p] >= 2 && height_[p] % 2 == 0 && top(p);
-      for (int j = 0; j < 2; ++j) {
-        int32_t ch = (int32_t)d->cl_child[2 * p + j];
-        if (skip && !is_leaf(ch)) {
-          // x^_p += (F_g F_ch)^T x^_g over the grandchildren g (h2.py:201-205 expanded)
-          const int64_t kc = d->k_col[ch];
-          if (kc == 0) continue;
-          for (int jj = 0; jj < 2; ++jj) {
-            const int32_t g = (int32_t)d->cl_child[2 * ch + jj];
-            if (!xhat_[g].exists()) continue;
-            const int64_t kg = d->k_col[g];
-            const double* fg = product(d->col_transfer[g], d->col_transfer[ch], kg, kc, k);
-            segs.push_back({kSegCoef, 0, (int32_t)kg, &xhat_[g], fg, false, 0});
-          }
-          continue;
-        }
-        if (!xhat_[ch].exists()) continue;
-        segs.push_back({kSegCoef, 0, (int32_t)d->k_col[ch], &xhat_[ch], d->col_transfer[ch], false, 0});
-      }
-      cur_cl_ = p;
-      emit_group(kUpNode, height_[p], k, segs, &xhat_[p], 0, nullptr, true);
-    }
+    for (int32_t p : inner) emit_up_node(p);
   }
   // ---- near field, grouped by target leaf (h2.py:237-240).  Blocks whose
   // row cluster is not a leaf are split into their leaf row ranges.
@@ -443,13 +483,13 @@ int Builder::run(std::string* err) {
     // through E_c E_p plus E_c times that own sum:
     //   y^_c = E_c (E_p y^_gp + y^_p,own) + y^_c,own       (h2.py:220-235)
     std::vector<char> own_only(nc, 0);
-    for (int32_t t : order) {
+    auto emit_down = [&](int32_t t) {
       int32_t k = (int32_t)d->k_row[t];
       // odd heights (counted from the leaves, so the leaves skip their
       // parent's level), never two "own" levels in a row
       if (t != 0 && opt_.skip_levels && !is_leaf(t) && height_[t] % 2 == 1 && !own_only[parent_[t]] && top(t))
         own_only[t] = 1;
-      if (k == 0) continue;
+      if (k == 0) return;
       std::vector<SegSpec> segs;
       bool transfer = false;
       if (t != 0 && !own_only[t]) {
@@ -478,10 +518,31 @@ int Builder::run(std::string* err) {
         int64_t ks = d->k_col[s];
         segs.push_back({kSegCoef, 0, (int32_t)ks, &xhat_[s], d->cp_data[b], true, ks});
       }
-      if (segs.empty()) continue;  // coefficient stays None (h2.py:224-226)
+      if (segs.empty()) return;  // coefficient stays None (h2.py:224-226)
       cur_cl_ = t;
-      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, is_leaf(t) ? 2 : 1, transfer);
+      const int32_t qc = is_leaf(t) ? 2 : 1;
+      if (!top(t) && transfer) {
+        // a bottom cluster's transfer is an item of the downward sweep: a
+        // matrix of its own (laid out with its unit's), writing slot 0 of
+        // y^_t; the coupling rows append their slots behind it
+        std::vector<SegSpec> xfer{segs[0]};
+        std::vector<SegSpec> rest(segs.begin() + 1, segs.end());
+        cur_region_ = 2;
+        emit_group(kDown, depth_[t], k, xfer, &yhat_[t], 0, nullptr, true, qc, true);
+        cur_region_ = 0;
+        if (!rest.empty()) emit_group(kDown, depth_[t], k, rest, &yhat_[t], 0, nullptr, true, qc, false, true);
+        return;
+      }
+      emit_group(kDown, depth_[t], k, segs, &yhat_[t], 0, nullptr, true, qc, transfer);
+    };
+    for (int32_t t : order) if (top(t)) emit_down(t);
+    for (auto& sub : units) {
+      cur_unit_ = d->cl_start[sub[0]];
+      std::vector<int32_t> by_depth(sub);
+      std::stable_sort(by_depth.begin(), by_depth.end(), [&](int32_t a, int32_t b) { return depth_[a] < depth_[b]; });
+      for (int32_t t : by_depth) emit_down(t);
     }
+    cur_unit_ = 0;
   }
   // ---- leaf back-transform + near partials -> y (h2.py:227-229, 242-243)
   for (int32_t l : leaves_) {
@@ -490,7 +551,32 @@ int Builder::run(std::string* err) {
     if (k > 0 && yhat_[l].exists())
       segs.push_back({kSegCoef, 0, k, &yhat_[l], d->row_basis[l], true, k});
     cur_cl_ = l;
+    if (opt_.staged) { cur_region_ = 2; cur_unit_ = d->cl_start[broot_[l]]; }
     emit_group(kFinal, 0, (int32_t)size(l), segs, nullptr, d->cl_start[l], &nearv_[l], false, opt_.final_class);
+  }
+  cur_region_ = 0;
+  cur_unit_ = 0;
+  // Staged plans: the pool region by region -- the upward sweep's units, the
+  // dataflow launch's matrices, the downward sweep's units (transfers and
+  // leaf bases of a unit together)
+  if (opt_.staged) {
+    const size_t G = P.groups.size();
+    std::vector<int32_t> perm_g(G);
+    std::iota(perm_g.begin(), perm_g.end(), 0);
+    auto key = [&](int32_t g) { return P.groups[g].region == 1 ? 0 : P.groups[g].region == 0 ? 1 : 2; };
+    std::stable_sort(perm_g.begin(), perm_g.end(), [&](int32_t a, int32_t b) {
+      if (key(a) != key(b)) return key(a) < key(b);
+      return key(a) == 2 && P.groups[a].unit < P.groups[b].unit;
+    });
+    std::vector<int32_t> new_id(G);
+    std::vector<Group> sorted;
+    sorted.reserve(G);
+    for (size_t k2 = 0; k2 < G; ++k2) {
+      new_id[perm_g[k2]] = (int32_t)k2;
+      sorted.push_back(std::move(P.groups[perm_g[k2]]));
+    }
+    P.groups.swap(sorted);
+    for (auto& t : tasks_) t.group = new_id[t.group];
   }
   // Entries never read by the product (e.g. row bases of an operator
   // without coupling blocks) are not packed, so the pool can be smaller.
@@ -515,21 +601,24 @@ int Builder::run(std::string* err) {
   };
   // the launches of one group of selected items: [up sweep] dataflow [down
   // sweep]; with `split` the near field gets a launch of its own (mode 2)
+  // (the split multi-RHS product keeps every far-field item in its dataflow
+  // launch: sweeps of 8/16 right-hand sides run one CTA per SM and measured
+  // slower, 16 RHS on config 3 4.57 -> 5.09 ms)
   auto emit_launches = [&](std::vector<Phase>* out, const std::vector<char>& in, int32_t group, bool split) -> int {
     std::vector<int32_t> up, dn, near, rest;
     std::vector<char> in_near(T, 0), in_rest(T, 0);
     for (int32_t i = 0; i < T; ++i) {
       if (!in[i]) continue;
       const TaskTmp& t = tasks_[i];
-      if (in_up_sweep(t)) up.push_back(i);
-      else if (in_down_sweep(t)) dn.push_back(i);
+      if (!split && in_up_sweep(t)) up.push_back(i);
+      else if (!split && in_down_sweep(t)) dn.push_back(i);
       else if (split && t.kind == kNear) { near.push_back(i); in_near[i] = 1; }
       else { rest.push_back(i); in_rest[i] = 1; }
     }
     // closure: the dataflow launch must not wait for an item of the down sweep
     for (int32_t i : rest)
       for (int32_t dp : tasks_[i].deps)
-        if (in[dp] && in_down_sweep(tasks_[dp])) { *err = "internal: dataflow item depends on the down sweep"; return H2B_EINVAL; }
+        if (!split && in[dp] && in_down_sweep(tasks_[dp])) { *err = "internal: dataflow item depends on the down sweep"; return H2B_EINVAL; }
     int rc2 = H2B_OK;
     if (!up.empty()) {
       out->emplace_back();
@@ -680,6 +769,9 @@ int Builder::run(std::string* err) {
     }
     for (size_t k = 0; k < s_src_.size(); ++k)
       if (s_kind_[k] == kSegCoef) s_src_[k] = map(s_src_[k]);
+    for (auto* vs : {&xhat_, &yhat_, &nearv_})
+      for (auto& v : *vs)
+        if (v.exists()) v.off = map(v.off);
     P.coef_len = nxt;
     P.exch_off = 0;
     P.exch_count = rsz;
@@ -712,7 +804,7 @@ int Builder::run(std::string* err) {
 void Builder::mark_bottom_subtrees() {
   const h2b_desc* d = d_;
   const int64_t nc = d->nclusters;
-  int64_t S = opt_.sweep_nodes > 0 ? opt_.sweep_nodes : 1024;
+  int64_t S = opt_.sweep_nodes > 0 ? opt_.sweep_nodes : 128;
   auto mark = [&](int64_t cap) -> int64_t {
     broot_.assign(nc, -1);
     int64_t roots = 0;
@@ -724,6 +816,16 @@ void Builder::mark_bottom_subtrees() {
     return roots;
   };
   int64_t roots = mark(S);
+  // Default size: about 256 subtrees per rank (one per resident CTA of the
+  // sweep kernels, so that a sweep is one round of similar units and their
+  // leaf waves keep every warp busy): measured best on configs 2 and 3 on
+  // one GPU and on config 3 split over 8 ranks.
+  if (opt_.sweep_nodes <= 0) {
+    const int64_t per = d->n / (256 * (int64_t)std::max(1, opt_.world_size));
+    S = 128;
+    while (S < per && S < 16384) S *= 2;
+    roots = mark(S);
+  }
   // multi-GPU: ranks own whole subtrees, so there must be enough of them to
   // balance the ranks' bytes
   const int64_t want = opt_.world_size > 1 ? std::min<int64_t>(8 * (int64_t)opt_.world_size, (int64_t)leaves_.size()) : 1;
@@ -792,6 +894,76 @@ int Builder::finalize_sweep(Phase* F, const std::vector<int32_t>& ids, std::stri
   F->unit0.push_back((int32_t)F->wave0.size());
   F->wave0.push_back(T);
   F->nnodes = (int64_t)F->unit0.size() - 1;
+  // Resident form: per unit the contiguous ranges its CTA copies into shared
+  // memory -- matrices, main coefficients (x^ / y^ slots of its clusters),
+  // near-field partial slots of its leaves, its x range.
+  {
+    const int64_t U = F->nnodes;
+    F->u_range.assign((size_t)(8 * U), 0);
+    F->resident = U > 0;
+    std::unordered_map<int32_t, const std::vector<int32_t>*> sub_of;
+    for (const auto& sub : units_) sub_of[sub[0]] = &sub;
+    const bool up = T > 0 && F->t_kind[0] <= kUpNode;
+    for (int64_t u = 0; u < U; ++u) {
+      const int32_t k0 = F->wave0[F->unit0[u]], k1 = F->wave0[F->unit0[u + 1]];
+      const int32_t root = broot_[tasks_[sorted[k0]].cl];
+      // matrices: the groups of the unit's items
+      int64_t lo = INT64_MAX, hi = -1, sum = 0;
+      std::vector<int32_t> gs;
+      for (int32_t k = k0; k < k1; ++k) gs.push_back(tasks_[sorted[k]].group);
+      std::sort(gs.begin(), gs.end());
+      gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+      for (int32_t g : gs) {
+        const Group& G = plan_->groups[g];
+        if (G.base < 0) { F->resident = false; continue; }
+        lo = std::min(lo, G.base); hi = std::max(hi, G.base + G.size()); sum += G.size();
+      }
+      if (hi < 0) { lo = hi = 0; }
+      if (sum != hi - lo) {
+        if (F->resident && std::getenv("H2B_DEBUG_PLAN"))
+          std::fprintf(stderr, "[plan] unit %lld (%s): matrices not contiguous (%lld of %lld)\n", (long long)u,
+                       up ? "up" : "down", (long long)sum, (long long)(hi - lo));
+        F->resident = false;
+      }
+      int64_t* R = &F->u_range[(size_t)(8 * u)];
+      R[0] = lo; R[1] = hi - lo;
+      // coefficient ranges of the subtree's clusters
+      auto hull = [&](const std::vector<Vec>& vs, bool leaves_only, int64_t* out) {
+        int64_t a = INT64_MAX, b = -1, tot = 0;
+        for (int32_t c : *sub_of.at(root)) {
+          const Vec& v = vs[c];
+          if (!v.exists() || (leaves_only && !is_leaf(c))) continue;
+          const int64_t len = (int64_t)v.len * v.nslots;
+          a = std::min(a, v.off); b = std::max(b, v.off + len); tot += len;
+        }
+        if (b < 0) { out[0] = out[1] = 0; return; }
+        if (tot != b - a) {
+          if (F->resident && std::getenv("H2B_DEBUG_PLAN"))
+            std::fprintf(stderr, "[plan] unit %lld (%s): %s not contiguous (%lld of %lld)\n", (long long)u,
+                         up ? "up" : "down", leaves_only ? "partials" : "coefficients", (long long)tot, (long long)(b - a));
+          F->resident = false;
+        }
+        out[0] = a; out[1] = b - a;
+      };
+      hull(up ? xhat_ : yhat_, false, R + 2);
+      if (!up) hull(nearv_, true, R + 4);
+      R[6] = d_->cl_start[root]; R[7] = d_->cl_end[root] - d_->cl_start[root];  // x (upward) / perm (downward)
+      {
+        const int32_t nwv = F->unit0[u + 1] - F->unit0[u];
+        if (nwv > 12) F->resident = false;
+        if ((int64_t)F->u_rec.size() < 16 * U) F->u_rec.assign((size_t)(16 * U), 0);
+        int64_t* Q = &F->u_rec[(size_t)(16 * u)];
+        for (int j = 0; j < 8; ++j) Q[j] = R[j];
+        Q[8] = (int64_t)k0 | ((int64_t)(k1 - k0) << 32);
+        Q[9] = (int64_t)nwv | ((int64_t)(up ? 1 : 0) << 32);
+        int32_t* we = reinterpret_cast<int32_t*>(Q + 10);
+        for (int32_t j = 0; j < std::min(nwv, 12); ++j) we[j] = F->wave0[F->unit0[u] + j + 1] - k0;
+      }
+      F->res_mat_max = std::max(F->res_mat_max, R[1]);
+      F->res_vec_max = std::max(F->res_vec_max, R[3] + R[5] + R[7]);
+      F->res_items_max = std::max(F->res_items_max, k1 - k0);
+    }
+  }
   return H2B_OK;
 }
 

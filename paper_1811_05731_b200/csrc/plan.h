@@ -82,6 +82,21 @@ struct Phase {
   // [wave0[w], wave0[w+1]) of the queue (a unit's items are contiguous and
   // form one fused run: t_mlen = its length at its first item)
   std::vector<int32_t> unit0, wave0;
+  // Resident sweeps: everything a unit reads is a few contiguous ranges that
+  // its CTA copies into shared memory before running the waves from there.
+  // Per unit 8 numbers (doubles, pool / workspace / tree positions): matrices
+  // [0] + [1]; main coefficients (the unit's x^ or y^ slots) [2] + [3]; the
+  // near-field partial slots of its leaves (downward sweep) [4] + [5]; its
+  // tree-position range of x (upward sweep) [6] + [7].  `resident` is false
+  // when some unit's ranges are not contiguous (the generic sweep runs then).
+  std::vector<int64_t> u_range;
+  // ... and, for the kernel, one 128-byte record per unit (16 x int64): the
+  // 8 range numbers; first item | items << 32; number of waves; then the
+  // waves' end items (relative to the unit's first) as 12 x int32
+  std::vector<int64_t> u_rec;
+  bool resident = false;
+  int64_t res_mat_max = 0, res_vec_max = 0;  // largest unit: matrix doubles; coefficient + partial + x doubles
+  int32_t res_items_max = 0;                 // most items in a unit
 
   int64_t ntasks() const { return (int64_t)t_m.size(); }
   int64_t nsegs() const { return (int64_t)s_ncols.size(); }
@@ -101,6 +116,12 @@ struct Group {
   int64_t base = -1;
   int32_t m = 0;
   int64_t ncols = 0;
+  // staged plans: 1 the matrices of an upward sweep unit, 2 of a downward
+  // sweep unit (`unit`: the tree position where its subtree starts), 0 others;
+  // the pool is laid out region by region and unit by unit, so that a unit's
+  // matrices are one contiguous range (one bulk copy into shared memory)
+  int32_t region = 0;
+  int64_t unit = 0;
   std::vector<PackSeg> segs;
   int64_t size() const { return (int64_t)m * ncols; }
 };
@@ -168,7 +189,7 @@ struct PlanOptions {
   // coupling rows of bottom clusters have neither inputs to wait for nor
   // successors to notify.  Multi-GPU: ranks own whole subtrees.
   bool staged = false;
-  int64_t sweep_nodes = 0;        // 0: default (1024)
+  int64_t sweep_nodes = 0;        // 0: default (about 256 subtrees per rank)
   int32_t rank = 0;
   int32_t world_size = 1;
 };

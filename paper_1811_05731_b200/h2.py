@@ -267,6 +267,10 @@ def _grab_view(v) -> dict:
         "mode": int(v.mode), "group": int(v.group), "split": int(v.split),
         "unit0": grab(v.unit0, int(v.nunits) + 1, np.int32) if v.mode == 1 else np.zeros(0, np.int32),
         "wave0": grab(v.wave0, int(v.nwaves) + 1, np.int32) if v.mode == 1 else np.zeros(0, np.int32),
+        "resident": bool(v.resident),
+        "res_max": (int(v.res_mat_max), int(v.res_vec_max), int(v.res_items_max)),
+        "u_range": (grab(v.u_range, 8 * int(v.nunits), np.int64).reshape(-1, 8) if v.mode == 1
+                    else np.zeros((0, 8), np.int64)),
     }
 
 
@@ -363,6 +367,29 @@ class DeviceOperator:
         For a multi-GPU rank operator, y receives this rank's rows."""
         nat.check(self._lib.h2b_matvec_dev(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
                                            int(nrhs), C.c_void_p(stream)), "h2b_matvec_dev")
+
+    LAUNCH_KINDS = {-1: "h2b_permute_kernel", 0: "h2b_dataflow_kernel", 1: "h2b_sweep_kernel", 2: "h2b_near_tma_kernel"}
+
+    def launches(self, nrhs: int = 1) -> list:
+        """The kernel launches of one product: kind, work items, matrix bytes."""
+        out = []
+        for k in range(self._lib.h2b_launch_count(self._h, int(nrhs))):
+            kind, items, nbytes = np.zeros(1, np.int32), np.zeros(1, np.int64), np.zeros(1, np.int64)
+            nat.check(self._lib.h2b_launch_info(self._h, int(nrhs), k, kind.ctypes.data_as(nat._p32),
+                                                nat.as_i64_ptr(items), nat.as_i64_ptr(nbytes)))
+            out.append({"kernel": self.LAUNCH_KINDS[int(kind[0])], "items": int(items[0]), "bytes": int(nbytes[0])})
+        return out
+
+    def launch_times(self, x_ptr: int, y_ptr: int, nrhs: int = 1, steps: int = 10, stream: int = 0) -> list:
+        """Mean device milliseconds of every launch of a product (CUDA events
+        around each launch; measurement aid, single GPU)."""
+        info = self.launches(nrhs)
+        ms = np.zeros(len(info))
+        nat.check(self._lib.h2b_launch_times(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), int(nrhs), int(steps),
+                                             C.c_void_p(stream), nat.as_d_ptr(ms)), "h2b_launch_times")
+        for d, t in zip(info, ms):
+            d["ms"] = float(t)
+        return info
 
     def reset(self) -> None:
         """Scheduler state back to the just-created one (``h2b_reset``)."""

@@ -143,3 +143,27 @@ def test_staged_virtual_ranks_on_one_gpu(world):
             assert rel(y, ex["y_full"][:, 0]) <= TOL, (name, world)
         for d in devs:
             d.close()
+
+
+def test_resident_and_generic_sweeps_agree(monkeypatch):
+    """The resident sweep kernel (units run from shared memory) and the
+    generic one compute the same items; both match the reference, and the
+    small golden operators fit shared memory for 1-4 right-hand sides."""
+    h2 = _h2()
+    for name in ("config1_sphere4", "torus_32_16_4_default"):
+        op, ex = load_golden(name)
+        ys = []
+        for res in ("1", "0"):
+            monkeypatch.setenv("H2B_SWEEP_RESIDENT", res)
+            dev = h2.DeviceOperator(op, plan_flags=h2.PLAN_STAGED | h2.PLAN_SWEEP_NODES(2))
+            try:
+                mask = dev.stats()["resident_mask"]
+                assert (mask & 1) == (1 if res == "1" else 0), (name, res, mask)
+                ys.append(dev.matvec(ex["X"][:, 0]))
+                Y = dev.matvec(ex["X"][:, :4])
+                for i in range(4):
+                    assert rel(Y[:, i], ex["y_full"][:, i]) <= TOL, (name, res, i)
+            finally:
+                dev.close()
+        assert rel(ys[0], ex["y_full"][:, 0]) <= TOL and rel(ys[1], ex["y_full"][:, 0]) <= TOL
+        assert rel(ys[0], ys[1]) <= 1e-14

@@ -14,7 +14,7 @@ from conftest import ROOT, load_golden, rel
 from oracle.flat_matvec import check_plan_invariants, run_plan
 from oracle.h2_matvec_ref import h2_matvec_ref
 from paper_1811_05731_b200 import _native as nat
-from paper_1811_05731_b200.h2 import plan_view
+from paper_1811_05731_b200.h2 import PLAN_NO_STAGED, plan_view
 from synth import random_h2
 
 
@@ -118,7 +118,7 @@ def test_fused_runs_any_order(golden, band_depth):
     all its external inputs, so any dependency-respecting order of the units
     (as the kernel's dynamic scheduler may pick) reproduces the reference."""
     name, op, ex = golden
-    P = plan_view(op, band_depth=band_depth, far_task_bytes=1024)
+    P = plan_view(op, band_depth=band_depth, far_task_bytes=1024, plan_flags=PLAN_NO_STAGED)
     check_plan_invariants(P)
     mlen = P["t_mlen"]
     if band_depth == 1:
@@ -134,7 +134,7 @@ def test_fused_runs_any_order(golden, band_depth):
 def test_fused_runs_random_structures(seed):
     op = random_h2(seed)
     for bd in (2, 4):
-        P = plan_view(op, band_depth=bd, task_bytes=700)
+        P = plan_view(op, band_depth=bd, task_bytes=700, plan_flags=PLAN_NO_STAGED)
         x = np.random.default_rng(seed).standard_normal(op.n)
         y = run_plan(P, x, rng=np.random.default_rng(seed + 10))
         assert rel(y, h2_matvec_ref(op, x)) <= 1e-13
@@ -149,13 +149,13 @@ def test_level_skipping_chain(golden, world):
     from oracle.flat_matvec import run_ranks
     from paper_1811_05731_b200.h2 import PLAN_SKIP_LEVELS, plan_view
     name, op, ex = golden
-    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_SKIP_LEVELS) for r in range(world)]
+    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_SKIP_LEVELS | PLAN_NO_STAGED) for r in range(world)]
     for i in (0, 3):
         y = run_ranks(plans, ex["X"][:, i]) if world > 1 else run_plan(plans[0], ex["X"][:, i])
         assert rel(y, ex["y_full"][:, i]) <= 1e-13, (name, world, i)
     if world == 1:
         check_plan_invariants(plans[0])
-        base = plan_view(op)
+        base = plan_view(op, plan_flags=PLAN_NO_STAGED)
         assert plans[0]["stats"]["extra_bytes"] >= 0
         assert chain_length(plans[0]) <= chain_length(base)
         if chain_length(base) >= 8:   # deep enough for skipped links (config 1: 9 -> 7 items)
@@ -180,13 +180,13 @@ def test_gated_coupling_rows(golden, world):
     from oracle.flat_matvec import run_ranks
     from paper_1811_05731_b200.h2 import PLAN_GATE, plan_view
     name, op, ex = golden
-    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_GATE) for r in range(world)]
+    plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_GATE | PLAN_NO_STAGED) for r in range(world)]
     for i in (0, 2):
         y = run_ranks(plans, ex["X"][:, i]) if world > 1 else run_plan(plans[0], ex["X"][:, i])
         assert rel(y, ex["y_full"][:, i]) <= 1e-13, (name, world, i)
     if world == 1:
         p0 = plans[0]
-        base = plan_view(op, plan_flags=0x200)   # no gate
+        base = plan_view(op, plan_flags=0x200 | PLAN_NO_STAGED)   # no gate
         if len(op.coupling):
             assert p0["gated"].size > 0 and p0["ndeps"] < base["ndeps"] if "ndeps" in p0 else p0["gated"].size > 0
         assert np.all(p0["t_kind"][p0["gated"]] == 2)

@@ -84,13 +84,14 @@ def test_staged_random_structures(seed):
 
 
 def test_staged_split_product(golden):
-    """The split multi-RHS product of a staged plan: upward sweep, the near
-    field alone, the rest, downward sweep."""
+    """The split multi-RHS product planned beside a staged plan keeps every
+    far-field item in its dataflow launch (sweeps of 8/16 right-hand sides
+    measured slower): the near field alone, then the rest."""
     name, op, ex = golden
     P = plan_view(op, plan_flags=PLAN_STAGED | PLAN_SWEEP_NODES(2) | PLAN_NEAR_SPLIT)
     sp = launches(P, split=True)
-    assert [ph["mode"] for ph in sp if ph["mode"] != 1] == ([2, 0] if len(op.coupling) else [2])
-    assert np.all(sp[[ph["mode"] for ph in sp].index(2)]["t_kind"] == 3)
+    assert [ph["mode"] for ph in sp] == [2, 0]
+    assert np.all(sp[0]["t_kind"] == 3) and int((sp[1]["t_kind"] == 4).sum()) > 0
     Y = run_plan(P, ex["X"][:, :4], split=True)
     for i in range(4):
         assert rel(Y[:, i], ex["y_full"][:, i]) <= 1e-13, (name, i)
@@ -119,3 +120,36 @@ def test_staged_rank_plans_random_structures(seed):
     for world in (2, 5):
         plans = [plan_view(op, world_size=world, rank=r, plan_flags=PLAN_STAGED) for r in range(world)]
         assert rel(run_ranks(plans, x), ref) <= 1e-13
+
+
+def test_staged_units_are_contiguous_ranges(golden):
+    """Resident sweeps: a unit's matrices, coefficient slots, near-field
+    partial slots and x range are contiguous, cover exactly what its items
+    touch inside the subtree, and units do not overlap."""
+    name, op, ex = golden
+    P = plan_view(op, plan_flags=PLAN_STAGED | PLAN_SWEEP_NODES(2))
+    for ph in launches(P):
+        if ph["mode"] != 1:
+            continue
+        assert ph["resident"], name
+        R = ph["u_range"]
+        up = ph["t_kind"][0] <= 1
+        assert np.all(R[:, 1::2] >= 0)
+        for col in (0, 2, 4):           # pool, coefficient and partial ranges of different units are disjoint
+            o = np.argsort(R[:, col], kind="stable")
+            lo, ln = R[o, col], R[o, col + 1]
+            assert np.all(lo[1:] >= (lo + ln)[:-1]), (name, col)
+        for u in range(len(R)):
+            k0, k1 = ph["wave0"][ph["unit0"][u]], ph["wave0"][ph["unit0"][u + 1]]
+            for t in range(k0, k1):
+                d0 = ph["t_data"][t]
+                last = d0 + (ph["t_ncols"][t] - 1) * ph["t_ld"][t] + ph["t_m"][t]
+                assert R[u, 0] <= d0 and last <= R[u, 0] + R[u, 1], (name, u, t)
+                if ph["t_kind"][t] != 4:   # outputs stay inside the unit's main coefficient range
+                    assert R[u, 2] <= ph["t_out"][t] and ph["t_out"][t] + ph["t_m"][t] <= R[u, 2] + R[u, 3]
+                else:
+                    assert R[u, 6] <= ph["t_out"][t] and ph["t_out"][t] + ph["t_m"][t] <= R[u, 6] + R[u, 7]
+                    if ph["t_bias"][t] >= 0:
+                        assert R[u, 4] <= ph["t_bias"][t] < R[u, 4] + R[u, 5]
+            if up:
+                assert R[u, 5] == 0

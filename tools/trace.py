@@ -79,6 +79,24 @@ def main():
     T = plan["t_m"].size
     tr = np.zeros((T, 8), np.uint64)
     nat.check(lib.h2b_trace_read(dev._h, tr.ctypes.data, T))
+    if plan.get("mode", 0) == 1 and plan.get("resident") and os.environ.get("H2B_SWEEP_RESIDENT", "1") != "0":
+        # resident sweep: one record per unit, in the slots of its first item:
+        # start, end, waves | cta, copies issued, copies landed, end of wave 0, 1, last but one
+        first = plan["wave0"][plan["unit0"][:-1]]
+        r = tr[first].astype(np.int64)
+        ok = r[:, 1] > 0
+        r = r[ok]
+        t0 = r[:, 0].min()
+        print(f"resident sweep: {ok.sum()} units of {len(first)}, span {(r[:, 1].max() - t0) / 1e3:.1f} us, "
+              f"first start {0.0:.1f}, last start {(r[:, 0].max() - t0) / 1e3:.1f} us")
+        names = ("issue", "land", "wave0", "wave1", "..last-1", "last")
+        cols = [(0, 3), (3, 4), (4, 5), (5, 6), (6, 7), (7, 1)]
+        print("  per unit us: " + " ".join(f"{n} {(r[:, b] - r[:, a]).clip(0).mean() / 1e3:5.2f}" for n, (a, b) in zip(names, cols))
+              + f"  total {(r[:, 1] - r[:, 0]).mean() / 1e3:5.2f}  waves {np.mean(r[:, 2] >> 32):.1f}")
+        R = plan["u_range"]
+        print(f"  per unit KB: matrices {R[:, 1].mean() * 8 / 1e3:.1f} coef {R[:, 3].mean() * 8 / 1e3:.1f} "
+              f"partials {R[:, 5].mean() * 8 / 1e3:.1f} items {np.diff(plan['wave0'][plan['unit0']]).mean():.1f}")
+        return
     # one record per scheduled unit (the first item of a fused run)
     unit = tr[:, 1] > 0
     start = tr[:, 0].astype(np.int64)
