@@ -175,6 +175,16 @@ struct __align__(128) WarpSmem {
 // KB for single-vector products (sched_flags bits 18-19), which lets more
 // warps of a CTA own a ring at two CTAs per SM.
 constexpr int kRingStageBytes = 8192;
+// 8/16 right-hand sides in the dataflow and sweep kernels: DMMA tiles over 64
+// rows per pass and 8 KB ring stages, one CTA of eight warps per SM.  The
+// lean alternative -- 32 rows per pass (kMrhsMT 2: half the accumulator
+// registers, items above 32 rows in two passes), 4 KB stages, two CTAs per
+// SM at 128 registers -- measured slower on config 3 (16 RHS 4.57 -> 5.35 ms,
+// 8 RHS 3.55 -> 4.07 ms: spills and the second pass cost more than the extra
+// warps hide), so it stays a compile-time option.
+constexpr int kMrhsMT = 4;
+constexpr int kMrhsStage = 8192;
+constexpr int kMrhsCtas = kMrhsMT >= 4 ? 1 : 2;
 struct WarpRing {  // view into dynamic shared memory (no dynamically indexed arrays)
   double* base;     // stage 0; stage 1 follows at base + sdbl
   uint64_t* bars;   // two mbarriers
@@ -385,7 +395,7 @@ __device__ __forceinline__ void gather_chunk(const KParams& p, WarpSmem& w, int 
     return;
   }
   constexpr int VW = NRHS >= 2 ? 2 : 1;
-  constexpr int UG = NRHS >= 16 ? 8 : 4;
+  constexpr int UG = 4;
   using V = typename std::conditional<VW == 2, double2, double>::type;
   const int total = cc * NRHS / VW;
   int k = 0;  // segment cursor (columns increase along a lane)
@@ -655,9 +665,9 @@ __device__ __forceinline__ void run_item(const KParams& p, const DTask& T, const
 }
 
 
-template <int NRHS>
-__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[4][NRHS / 8][4],
-                                             int lane);
+template <int NRHS, int MT>
+__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[MT][NRHS / 8][4],
+                                             int lane, int row0);
 
 // D(16x8) += A(16x4, row) B(4x8, col) in fp64 on the tensor cores (DMMA).
 __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
@@ -672,18 +682,22 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 // 16-row tile (eight consecutive doubles per column and tile: coalesced),
 // X row t / column g of each 8-column tile from the gathered sources in
 // shared memory, and accumulator rows g, g+8 / columns 2t, 2t+1.
-template <int NRHS, bool SMEM>
+template <int NRHS, bool SMEM, int MT = 4>
 __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
                                              int lane, const double* A, uint64_t* bar, unsigned parity,
                                              unsigned long long& t_gath) {
   static_assert(NRHS == 8 || NRHS == 16, "DMMA path: 8 or 16 right-hand sides");
   constexpr int kCols = kChunkBytes / (8 * NRHS);
   constexpr int NT = NRHS / 8;  // 8-column tiles
-  constexpr int MT = 4;         // 16-row tiles (m <= 64)
+  // MT 16-row tiles per pass: 4 covers an item (m <= 64) in one pass; the
+  // dataflow kernel uses 2 (half the accumulator registers, two CTAs per SM)
+  // and runs items of more than 32 rows in two passes over the rows
   const int m = T.m, ld = T.ld;
-  const int mtiles = (m + 15) >> 4;
   const int g = lane >> 2, t = lane & 3;
   load_segtable(p, T, sin, w, lane);
+  bool waited = false;
+  for (int row0 = 0; row0 < m || row0 == 0; row0 += 16 * MT) {
+  const int mtiles = (min(m - row0, 16 * MT) + 15) >> 4;
 
   double acc[MT][NT][4];
 #pragma unroll
@@ -695,7 +709,7 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
 
   for (int col = 0; col < T.ncols; col += kCols) {
     const int cc = min(kCols, T.ncols - col);
-    const double* Ac = A + (int64_t)col * ld;
+    const double* Ac = A + (int64_t)col * ld + row0;
     // A fragments of the first k-step: streamed ones are issued before the
     // gather, staged ones read once the bulk copy has landed
     double a[MT][2];
@@ -704,17 +718,23 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
       for (int i = 0; i < MT; ++i) {
         const int r = 16 * i + g;
         const bool ok = i < mtiles && t < cc;
-        a[i][0] = (ok && r < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r) : 0.0;
-        a[i][1] = (ok && r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r + 8) : 0.0;
+        a[i][0] = (ok && row0 + r < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r) : 0.0;
+        a[i][1] = (ok && row0 + r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)t * ld + r + 8) : 0.0;
       }
     };
     if (!SMEM) load_a0();
-    gather_chunk<NRHS>(p, w, lane, col, cc);
-    for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) w.xs[j] = 0.0;  // k padding
+    // (a later pass over the rows of a single-chunk item finds its sources staged)
+    if (row0 == 0 || T.ncols > kCols) {
+      gather_chunk<NRHS>(p, w, lane, col, cc);
+      for (int j = cc * NRHS + lane; j < ((cc + 3) & ~3) * NRHS; j += 32) w.xs[j] = 0.0;  // k padding
+    }
     __syncwarp();
-    if (SMEM && col == 0) mbar_wait(bar, parity);
+    if (SMEM && !waited) {
+      mbar_wait(bar, parity);
+      waited = true;
+    }
     if (SMEM) load_a0();
-    if (p.trace && col == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
+    if (p.trace && col == 0 && row0 == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
     for (int c = 0; c < cc; c += 4) {
       // next k-step's A fragments in flight while this one multiplies
       double an[MT][2];
@@ -723,8 +743,8 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
       for (int i = 0; i < MT; ++i) {
         const int r = 16 * i + g;
         const bool ok = i < mtiles && cn < cc;
-        an[i][0] = (ok && r < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r) : 0.0;
-        an[i][1] = (ok && r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r + 8) : 0.0;
+        an[i][0] = (ok && row0 + r < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r) : 0.0;
+        an[i][1] = (ok && row0 + r + 8 < m) ? ldA<SMEM>(Ac + (int64_t)cn * ld + r + 8) : 0.0;
       }
       double b[NT];
 #pragma unroll
@@ -743,31 +763,33 @@ __device__ __forceinline__ void run_item_mma(const KParams& p, const DTask& T, c
     __syncwarp();
   }
 
-  mma_epilogue<NRHS>(p, T, acc, lane);
+  mma_epilogue<NRHS, MT>(p, T, acc, lane, row0);
+  }
 }
 
 // Bias slots, then the output rows this lane holds (accumulator rows g, g+8
-// of each 16-row tile, columns 2t, 2t+1 of each 8-column tile).
-template <int NRHS>
-__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[4][NRHS / 8][4],
-                                             int lane) {
+// of each 16-row tile, columns 2t, 2t+1 of each 8-column tile); the tiles
+// cover rows [row0, row0 + 16 MT) of the item.
+template <int NRHS, int MT>
+__device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, double (&acc)[MT][NRHS / 8][4],
+                                             int lane, int row0) {
   constexpr int NT = NRHS / 8;
-  constexpr int MT = 4;
   const int m = T.m;
-  const int mtiles = (m + 15) >> 4;
+  const int mtiles = (min(m - row0, 16 * MT) + 15) >> 4;
   const int g = lane >> 2, t = lane & 3;
-  // bias slots (the final items' near-field partials): two slots of every
-  // row this lane holds in flight at once, added in slot order
+  // bias slots (the final items' near-field partials): slots of every row
+  // this lane holds in flight at once, added in slot order
+  constexpr int QB = (MT >= 4 || NT >= 2) ? 2 : 4;
   if (T.bias >= 0) {
-    for (int s = 0; s < T.bias_nslots; s += 2) {
-      double2 q[2][MT][2][NT];
+    for (int s = 0; s < T.bias_nslots; s += QB) {
+      double2 q[QB][MT][2][NT];
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < QB; ++u)
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int r = 16 * i + g + 8 * h;
+            const int r = row0 + 16 * i + g + 8 * h;
             const bool ok = s + u < T.bias_nslots && i < mtiles && r < m;
             const double* bp = p.coef + (T.bias + (int64_t)(s + u) * T.bias_stride + r) * NRHS + 2 * t;
 #pragma unroll
@@ -775,7 +797,7 @@ __device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, d
               q[u][i][h][j] = ok ? __ldcg(reinterpret_cast<const double2*>(bp + 8 * j)) : make_double2(0.0, 0.0);
           }
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < QB; ++u)
         if (s + u < T.bias_nslots)
 #pragma unroll
           for (int i = 0; i < MT; ++i)
@@ -793,7 +815,7 @@ __device__ __forceinline__ void mma_epilogue(const KParams& p, const DTask& T, d
     if (i >= mtiles) break;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = 16 * i + g + 8 * h;
+      const int r = row0 + 16 * i + g + 8 * h;
       if (r >= m) continue;
       double2 v[NT];
 #pragma unroll
@@ -859,15 +881,13 @@ __device__ __forceinline__ void gather_commit(GatherBatch<NRHS>& g, int lane, in
 // leaves HBM idle).  The sources of chunk j + 1 are gathered into the other
 // half of the warp's source buffer while chunk j multiplies.  `rpar` holds
 // the ring's mbarrier parities (bit s).
-template <int NRHS, int STAGE = kRingStageBytes>
+template <int NRHS, int STAGE = kRingStageBytes, int MT = 4>
 __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask& T, const DSeg& sin, WarpSmem& w,
                                                   const WarpRing R, unsigned& rpar, int lane,
                                                   unsigned long long& t_gath) {
   constexpr int kHalf = kChunkBytes / (16 * NRHS);  // columns per source half (16 or 32)
   constexpr int NT = NRHS / 8;
-  constexpr int MT = 4;
   const int m = T.m;
-  const int mtiles = (m + 15) >> 4;
   const int g = lane >> 2, t = lane & 3;
   // columns per stage (>= 16), a whole number of 4-column k-steps so that
   // the DMMA sums group columns exactly like the register-staged loop
@@ -914,6 +934,10 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     // acquired by this warp: order them before the async-proxy reads
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
+  // MT < 4: items of more than 16 MT rows stream once per pass over the rows
+  for (int row0 = 0; row0 < m; row0 += 16 * MT) {
+  const int mtiles = (min(m - row0, 16 * MT) + 15) >> 4;
+  kseg_tma = 0;
   if (lane == 0) {
     issue(0);
     if (nch > 1) issue(1);
@@ -951,7 +975,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
       double a[MT][2];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const int r = 16 * i + g;
+        const int r = row0 + 16 * i + g;
         const bool ok = okc && i < mtiles;
         a[i][0] = (ok && r < m) ? A[(c + t) * m + r] : 0.0;
         a[i][1] = (ok && r + 8 < m) ? A[(c + t) * m + r + 8] : 0.0;
@@ -972,7 +996,9 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
       __syncwarp();
     }
   }
-  mma_epilogue<NRHS>(p, T, acc, lane);
+  mma_epilogue<NRHS, MT>(p, T, acc, lane, row0);
+  __syncwarp();
+  }
 }
 
 
@@ -1126,7 +1152,7 @@ __device__ __forceinline__ void run_item_ring_multi(const KParams& p, const DTas
 }
 
 template <int NRHS>
-__global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KParams p) {
+__global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1140,7 +1166,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
   // staging: a TMA ring (ring warps) or one far-field buffer
   const int nring = NRHS >= 8 ? nw : p.ring_warps;
   const int first_ring = nw - nring;
-  const int rstage = NRHS >= 8 ? kRingStageBytes : p.ring_stage;
+  const int rstage = NRHS >= 8 ? kMrhsStage : p.ring_stage;
   WarpRing ring_v{nullptr, nullptr, 0};
   bool has_ring = false;
   double* abuf;
@@ -1392,12 +1418,12 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_dataflow_kernel(KP
     }
     if constexpr (NRHS >= 8) {
       if (off >= 0) {
-        run_item_mma<NRHS, true>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
+        run_item_mma<NRHS, true, kMrhsMT>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
         phase ^= 1u;
       } else if (T.ld == T.m && T.m <= 64 && T.ncols > 0 && !(p.flags & kFlagNoRing)) {  // all warps ring
-        run_item_mma_ring<NRHS>(p, T, sin, w, ring_v, rpar, lane, t_gath);
+        run_item_mma_ring<NRHS, kMrhsStage, kMrhsMT>(p, T, sin, w, ring_v, rpar, lane, t_gath);
       } else {
-        run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
+        run_item_mma<NRHS, false, kMrhsMT>(p, T, sin, w, lane, p.mat + T.data, bar, phase, t_gath);
       }
     } else if (off >= 0) {
       run_item<NRHS, true, 16>(p, T, sin, w, lane, abuf + off, bar, phase, t_gath);
@@ -1629,7 +1655,7 @@ __device__ __forceinline__ void run_near_tma(const KParams& p, const DTask& T, c
     __syncwarp();  // every lane is done with stage s
     if (lane == 0 && jc + NST < nch) issue(jc + NST);
   }
-  mma_epilogue<NRHS>(p, T, acc, lane);
+  mma_epilogue<NRHS, MT>(p, T, acc, lane, 0);
 }
 
 // The near field of a multi-RHS product (8 or 16 right-hand sides) on its
@@ -1753,7 +1779,7 @@ __device__ __forceinline__ void prefetch_l1(const void* q) {
 // the current one runs.  Used when a unit's inputs do not fit shared memory
 // (large subtrees, many right-hand sides); see the resident kernel below.
 template <int NRHS>
-__global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KParams p) {
+__global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_sweep_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1861,8 +1887,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? 1 : 2) h2b_sweep_kernel(KPara
         unsigned long long t_desc = 0;
         if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_desc)::"memory");
         if constexpr (NRHS >= 8) {
-          if (mode) run_item_mma<NRHS, true>(p, T, sin, w, lane, buf[cur] + off, bars + cur, ph, t_gath);
-          else run_item_mma<NRHS, false>(p, T, sin, w, lane, p.mat + T.data, wbar, 0u, t_gath);
+          if (mode) run_item_mma<NRHS, true, kMrhsMT>(p, T, sin, w, lane, buf[cur] + off, bars + cur, ph, t_gath);
+          else run_item_mma<NRHS, false, kMrhsMT>(p, T, sin, w, lane, p.mat + T.data, wbar, 0u, t_gath);
         } else {
           if (mode) run_item<NRHS, true, 16>(p, T, sin, w, lane, buf[cur] + off, bars + cur, ph, t_gath);
           else run_item<NRHS, false, 8>(p, T, sin, w, lane, p.mat + T.data, wbar, 0u, t_gath);
@@ -2371,9 +2397,6 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
     if (sg && sg[0] == '1') po.staged = true;
     if (sg && sg[0] == '0') po.staged = false;
   }
-  // staged plans: the subtrees' items are staged one per 4 KB buffer and the
-  // next one prefetched, so they keep the small far-field pieces
-  if (po.staged && !(o && o->far_task_bytes > 0)) po.far_task_bytes = 4096;
   return po;
 }
 
@@ -2411,7 +2434,7 @@ int nrhs_index(int nrhs) {
 
 template <int NRHS>
 int occupancy_grid(int wpc, int ring_warps, int ring_stage, int ctas_per_sm, int* grid) {
-  const size_t sm = NRHS >= 8 ? smem_bytes(wpc, wpc, kRingStageBytes) : smem_bytes(wpc, ring_warps, ring_stage);
+  const size_t sm = NRHS >= 8 ? smem_bytes(wpc, wpc, kMrhsStage) : smem_bytes(wpc, ring_warps, ring_stage);
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -2494,7 +2517,7 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) 
   if (F.ntasks == 0) return H2B_OK;
   const KParams p = phase_params<NRHS>(op, F, y);
   const int gi = nrhs_index(NRHS);
-  const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kRingStageBytes)
+  const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kMrhsStage)
                                 : smem_bytes(op->wpc, op->ring_warps, op->ring_stage);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   // the attribute is per function and shared by every operator of the process

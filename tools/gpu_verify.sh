@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-end style verification on one B200: GPU tests, smoke, default bench,
-# ncu launch list and one full capture of the dataflow kernel.
+# ncu launch list and full captures of the dataflow and sweep kernels.
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
@@ -8,3 +8,4 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; 
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:h2b_dataflow_kernel -s 3 -c 1 -o gpurun_out/dataflow_full python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:h2b_sweep -s 6 -c 2 -o gpurun_out/sweep_full python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_sweep.log 2>&1; echo "ncu sweep rc=$?"
