@@ -402,6 +402,57 @@ int h2b_cg_solve_dev(h2b_cg* c, const double* b_dev, double* x_dev, double tol, 
                      int64_t* iterations, double* residual, void* stream);
 void h2b_cg_destroy(h2b_cg* c);
 
+/* ---- H -> H^2 recompression on the device -------------
+ * hmatrix/h2.py:86-183 (_basis_side, recompress_h2), restated level by level
+ * with projected factors: paper_1811_05731_b200/assembly/gpu_recompress.py
+ * drives these launches; oracle/rc_ops_ref.py restates each in numpy.  All
+ * pointers are DEVICE pointers; every call only enqueues one kernel on
+ * `stream` and returns.  One CTA per cluster, no atomics (deterministic).
+ *
+ * Tree arrays, indexed by cluster id: start/end (tree positions), depth,
+ * anc[c * nanc + j] = the ancestor of c at depth j (j <= depth[c], anc = c at
+ * j = depth[c]), child[2c], child[2c+1] (-1 for leaves), parent.
+ * One side's factors: the blocks anchored at cluster a packed side by side
+ * as one row-major (end[a]-start[a]) x cown[a] matrix at fac + foff[a], their
+ * column weights at wts + woff[a]; ccur[c] = sum of cown over c's ancestors
+ * and c.  k[c]: kept rank.  P: the projected factors of one tree depth,
+ * P_c = V_c^T [weighted factor rows] as k[c] x ccur[c] column-major at
+ * P + poff[c].  Matrices of a batch: G + i * ldg * ldg, row-major, leading
+ * dimension ldg, for the i-th id of the call. */
+
+/* G_i = sum_a R_a diag(w_a^2) R_a^T over the ancestors a of leaf ids[i]
+ * (at most 64 rows), R_a = the leaf's rows of a's packed block. */
+int h2b_rc_leaf_gram(int64_t nleaf, const int64_t* ids, const int64_t* start, const int64_t* end, const int32_t* anc,
+                     const int64_t* depth, const int64_t* foff, const int64_t* cown, int32_t nanc, const int64_t* woff,
+                     const double* fac, const double* wts, int32_t ldg, double* G, void* stream);
+/* Eigenpairs of nmat symmetric matrices (nvec[i] <= ldg <= 128 rows) by
+ * cyclic Jacobi, in place: column j of G_i becomes the eigenvector of the
+ * j-th largest eigenvalue lam[i * ldg + j].  max_sweeps <= 0: 30. */
+int h2b_rc_eigh(int64_t nmat, const int64_t* nvec, double* G, int32_t ldg, double* lam, int32_t max_sweeps, void* stream);
+/* P_c = V(:, :k[c])^T [R_a diag(w_a)]_a for the leaves ids[i], V = V + i ldg^2. */
+int h2b_rc_leaf_project(int64_t nleaf, const int64_t* ids, const int64_t* start, const int64_t* end, const int32_t* anc,
+                        const int64_t* depth, const int64_t* foff, const int64_t* cown, int32_t nanc, const int64_t* woff,
+                        const double* fac, const double* wts, const double* V, int32_t ldg, const int64_t* k, double* P,
+                        const int64_t* poff, const int64_t* ccur, void* stream);
+/* G_i = Z Z^T, Z = the children's P (depth below: Pc, poffc) stacked, first
+ * ccur[c] columns; k[child 1] + k[child 2] <= 128. */
+int h2b_rc_inner_gram(int64_t n, const int64_t* ids, const int64_t* child, const int64_t* k, const int64_t* ccur,
+                      const double* Pc, const int64_t* poffc, double* G, int32_t ldg, void* stream);
+/* P_c = V(:, :k[c])^T Z. */
+int h2b_rc_inner_project(int64_t n, const int64_t* ids, const int64_t* child, const int64_t* k, const int64_t* ccur,
+                         const double* Pc, const int64_t* poffc, const double* V, int32_t ldg, double* P,
+                         const int64_t* poff, void* stream);
+/* Q_c = the last cown[c] columns of P_c with the weights divided out (a zero
+ * weight gives a zero column), k[c] x cown[c] column-major at Q + qoff[c]. */
+int h2b_rc_extract_own(int64_t n, const int64_t* ids, const int64_t* parent, const int64_t* k, const int64_t* ccur,
+                       const int64_t* cown, const int64_t* woff, const double* wts, const double* P, const int64_t* poff,
+                       double* Q, const int64_t* qoff, void* stream);
+/* Coupling matrices (h2.py:171-176): S_b = Qr_t(:, rcol[b] .. + kb[b]) Qc_s(:, ccol[b] .. + kb[b])^T,
+ * kr[t] x kc[s] row-major at S + soff[b], t = bt[b], s = bs[b]. */
+int h2b_rc_coupling(int64_t nb, const int64_t* bt, const int64_t* bs, const int64_t* rcol, const int64_t* ccol,
+                    const int64_t* kb, const double* Qr, const int64_t* qoffr, const int64_t* kr, const double* Qc,
+                    const int64_t* qoffc, const int64_t* kc, double* S, const int64_t* soff, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -402,7 +402,8 @@ def _map(fn, items, workers, chunksize=64):
 
 def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(), *,
                 evaluator=None, workers: int | None = None, log=None,
-                backend: str = "numpy", device: str = "cuda") -> tuple[H2Matrix, BuildReport]:
+                backend: str = "numpy", device: str = "cuda",
+                recompress_backend: str = "host") -> tuple[H2Matrix, BuildReport]:
     """Build the compressed operator M = K + D of ``surface`` as an H2Matrix
     (``hmatrix.assemble_operator(mesh, "h2", config).payload``).
 
@@ -410,7 +411,9 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
     operators, tests/test_builder.py).  backend "gpu": the admissible blocks
     by batched HCA on the GPU (assembly/gpu_hca.py) and Gram-based bases in
     the recompression -- the same algorithm to rounding, for the large
-    BASELINE workloads."""
+    BASELINE workloads; with ``recompress_backend="gpu"`` the recompression
+    itself runs on the device too (assembly/gpu_recompress.py, SURVEY §8f
+    row 4)."""
     _say = log or (lambda *a: None)
 
     def say(msg):  # with the process's resident / peak memory
@@ -509,19 +512,31 @@ def assemble_h2(surface: Surface, config: CompressionConfig = CompressionConfig(
         say(f"HCA (gpu): {adm_ids.size} blocks, factors {fbytes / 1e9:.2f} GB, {n_fb} ACA fallbacks ({times['hca_gpu']:.1f}s: "
             + ", ".join(f"{k} {times[k]:.1f}s" for k in ("cross", "solve", "rows", "truncate") if k in times) + ")")
         t5 = time.perf_counter()
-        from .recompress import recompress
-        op = recompress(tree, surface.n,
-                        [(int(bt[adm_ids[i]]), int(bs[adm_ids[i]]), lowrank[i][0], lowrank[i][1])
-                         for i in range(adm_ids.size)],
-                        [(int(dt[i]), int(ds[i]), near_mats[i]) for i in range(dense_ids.size)],
-                        config.eps_rec, workers=workers, weights=weights, timings=times)
-        times["recompress"] = time.perf_counter() - t5
-        times["total"] = time.perf_counter() - t0
-        say(f"recompress {times['recompress']:.1f}s (bases rows {times.get('rec_rows', 0):.1f}s, cols "
-            f"{times.get('rec_cols', 0):.1f}s [weighting {times.get('rec_cols_weighting', 0):.1f}s, leaves "
-            f"{times.get('rec_cols_leaf_cpu', 0):.1f} / inner {times.get('rec_cols_inner_cpu', 0):.1f} thread-s], coupling "
-            f"{times.get('rec_coupling', 0):.1f}s); "
-            f"H² {op.storage_bytes() / 1e6:.1f} MB; total {times['total']:.1f}s")
+        lr_list = [(int(bt[adm_ids[i]]), int(bs[adm_ids[i]]), lowrank[i][0], lowrank[i][1])
+                   for i in range(adm_ids.size)]
+        dense_list = [(int(dt[i]), int(ds[i]), near_mats[i]) for i in range(dense_ids.size)]
+        if recompress_backend == "gpu":
+            from .gpu_recompress import recompress_gpu
+            op = recompress_gpu(tree, surface.n, lr_list, dense_list, config.eps_rec, weights, timings=times)
+            times["recompress"] = time.perf_counter() - t5
+            times["total"] = time.perf_counter() - t0
+            say(f"recompress (gpu) {times['recompress']:.1f}s (rows: pack {times.get('rec_rows_pack', 0):.1f}s, levels "
+                f"{times.get('rec_rows', 0):.1f}s; cols: pack {times.get('rec_cols_pack', 0):.1f}s, levels "
+                f"{times.get('rec_cols', 0):.1f}s; coupling {times.get('rec_coupling', 0):.1f}s); "
+                f"H² {op.storage_bytes() / 1e6:.1f} MB; total {times['total']:.1f}s")
+        elif recompress_backend == "host":
+            from .recompress import recompress
+            op = recompress(tree, surface.n, lr_list, dense_list, config.eps_rec, workers=workers, weights=weights,
+                            timings=times)
+            times["recompress"] = time.perf_counter() - t5
+            times["total"] = time.perf_counter() - t0
+            say(f"recompress {times['recompress']:.1f}s (bases rows {times.get('rec_rows', 0):.1f}s, cols "
+                f"{times.get('rec_cols', 0):.1f}s [weighting {times.get('rec_cols_weighting', 0):.1f}s, leaves "
+                f"{times.get('rec_cols_leaf_cpu', 0):.1f} / inner {times.get('rec_cols_inner_cpu', 0):.1f} thread-s], coupling "
+                f"{times.get('rec_coupling', 0):.1f}s); "
+                f"H² {op.storage_bytes() / 1e6:.1f} MB; total {times['total']:.1f}s")
+        else:
+            raise ValueError(f"unknown recompress_backend {recompress_backend!r}")
         rep = BuildReport(n=surface.n, nclusters=len(cl), n_admissible=int(adm_ids.size),
                           n_dense=int(dense_ids.size), n_fallback=n_fb, seconds=times)
         return op, rep

@@ -66,7 +66,11 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     The cache only saves build time; it is keyed by the workload recipe."""
     w = WORKLOADS[name]
     backend = w.get("backend", "numpy")
-    key = hashlib.sha256(repr((name, w["desc"], w["cfg"], 1, backend)).encode()).hexdigest()[:16]
+    # H2B_RECOMPRESS=gpu: the recompression on the device too (assembly/gpu_recompress.py);
+    # a kept rank can differ at the threshold, so those operators are cached apart
+    rec = os.environ.get("H2B_RECOMPRESS", "host") if backend == "gpu" else "host"
+    recipe = (name, w["desc"], w["cfg"], 1, backend) + ((rec,) if rec != "host" else ())
+    key = hashlib.sha256(repr(recipe).encode()).hexdigest()[:16]
     path = Path(cache_dir) / f"h2b_{name}_{key}" if cache_dir else None
     if path is not None and (path / "DONE").exists():
         t = time.perf_counter()
@@ -80,7 +84,7 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     surf = w["surface"]()
     log(f"[workload] {name}: surface N={surf.n} T={surf.triangles.shape[0]} ({time.perf_counter() - t:.1f}s)")
     op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"),
-                          backend=backend)
+                          backend=backend, recompress_backend=rec)
     info = {"cached": False, "n": surf.n, "build_seconds": rep.seconds, "n_admissible": rep.n_admissible,
             "n_dense": rep.n_dense, "n_fallback": rep.n_fallback, "coords": surf.coords}
     if path is not None:
