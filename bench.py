@@ -355,6 +355,32 @@ def run_b200(args):
                 errs.append(float(np.linalg.norm(yc - yr) / np.linalg.norm(yr)))
             parity[k] = max(errs)
             log(f"[bench] parity {k}: {parity[k]:.2e} over {len(errs)} column(s)")
+    # compression error of the built operator itself (rank 0): sampled rows of
+    # the exact collocation matrix (GPU collocation kernel) times the seeded
+    # input against the same rows of the H² product.  By default when the
+    # operator was built in this run (its surface is at hand).
+    op_check = None
+    rows_wanted = args.check_rows if args.check_rows is not None else (32 if info.get("surface") is not None else 0)
+    if rank == 0 and not args.profile and rows_wanted > 0:
+        from paper_1811_05731_b200.workloads import exact_rows, surface_for
+        surf = info.get("surface") or surface_for(args.config)
+        nodes = np.sort(np.random.default_rng(99).choice(n, size=min(rows_wanted, n), replace=False))
+        rows = exact_rows(surf, nodes)
+        x0 = xh if xh.ndim == 1 else xh[:, 0]
+        y0 = ys["randn"] if xh.ndim == 1 else ys["randn"][:, 0]
+        exact = rows @ x0
+        scale = float(np.linalg.norm(y0) / np.sqrt(n))   # rms of y
+        err = np.abs(y0[nodes] - exact) / scale
+        rsum = rows.sum(axis=1)   # (M 1)_i: the same constant for every node of a closed surface
+        op_check = {"rows": int(nodes.size), "max_err_over_rms_y": float(err.max()),
+                    "rms_err_over_rms_y": float(np.sqrt(np.mean(err ** 2))),
+                    "exact_row_sum_mean": float(rsum.mean()), "exact_row_sum_spread": float(np.ptp(rsum)),
+                    "note": "exact rows of M = K + D by the collocation kernel (bem.py:221-235) times the seeded "
+                            "input vs the same rows of the H² product; the operator was compressed with "
+                            "eps 1e-5 / eps_rec 2e-4"}
+        log(f"[bench] operator check: {nodes.size} exact rows, max err {err.max():.2e}, rms {op_check['rms_err_over_rms_y']:.2e} (of rms y)")
+        del rows
+    info.pop("surface", None)
     for _ in range(args.warmup):
         dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, sp)
     torch.cuda.synchronize()
@@ -450,6 +476,7 @@ def run_b200(args):
                 "gpu_launches": nlaunch * args.steps, "clocks": clocks,
                 "parity_rel_err_vs_oracle": max(parity.values()) if parity else None,
                 "parity": parity,
+                "operator_check": op_check,
                 "build": {**{k: v for k, v in info.items() if k not in ("build_seconds", "coords")},
                           "seconds": {k: round(v, 2) for k, v in (info.get("build_seconds") or {}).items()}},
                 "plan": {"work_items": st["ntasks"], "grid": st["grid"], "bytes_by_kind": st["bytes_by_kind"]},
@@ -472,6 +499,9 @@ def main(argv=None):
     ap.add_argument("--cache-dir", default=os.environ.get("H2B_CACHE", "/tmp/h2b_cache"))
     ap.add_argument("--profile", action="store_true", help="skip parity/e2e/CPU legs (for ncu)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check-rows", type=int, default=None,
+                    help="exact collocation rows to check the built operator against (default: 32 when the "
+                         "operator was built in this run, else 0)")
     ap.add_argument("--l2-flush", action="store_true",
                     help="rewrite a 252 MB buffer before every timed step (default: K back-to-back "
                          "steps; the operator is larger than the L2 for configs 2-5)")

@@ -196,6 +196,12 @@ class CudaOps:
     def sync(self):
         self.torch.cuda.synchronize()
 
+    def release(self):
+        """Return the caching allocator's blocks to the driver (h2b_create
+        allocates the operator with cudaMalloc, outside torch)."""
+        self.torch.cuda.synchronize()
+        self.torch.cuda.empty_cache()
+
     def _call(self, name, *args):
         st = self.torch.cuda.current_stream().cuda_stream
         conv = [a.data_ptr() if hasattr(a, "data_ptr") else a for a in args]
@@ -436,6 +442,9 @@ def recompress_gpu(tree, n: int, lowrank: list, dense: list, eps_rec: float, wei
         op.coupling.append((int(bt[i]), int(bs[i]), Sh[soff[i]:soff[i + 1]].reshape(int(kr[bt[i]]), int(kc[bs[i]]))))
     for t, s, m in dense:
         op.near.append((t, s, m))
+    del S, Qr, Qc, Qr_parts, Qc_parts, sides
+    if hasattr(ops, "release"):
+        ops.release()
     if timings is not None:
         timings["rec_coupling"] = time.perf_counter() - t4
         timings["rec_total"] = time.perf_counter() - t0

@@ -136,6 +136,7 @@ struct KParams {
   // capacities (doubles; items) the launch was sized for
   const int64_t* __restrict__ u_range;
   int32_t cap_mat, cap_vec, cap_items;
+  int32_t sweep_prefetch;               // generic sweep: the next item's static inputs prefetched to L2
 };
 
 // scheduling switches
@@ -1772,6 +1773,9 @@ __device__ __forceinline__ DTask load_task(const DTask* t) {
 __device__ __forceinline__ void prefetch_l1(const void* q) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
 }
+__device__ __forceinline__ void prefetch_l2(const void* q) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+}
 
 // The generic sweep: units are claimed from one counter; a warp stages its
 // items' matrices through two shared-memory buffers by TMA bulk copies and
@@ -1868,8 +1872,27 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_sweep_kern
         // one runs, and the descriptor after that towards L1
         pf_mode = 0;
         if (nx >= 0) {
+          const DTask N = load_task(p.tasks + nx);
+          // the next item's inputs that earlier launches left in DRAM, towards
+          // L2 while this item runs: its bias slots (near-field partial sums,
+          // coupling sums), the finals' permutation entries, its range of x.
+          // Otherwise the item pays them as dependent misses, one after the
+          // other (bias, sources, permutation).
+          if (p.sweep_prefetch) {
+            const int rl = (N.m * NRHS * 8 + 127) / 128 + 1;
+            if ((p.sweep_prefetch & 2) && N.bias >= 0 && lane < rl) {
+              const int ns = min(N.bias_nslots, 32);
+              for (int s2 = 0; s2 < ns; ++s2)
+                prefetch_l2(p.coef + (N.bias + (int64_t)s2 * N.bias_stride) * NRHS + lane * 16);
+            }
+            if ((p.sweep_prefetch & 4) && N.kind == h2b::kFinal && lane < (N.m * 8 + 127) / 128 + 1) prefetch_l2(p.perm + N.out + lane * 16);
+            if ((p.sweep_prefetch & 1) && lane < kInlineSegs && lane < N.seg1 - N.seg0 && N.seg1 - N.seg0 <= kInlineSegs) {
+              const DSeg ns = p.seg_inline[(int64_t)nx * kInlineSegs + lane];
+              if (ns.kind == h2b::kSegX)
+                for (int o = 0; o < ns.ncols * NRHS + 15; o += 16) prefetch_l2(p.xp + ns.src * NRHS + o);
+            }
+          }
           if (mode == 1) {
-            const DTask N = load_task(p.tasks + nx);
             uintptr_t n0 = 0;
             const unsigned nb = span(N, n0);
             if (nb > 0 && nb <= (unsigned)kSweepStage) {
@@ -2279,6 +2302,7 @@ struct h2b_op {
   int ring_warps = 0;  // NRHS < 8: TMA-ring warps per CTA (sched_flags bits 4-7)
   int sched = 0;       // effective sched_flags (defaults applied)
   int ring_stage = kRingStageBytes;  // NRHS < 8: ring stage payload (sched_flags bits 18-19)
+  int sweep_prefetch = 0;            // generic sweep: L2 prefetch of the next item's static inputs (H2B_SWEEP_PREFETCH mask)
   std::vector<PhaseDev> ph;
   // single GPU, 8/16 right-hand sides: near field (lean kernel), then the rest
   std::vector<PhaseDev> ph_split;
@@ -2508,6 +2532,7 @@ KParams phase_params(h2b_op* op, const PhaseDev& F, double* y) {
   p.cap_mat = F.cap_mat;
   p.cap_vec = F.cap_vec;
   p.cap_items = F.cap_items;
+  p.sweep_prefetch = op->sweep_prefetch;
   return p;
 }
 
@@ -2909,6 +2934,13 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   {
     const int sel = (sf >> 18) & 3;
     op->ring_stage = sel == 1 ? 6144 : sel == 2 ? 4096 : kRingStageBytes;
+    {
+      const char* e = std::getenv("H2B_SWEEP_PREFETCH");  // A/B switch, read at create (tools/sweep.py --env)
+      // bit 0: x ranges, 1: bias slots, 2: permutation entries.  Off by default: measured on
+      // config 3 the up sweep gets faster (0.110 -> 0.093 ms) but the product does not
+      // (2.263 ms off, 2.279 / 2.264 / 2.266 / 2.275 ms with masks 1 / 2 / 4 / 3)
+      op->sweep_prefetch = e ? std::atoi(e) : 0;
+    }
   }
   op->rank = P.rank;
   op->world = P.world_size;

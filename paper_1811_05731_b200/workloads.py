@@ -66,9 +66,11 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     The cache only saves build time; it is keyed by the workload recipe."""
     w = WORKLOADS[name]
     backend = w.get("backend", "numpy")
-    # H2B_RECOMPRESS=gpu: the recompression on the device too (assembly/gpu_recompress.py);
-    # a kept rank can differ at the threshold, so those operators are cached apart
-    rec = os.environ.get("H2B_RECOMPRESS", "host") if backend == "gpu" else "host"
+    # the recompression runs on the device too (assembly/gpu_recompress.py) for the
+    # GPU-built workloads; H2B_RECOMPRESS=host selects the host-thread restatement
+    # (recompress.py).  Config 3 gets the same ranks either way, but a kept rank can
+    # differ at the threshold, so the two are cached apart.
+    rec = os.environ.get("H2B_RECOMPRESS", "gpu") if backend == "gpu" else "host"
     recipe = (name, w["desc"], w["cfg"], 1, backend) + ((rec,) if rec != "host" else ())
     key = hashlib.sha256(repr(recipe).encode()).hexdigest()[:16]
     path = Path(cache_dir) / f"h2b_{name}_{key}" if cache_dir else None
@@ -86,7 +88,7 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
     op, rep = assemble_h2(surf, w["cfg"], workers=workers, log=lambda m: log(f"[workload] {name}: {m}"),
                           backend=backend, recompress_backend=rec)
     info = {"cached": False, "n": surf.n, "build_seconds": rep.seconds, "n_admissible": rep.n_admissible,
-            "n_dense": rep.n_dense, "n_fallback": rep.n_fallback, "coords": surf.coords}
+            "n_dense": rep.n_dense, "n_fallback": rep.n_fallback, "coords": surf.coords, "surface": surf}
     if path is not None:
         try:
             save_cached(op, path, coords=surf.coords)
@@ -152,3 +154,21 @@ def z_over_3(coords: np.ndarray) -> np.ndarray:
     """u1 = z/3 per node (BASELINE.json configs 1 and 5: the interior
     potential of a uniformly magnetized unit sphere, M = (0, 0, 1))."""
     return np.ascontiguousarray(np.asarray(coords)[:, 2] / 3.0)
+
+
+def exact_rows(surface, nodes: np.ndarray) -> np.ndarray:
+    """Rows ``nodes`` of the uncompressed operator M = K + D (bem.py:221-235:
+    collocated double layer plus the solid-angle diagonal), in node order, by
+    the GPU collocation kernel (csrc/colloc.cu): the yardstick for the
+    compression error of a built operator (len(nodes) x N)."""
+    from .assembly.hbuild import GpuCollocation, incidence, panel_table
+    ev = GpuCollocation(surface, panel_table(surface), incidence(surface))
+    try:
+        nodes = np.asarray(nodes, np.int64)
+        n = surface.n
+        out = ev.rows(surface.coords[nodes], np.zeros(nodes.size, np.int64), np.full(nodes.size, n, np.int32),
+                      nodes, np.arange(nodes.size, dtype=np.int64) * n, np.arange(n, dtype=np.int64),
+                      nodes.size * n)
+        return out.reshape(nodes.size, n)
+    finally:
+        ev.close()
