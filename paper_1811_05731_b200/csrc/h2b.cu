@@ -146,6 +146,7 @@ constexpr int kFlagReleaseArrivals = 1 << 2;  // release-only arrival atomics, a
 constexpr int kFlagStreamEvictFirst = 1 << 25;  // ring copies with an L2 evict-first hint
 constexpr int kFlagMixInner = (int)(1u << 31);  // near-priority warps' mix serves inner coupling rows too
 constexpr int kFlagMrhsRingAll = 2;  // 8/16 RHS: far items through the ring too (TMA sources), not staged whole
+constexpr int kFlagMrhsSrcInStage = 1 << 4;  // 8/16 RHS rings: TMA-moved sources behind the matrix chunk in the stage
 constexpr int kFlagUpMix = 1 << 3;   // near-priority warps' mix takes up-leaf items first (H2B_UP_MIX=1)
 constexpr int kFlagPrioNoChain = 1 << 30;       // near-priority warps leave the chain queue to the others
 constexpr int kChunkBytes = 4096;  // per-warp shared staging of gathered sources
@@ -890,10 +891,6 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   constexpr int NT = NRHS / 8;
   const int m = T.m;
   const int g = lane >> 2, t = lane & 3;
-  // columns per stage (>= 16), a whole number of 4-column k-steps so that
-  // the DMMA sums group columns exactly like the register-staged loop
-  const int cs = min(kHalf, STAGE / (8 * m)) & ~3;  // multi-RHS rings: 8 KB stages (4 KB: lean kernel option)
-  const int nch = (T.ncols + cs - 1) / cs;
   const double* g0 = p.mat + T.data;
   load_segtable(p, T, sin, w, lane);
   // Sources by TMA too when every segment is one contiguous range: x (a
@@ -903,6 +900,19 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   const int nseg = T.seg1 - T.seg0;
   const bool tma_src = __all_sync(0xffffffffu, lane >= nseg || w.seg_kind[lane] == h2b::kSegX ||
                                                    w.seg_nslots[lane] == 1);
+  // columns per stage, a whole number of 4-column k-steps so that the DMMA
+  // sums group columns exactly like the register-staged loop.  The sources
+  // of a chunk sit in the warp's source buffer (two halves of kHalf columns)
+  // or, when they come by TMA and the item has few rows, behind the matrix
+  // chunk inside the ring stage itself: a 16-row item then moves 32 columns
+  // per stage instead of 16 -- half the round trips of the latency-bound far
+  // field (ranks are ~16: most up, transfer and coupling items).
+  const int cs_buf = min(kHalf, STAGE / (8 * m)) & ~3;
+  const int cs_stage = (p.flags & kFlagMrhsSrcInStage) ? (min(64, STAGE / (8 * (m + NRHS))) & ~3) : 0;
+  const bool src_in_stage = tma_src && cs_stage > cs_buf;
+  const int cs = src_in_stage ? cs_stage : cs_buf;
+  const int soff = (cs * m + 3) & ~1;  // doubles: behind the chunk (which may start 8 bytes into the stage)
+  const int nch = (T.ncols + cs - 1) / cs;
   int kseg_tma = 0;  // lane 0: segment cursor of the TMA source copies
   auto issue = [&](int j) {  // lane 0: chunk j into stage j % 2
     const double* src = g0 + (int64_t)j * cs * m;
@@ -918,7 +928,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     if (p.flags & kFlagStreamEvictFirst) bulk_copy_hint(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j),
                                                         evict_first_policy());
     else bulk_copy(R.buf(j), (const void*)a0, (unsigned)(a1 - a0), R.bar(j));
-    double* xs = w.xs + (j & 1) * kHalf * NRHS;
+    double* xs = src_in_stage ? R.buf(j) + soff : w.xs + (j & 1) * kHalf * NRHS;
     const int col = j * cs;
     int c = col;
     while (c < col + cc) {
@@ -970,7 +980,7 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
     rpar ^= 1u << s;
     if (p.trace && jc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gath)::"memory");
     const double* A = R.buf(s) + ((((uintptr_t)(g0 + (int64_t)col * m)) & 15) >> 3);
-    const double* xs = w.xs + (jc & 1) * kHalf * NRHS;
+    const double* xs = src_in_stage ? R.buf(s) + soff : w.xs + (jc & 1) * kHalf * NRHS;
     for (int c = 0; c < cc; c += 4) {
       const bool okc = c + t < cc;
       double a[MT][2];
@@ -2929,6 +2939,9 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     if (!(ra && ra[0] == '0')) op->flags |= kFlagMrhsRingAll;
     const char* um = std::getenv("H2B_UP_MIX");
     if (um && um[0] == '1') op->flags |= kFlagUpMix;
+    // ... and the TMA-moved sources of few-row items inside the ring stage (twice the columns per stage)
+    const char* ss = std::getenv("H2B_MRHS_SRC_IN_STAGE");
+    if (!(ss && ss[0] == '0')) op->flags |= kFlagMrhsSrcInStage;
   }
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {

@@ -91,10 +91,32 @@ def build_workload(name: str, *, cache_dir: str | None = None, log=print, worker
             "n_dense": rep.n_dense, "n_fallback": rep.n_fallback, "coords": surf.coords, "surface": surf}
     if path is not None:
         try:
-            save_cached(op, path, coords=surf.coords)
+            if _make_room(Path(cache_dir), name, path, int(op.storage_bytes() * 1.02) + (64 << 20), log):
+                save_cached(op, path, coords=surf.coords)
         except OSError:
             pass
     return op, info
+
+
+def _make_room(cache: Path, name: str, keep: Path, need: int, log) -> bool:
+    """Free space for a cache entry of ``need`` bytes: unfinished entries
+    (no DONE marker) go first, then older recipes of the same workload.
+    The cache is written through memory maps, and a full disk there is a
+    SIGBUS, not an OSError -- so check before writing."""
+    import shutil
+    os.makedirs(cache, exist_ok=True)
+    for d in cache.glob("h2b_*"):
+        if d.is_dir() and not (d / "DONE").exists():
+            shutil.rmtree(d, ignore_errors=True)
+    if shutil.disk_usage(cache).free < need:
+        for d in cache.glob(f"h2b_{name}_*"):
+            if d.is_dir() and d != keep:
+                shutil.rmtree(d, ignore_errors=True)
+    free = shutil.disk_usage(cache).free
+    if free < need:
+        log(f"[workload] {name}: not cached ({free / 1e9:.1f} GB free under {cache}, {need / 1e9:.1f} GB needed)")
+        return False
+    return True
 
 
 def save_cached(op, path: Path, coords=None) -> None:
