@@ -92,6 +92,37 @@ class GpuCG:
         nat.check(rc, "h2b_cg_solve")
         return x, SolveReport(int(it.value), float(res.value), float(res.value) <= tol)
 
+    def solve_dev(self, b, tol: float = 1e-10, max_iter: int | None = None, deflate_constants: bool = False):
+        """The same solve with the right-hand side and the solution in device
+        memory (torch float64 CUDA tensors; ``h2b_cg_solve_dev`` on the
+        current stream): what ``pipeline.compute_demag`` chains with the H²
+        product without leaving the GPU.  The caller checks the deflated
+        right-hand side's compatibility (solver.py:68-70)."""
+        import torch
+        n = self.n
+        if b.shape != (n,) or b.dtype != torch.float64 or not b.is_cuda:
+            raise ValueError(f"rhs must be a float64 CUDA tensor of shape ({n},)")
+        if max_iter is None:
+            max_iter = 10 * n
+        b = b.contiguous()
+        x = torch.zeros_like(b)
+        b_norm = float(torch.linalg.vector_norm(b))
+        if b_norm == 0.0:
+            return x, SolveReport(0, 0.0, True)
+        if max_iter <= 0:
+            r = b - b.mean() if deflate_constants else b
+            res = float(torch.linalg.vector_norm(r)) / b_norm
+            return x, SolveReport(0, res, res <= tol)
+        it = C.c_int64(0)
+        res = C.c_double(0.0)
+        rc = self._lib.h2b_cg_solve_dev(self._h, b.data_ptr(), x.data_ptr(), float(tol), int(bool(deflate_constants)),
+                                        int(max_iter), C.byref(it), C.byref(res),
+                                        torch.cuda.current_stream().cuda_stream)
+        if rc == nat.H2B_ECONV:
+            raise ConvergenceError(self._lib.h2b_last_error().decode())
+        nat.check(rc, "h2b_cg_solve_dev")
+        return x, SolveReport(int(it.value), float(res.value), float(res.value) <= tol)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.h2b_cg_destroy(self._h)

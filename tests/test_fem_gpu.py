@@ -146,6 +146,39 @@ def test_reference_pipeline_with_gpu_solves_and_product():
 
 
 @gpu
+@pytest.mark.skipif(not (ROOT / "baseline" / "_ref" / "strayfield").exists(),
+                    reason="baseline/_ref not vendored (tools/vendor_reference.sh)")
+def test_device_pipeline_matches_reference_pipeline():
+    """``paper_1811_05731_b200.pipeline.compute_demag`` -- both solves and
+    the H² product chained in device memory -- against the unmodified
+    reference's compute_demag (pipeline.py:46-63) on the config-1 sphere:
+    the energy to 1e-9, the potentials to the solve tolerance."""
+    _cuda()
+    from oracle.reference import strayfield, to_reference
+    strayfield()
+    from strayfield import fem as rfem, mesh as rmesh, pipeline as rpipe
+    from strayfield.bem import BoundaryOperator
+    from paper_1811_05731_b200 import pipeline
+    op, ex = load_golden("config1_sphere4")
+    mesh = rmesh.generate_sphere_mesh(1.0, 4)
+    bop = BoundaryOperator(backend="h2", n=op.n, diag=np.zeros(op.n), payload=to_reference(op))
+    m = rpipe.magnetization_preset(mesh, "uniform-z")
+    want = rpipe.compute_demag(mesh, m, bop)          # the reference, on the CPU
+    got = pipeline.compute_demag(mesh, m, bop, fem=rfem)
+    assert isinstance(got, rpipe.PipelineResult)
+    ref = float(ex["energy_e_d_over_kd"])
+    assert abs(got.e_d_over_kd - ref) <= 1e-9 * abs(ref)
+    assert abs(got.e_d_over_kd - want.e_d_over_kd) <= 1e-9 * abs(ref)
+    assert abs(got.u1_iterations - want.u1_iterations) <= 2 and abs(got.u2_iterations - want.u2_iterations) <= 2
+    assert rel(got.u1, want.u1) <= 1e-8 and rel(got.u2, want.u2) <= 1e-8 and rel(got.u, want.u) <= 1e-8
+    assert got.h_field.shape == want.h_field.shape and rel(got.h_field, want.h_field) <= 1e-7
+    # contract: only the H² backend runs on the device
+    dense = BoundaryOperator(backend="dense", n=op.n, diag=np.zeros(op.n), payload=np.eye(op.n))
+    with pytest.raises(NotImplementedError):
+        pipeline.compute_demag(mesh, m, dense, fem=rfem)
+
+
+@gpu
 def test_gpu_cg_kernel_variants(monkeypatch):
     """Every kernel variant of csrc/cg.cu (H2B_CG_VARIANT, read when the
     solver is created) solves the same system to the oracle's solution.

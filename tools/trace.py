@@ -52,9 +52,16 @@ def main():
     split = a.nrhs >= 8 and os.environ.get("H2B_NEAR_SPLIT", "1") != "0"
     if split:   # trace the dataflow part of the split multi-RHS product
         os.environ["H2B_TRACE_SPLIT"] = "1"
-        pv = plan_view(op, **dict(opts, plan_flags=opts.get("plan_flags", 0) | 4))
-        plan = pv["phases"][2]
-        plan["stats"] = pv["stats"]
+        # the split product's dataflow part is the last launch of the view;
+        # 8/16 right-hand sides may run the classic (unstaged) split plan:
+        # the candidate whose size the library accepts is the one traced
+        cands = []
+        for extra in (4, 4 | 2048):
+            pv = plan_view(op, **dict(opts, plan_flags=opts.get("plan_flags", 0) | extra))
+            ph = pv["phases"][-1]
+            ph["stats"] = pv["stats"]
+            cands.append(ph)
+        plan = cands[0]
     else:
         pv = plan_view(op, **opts)
         k = a.phase if a.phase >= 0 else [ph["mode"] for ph in pv["phases"]].index(0)
@@ -76,6 +83,12 @@ def main():
     for _ in range(3):
         dev.matvec_dev(x.data_ptr(), y.data_ptr(), nrhs, s)
     torch.cuda.synchronize()
+    if split:
+        for ph in cands:
+            tr = np.zeros((ph["t_m"].size, 8), np.uint64)
+            if lib.h2b_trace_read(dev._h, tr.ctypes.data, ph["t_m"].size) == 0:
+                plan = ph
+                break
     T = plan["t_m"].size
     tr = np.zeros((T, 8), np.uint64)
     nat.check(lib.h2b_trace_read(dev._h, tr.ctypes.data, T))
