@@ -125,6 +125,7 @@ struct KParams {
   int32_t flags;                        // kFlag* scheduling switches (h2b_options.sched_flags)
   int32_t ring_warps;                   // NRHS < 8: warps per CTA (the top ones) with a TMA ring
   int32_t ring_stage;                   // NRHS < 8: ring stage payload bytes (8192, 6144, 4096)
+  int32_t mrhs_stage;                   // NRHS >= 8: ring stage payload bytes (8192; 6144 with 12 warps per CTA)
   unsigned long long* trace;            // diagnostics: per item {start ns, end ns, sm|warp, 0}
   const int32_t* __restrict__ gated;    // gated coupling rows (Phase::gated)
   int32_t ngated, ngated1, nup_gate;
@@ -177,16 +178,26 @@ struct __align__(128) WarpSmem {
 // KB for single-vector products (sched_flags bits 18-19), which lets more
 // warps of a CTA own a ring at two CTAs per SM.
 constexpr int kRingStageBytes = 8192;
-// 8/16 right-hand sides in the dataflow and sweep kernels: DMMA tiles over 64
-// rows per pass and 8 KB ring stages, one CTA of eight warps per SM.  The
-// lean alternative -- 32 rows per pass (kMrhsMT 2: half the accumulator
-// registers, items above 32 rows in two passes), 4 KB stages, two CTAs per
-// SM at 128 registers -- measured slower on config 3 (16 RHS 4.57 -> 5.35 ms,
-// 8 RHS 3.55 -> 4.07 ms: spills and the second pass cost more than the extra
-// warps hide), so it stays a compile-time option.
-constexpr int kMrhsMT = 4;
+// 8/16 right-hand sides in the dataflow and sweep kernels: one CTA per SM.
+// The far part of such a product is latency-bound (150 k small items on
+// config 3), so warps per SM are what counts, and registers decide them:
+//   MT 4 (64 rows per pass), 256 threads, 255 registers    16 RHS 4.555 ms
+//   MT 4, 384 threads at 168 registers: 2.2 KB of spills   5.27 ms (12 warps)
+//   MT 2 (32 rows per pass; taller items in two passes),
+//        384 threads at 168 registers, 6 KB ring stages     4.248 ms, 8 RHS 3.598 -> 3.394 ms
+//   MT 2, 256 threads x 2 CTAs at 128 registers, 4 KB stages: spills, 5.35 ms
+// (profiles/r02_config3_mrhs_warps.jsonl).  H2B_MRHS_WARPS launches fewer
+// warps than compiled for.
+#ifndef H2B_MRHS_MT
+#define H2B_MRHS_MT 2
+#endif
+#ifndef H2B_MRHS_THREADS
+#define H2B_MRHS_THREADS 384
+#endif
+constexpr int kMrhsMT = H2B_MRHS_MT;
 constexpr int kMrhsStage = 8192;
-constexpr int kMrhsCtas = kMrhsMT >= 4 ? 1 : 2;
+constexpr int kMrhsCtas = (kMrhsMT >= 4 || H2B_MRHS_THREADS > 256) ? 1 : 2;
+constexpr int kMrhsThreads = H2B_MRHS_THREADS;
 struct WarpRing {  // view into dynamic shared memory (no dynamically indexed arrays)
   double* base;     // stage 0; stage 1 follows at base + sdbl
   uint64_t* bars;   // two mbarriers
@@ -907,8 +918,9 @@ __device__ __forceinline__ void run_item_mma_ring(const KParams& p, const DTask&
   // chunk inside the ring stage itself: a 16-row item then moves 32 columns
   // per stage instead of 16 -- half the round trips of the latency-bound far
   // field (ranks are ~16: most up, transfer and coupling items).
-  const int cs_buf = min(kHalf, STAGE / (8 * m)) & ~3;
-  const int cs_stage = (p.flags & kFlagMrhsSrcInStage) ? (min(64, STAGE / (8 * (m + NRHS))) & ~3) : 0;
+  const int stage = R.sdbl * 8 - 32;  // the ring's stage payload (STAGE, or the run-time multi-RHS stage)
+  const int cs_buf = min(kHalf, stage / (8 * m)) & ~3;
+  const int cs_stage = (p.flags & kFlagMrhsSrcInStage) ? (min(64, stage / (8 * (m + NRHS))) & ~3) : 0;
   const bool src_in_stage = tma_src && cs_stage > cs_buf;
   const int cs = src_in_stage ? cs_stage : cs_buf;
   const int soff = (cs * m + 3) & ~1;  // doubles: behind the chunk (which may start 8 bytes into the stage)
@@ -1163,7 +1175,7 @@ __device__ __forceinline__ void run_item_ring_multi(const KParams& p, const DTas
 }
 
 template <int NRHS>
-__global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_dataflow_kernel(KParams p) {
+__global__ void __launch_bounds__(NRHS >= 8 ? kMrhsThreads : 256, NRHS >= 8 ? kMrhsCtas : 2) h2b_dataflow_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1177,7 +1189,7 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_dataflow_k
   // staging: a TMA ring (ring warps) or one far-field buffer
   const int nring = NRHS >= 8 ? nw : p.ring_warps;
   const int first_ring = nw - nring;
-  const int rstage = NRHS >= 8 ? kMrhsStage : p.ring_stage;
+  const int rstage = NRHS >= 8 ? p.mrhs_stage : p.ring_stage;
   WarpRing ring_v{nullptr, nullptr, 0};
   bool has_ring = false;
   double* abuf;
@@ -2312,6 +2324,8 @@ struct h2b_op {
   int ring_warps = 0;  // NRHS < 8: TMA-ring warps per CTA (sched_flags bits 4-7)
   int sched = 0;       // effective sched_flags (defaults applied)
   int ring_stage = kRingStageBytes;  // NRHS < 8: ring stage payload (sched_flags bits 18-19)
+  int mrhs_wpc = 8;                  // 8/16 RHS dataflow launches: warps per CTA (H2B_MRHS_WARPS, <= 12)
+  int mrhs_stage = kMrhsStage;       // ... and their ring stage payload (6 KB above 10 warps: shared memory)
   int sweep_prefetch = 0;            // generic sweep: L2 prefetch of the next item's static inputs (H2B_SWEEP_PREFETCH mask)
   std::vector<PhaseDev> ph;
   // single GPU, 8/16 right-hand sides: near field (lean kernel), then the rest
@@ -2468,7 +2482,8 @@ int nrhs_index(int nrhs) {
 
 template <int NRHS>
 int occupancy_grid(int wpc, int ring_warps, int ring_stage, int ctas_per_sm, int* grid) {
-  const size_t sm = NRHS >= 8 ? smem_bytes(wpc, wpc, kMrhsStage) : smem_bytes(wpc, ring_warps, ring_stage);
+  // NRHS >= 8: wpc and ring_stage are the multi-RHS launch's (h2b_op::mrhs_wpc, mrhs_stage)
+  const size_t sm = NRHS >= 8 ? smem_bytes(wpc, wpc, ring_stage) : smem_bytes(wpc, ring_warps, ring_stage);
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
   H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2b_dataflow_kernel<NRHS>, wpc * 32, sm));
@@ -2535,6 +2550,7 @@ KParams phase_params(h2b_op* op, const PhaseDev& F, double* y) {
   p.flags = op->flags;
   p.ring_warps = op->ring_warps;
   p.ring_stage = op->ring_stage;
+  p.mrhs_stage = op->mrhs_stage;
   p.unit0 = F.d_unit0;
   p.wave0 = F.d_wave0;
   p.nunits = F.nunits;
@@ -2552,16 +2568,17 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) 
   if (F.ntasks == 0) return H2B_OK;
   const KParams p = phase_params<NRHS>(op, F, y);
   const int gi = nrhs_index(NRHS);
-  const size_t smem = NRHS >= 8 ? smem_bytes(op->wpc, op->wpc, kMrhsStage)
+  const int wpc = NRHS >= 8 ? op->mrhs_wpc : op->wpc;
+  const size_t smem = NRHS >= 8 ? smem_bytes(wpc, wpc, op->mrhs_stage)
                                 : smem_bytes(op->wpc, op->ring_warps, op->ring_stage);
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   // the attribute is per function and shared by every operator of the process
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  h2b_dataflow_kernel<NRHS><<<op->grid[gi], op->wpc * 32, smem, st>>>(p);
+  h2b_dataflow_kernel<NRHS><<<op->grid[gi], wpc * 32, smem, st>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
-                               std::to_string(op->grid[gi]) + ", block=" + std::to_string(op->wpc * 32) +
+                               std::to_string(op->grid[gi]) + ", block=" + std::to_string(wpc * 32) +
                                ", smem=" + std::to_string(smem) +
                                "): " + cudaGetErrorString(e) + " (stale: " + cudaGetErrorString(stale) + ")");
   return H2B_OK;
@@ -2942,6 +2959,10 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     // ... and the TMA-moved sources of few-row items inside the ring stage (twice the columns per stage)
     const char* ss = std::getenv("H2B_MRHS_SRC_IN_STAGE");
     if (!(ss && ss[0] == '0')) op->flags |= kFlagMrhsSrcInStage;
+    // ... on H2B_MRHS_WARPS warps per SM (one CTA; 12 warps: 168 registers each, 6 KB ring stages)
+    const char* mw = std::getenv("H2B_MRHS_WARPS");
+    op->mrhs_wpc = mw ? std::max(1, std::min(kMrhsThreads / 32, std::atoi(mw))) : kMrhsThreads / 32;
+    op->mrhs_stage = op->mrhs_wpc > 12 ? 4096 : op->mrhs_wpc > 10 ? 6144 : kMrhsStage;
   }
   op->ring_warps = std::min((sf >> 4) & 0xf, op->wpc);
   {
@@ -2986,8 +3007,8 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   if ((rc = occupancy_grid<1>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[0]))) return rc;
   if ((rc = occupancy_grid<2>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[1]))) return rc;
   if ((rc = occupancy_grid<4>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[2]))) return rc;
-  if ((rc = occupancy_grid<8>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[3]))) return rc;
-  if ((rc = occupancy_grid<16>(op->wpc, op->ring_warps, op->ring_stage, cps, &op->grid[4]))) return rc;
+  if ((rc = occupancy_grid<8>(op->mrhs_wpc, op->mrhs_wpc, op->mrhs_stage, cps, &op->grid[3]))) return rc;
+  if ((rc = occupancy_grid<16>(op->mrhs_wpc, op->mrhs_wpc, op->mrhs_stage, cps, &op->grid[4]))) return rc;
   H2B_CUDA(cudaDeviceGetAttribute(&op->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
   H2B_CUDA(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, op->device));
   {
