@@ -351,3 +351,66 @@ def test_level_skipping_chain_on_gpu(golden, nrhs, flags):
             ref = h2_matvec_ref(o, X[:, i])
             if np.linalg.norm(ref) > 0:
                 assert rel(Y[:, i], ref) <= TOL, (name, i)
+
+
+@pytest.mark.gpu
+def test_host_entry_staged_copies_large_vector(monkeypatch):
+    """h2b_matvec stages vectors of >= 1 MB through pinned memory with copy
+    threads (pageable numpy arrays are what apply_operator / compute_demag
+    pass).  A block-diagonal operator with 163 840 nodes: the staged path
+    (default), the plain path (H2B_COPY_THREADS=0) and numpy agree; several
+    chunk counts, 1 and 2 right-hand sides, repeated calls."""
+    from paper_1811_05731_b200.cluster import Cluster, ClusterTree
+    from paper_1811_05731_b200.h2 import DeviceOperator, H2Matrix
+    rng = np.random.default_rng(5)
+    leaf, nleaf = 32, 5120
+    n = leaf * nleaf
+    clusters = []
+
+    def build(lo, hi):
+        c = Cluster(lo * leaf, hi * leaf, np.zeros(3), np.ones(3))
+        c.cid = len(clusters)
+        clusters.append(c)
+        if hi - lo > 1:
+            mid = (lo + hi) // 2
+            c.children = (build(lo, mid), build(mid, hi))
+        return c
+
+    root = build(0, nleaf)
+    tree = ClusterTree(root=root, perm=rng.permutation(n).astype(np.int64), clusters=clusters)
+    op = H2Matrix(tree=tree, n=n)
+    blocks = rng.standard_normal((nleaf, leaf, leaf))
+    for c in clusters:
+        if c.is_leaf:
+            op.row_basis[c.cid] = np.zeros((leaf, 0))
+            op.col_basis[c.cid] = np.zeros((leaf, 0))
+            op.near.append((c.cid, c.cid, blocks[c.start // leaf]))
+        for ch in c.children:
+            op.row_transfer[ch.cid] = np.zeros((0, 0))
+            op.col_transfer[ch.cid] = np.zeros((0, 0))
+
+    def ref(x):
+        xp = x[tree.perm].reshape(nleaf, leaf, -1)
+        yp = np.einsum("bij,bjr->bir", blocks, xp).reshape(n, -1)
+        y = np.empty_like(yp)
+        y[tree.perm] = yp
+        return y.reshape(x.shape)
+
+    outs = {}
+    for threads in ("", "0", "2", "7"):
+        if threads:
+            monkeypatch.setenv("H2B_COPY_THREADS", threads)
+        else:
+            monkeypatch.delenv("H2B_COPY_THREADS", raising=False)
+        dev = DeviceOperator(op)
+        try:
+            for nrhs in (1, 2):
+                x = rng.standard_normal((n, nrhs)) if nrhs > 1 else rng.standard_normal(n)
+                for _ in range(3):
+                    y = dev.matvec(x)
+                assert rel(y, ref(x)) < 1e-13
+            x1 = np.arange(n, dtype=np.float64) / n
+            outs[threads] = dev.matvec(x1)
+        finally:
+            dev.close()
+    assert all(np.array_equal(outs[""], v) for v in outs.values())
