@@ -2309,12 +2309,14 @@ struct PhaseDev {
   int cap_mat = 0, cap_vec = 0, cap_items = 0;
 };
 
-// Host threads for the staged copies of h2b_matvec: the callers' vectors are
-// pageable numpy arrays (apply_operator, compute_demag), which the driver
-// copies through its own staging at ~18 GB/s (0.89 ms for the 8.3 MB pair of
-// config 3 against 0.32 ms from pinned memory).  Here chunks are copied by a
-// few threads into / out of a pinned buffer and moved by DMA as they become
-// ready, so the memcpy and the DMA overlap.
+// Host threads for the optional staged copies of h2b_matvec
+// (H2B_COPY_THREADS > 0): the callers' vectors are pageable numpy arrays
+// (apply_operator, compute_demag), which the driver copies through its own
+// staging at ~18 GB/s (0.89 ms for the 8.3 MB pair of config 3 against
+// 0.32 ms from pinned memory).  With this option chunks are copied by a few
+// threads into / out of a pinned buffer and moved by DMA as they become
+// ready, so the memcpy and the DMA overlap.  Measured no better than the
+// driver's path on the B200 box, hence off by default.
 class CopyPool {
  public:
   explicit CopyPool(int nthreads) {
@@ -2438,6 +2440,7 @@ struct h2b_op {
   std::vector<cudaEvent_t> chunk_ev;
   std::unique_ptr<CopyPool> pool;
   int copy_threads = -1;  // -1: not decided yet; 0: plain cudaMemcpyAsync from the caller's memory
+  size_t copy_chunk = (size_t)1 << 20;
   // One product in flight per operator: the scheduler state (queue heads,
   // arrival counters, epoch) and the coefficient workspace are per operator.
   // Every launch waits for the previous one's completion event, whatever
@@ -3397,12 +3400,30 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
   if (op->copy_threads < 0) {
     const char* e = std::getenv("H2B_COPY_THREADS");
     const int hw = (int)std::thread::hardware_concurrency();
-    op->copy_threads = e ? std::max(0, std::min(16, std::atoi(e))) : std::max(0, std::min(4, hw - 1));
+    // Off by default: on the 16-vCPU B200 box the threads' memcpy does not beat the
+    // driver's own staging (config 3, h2_matvec from pageable arrays: 2.90 ms plain,
+    // 2.87 / 2.86 ms with 4 / 8 threads and 1 MB chunks, 3.1-3.6 ms with 256 KB
+    // chunks; profiles/r02_config3_e2e_staged_copies.jsonl)
+    (void)hw;
+    op->copy_threads = e ? std::max(0, std::min(16, std::atoi(e))) : 0;
+    const char* ck = std::getenv("H2B_COPY_CHUNK_KB");
+    op->copy_chunk = (size_t)std::max(64, ck ? std::atoi(ck) : 1024) << 10;
   }
-  constexpr size_t kChunk = (size_t)1 << 20;  // bytes per staged chunk
-  const bool staged = op->copy_threads > 0 && bytes >= kChunk;
-  const int nchunks = staged ? (int)((bytes + kChunk - 1) / kChunk) : 0;
-  if (staged) {
+  const size_t kChunk = op->copy_chunk;  // bytes per staged chunk
+  // vectors already in page-locked memory go straight to the DMA engine
+  auto pinned = [](const void* q) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool big = op->copy_threads > 0 && bytes >= ((size_t)1 << 20);
+  const bool staged_x = big && !pinned(x_host);
+  const bool staged = big && !pinned(y_host);   // the output side
+  const int nchunks = (staged || staged_x) ? (int)((bytes + kChunk - 1) / kChunk) : 0;
+  if (staged || staged_x) {
     if (op->pin_cap < bytes) {
       if (op->pin_x) cudaFreeHost(op->pin_x);
       if (op->pin_y) cudaFreeHost(op->pin_y);
@@ -3418,6 +3439,8 @@ int h2b_matvec(h2b_op* op, const double* x_host, double* y_host, int64_t n, int 
       op->chunk_ev.push_back(ev);
     }
     if (!op->pool) op->pool.reset(new CopyPool(op->copy_threads - 1));
+  }
+  if (staged_x) {
     // x: each chunk is copied into pinned memory and handed to the DMA engine
     // by the thread that copied it (chunks are disjoint; their order is free)
     std::atomic<int> bad{0};

@@ -355,11 +355,11 @@ def test_level_skipping_chain_on_gpu(golden, nrhs, flags):
 
 @pytest.mark.gpu
 def test_host_entry_staged_copies_large_vector(monkeypatch):
-    """h2b_matvec stages vectors of >= 1 MB through pinned memory with copy
-    threads (pageable numpy arrays are what apply_operator / compute_demag
-    pass).  A block-diagonal operator with 163 840 nodes: the staged path
-    (default), the plain path (H2B_COPY_THREADS=0) and numpy agree; several
-    chunk counts, 1 and 2 right-hand sides, repeated calls."""
+    """h2b_matvec can stage vectors of >= 1 MB through pinned memory with
+    copy threads (H2B_COPY_THREADS; pageable numpy arrays are what
+    apply_operator / compute_demag pass).  A block-diagonal operator with
+    163 840 nodes: the plain path (default), the staged path with 2 and 7
+    threads and numpy agree; 1 and 2 right-hand sides, repeated calls."""
     from paper_1811_05731_b200.cluster import Cluster, ClusterTree
     from paper_1811_05731_b200.h2 import DeviceOperator, H2Matrix
     rng = np.random.default_rng(5)
