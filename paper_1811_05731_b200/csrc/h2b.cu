@@ -201,6 +201,12 @@ constexpr int kMrhsMT = H2B_MRHS_MT;
 constexpr int kMrhsStage = 8192;
 constexpr int kMrhsCtas = (kMrhsMT >= 4 || H2B_MRHS_THREADS > 256) ? 1 : 2;
 constexpr int kMrhsThreads = H2B_MRHS_THREADS;
+// The generic sweep kernel has no scheduler state: with 32-row passes it fits
+// 128 registers (16 RHS: 248 bytes of spills), two CTAs per SM.
+#ifndef H2B_MRHS_SWEEP_CTAS
+#define H2B_MRHS_SWEEP_CTAS 2
+#endif
+constexpr int kMrhsSweepCtas = H2B_MRHS_SWEEP_CTAS;
 struct WarpRing {  // view into dynamic shared memory (no dynamically indexed arrays)
   double* base;     // stage 0; stage 1 follows at base + sdbl
   uint64_t* bars;   // two mbarriers
@@ -1808,7 +1814,7 @@ __device__ __forceinline__ void prefetch_l2(const void* q) {
 // the current one runs.  Used when a unit's inputs do not fit shared memory
 // (large subtrees, many right-hand sides); see the resident kernel below.
 template <int NRHS>
-__global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsCtas : 2) h2b_sweep_kernel(KParams p) {
+__global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsSweepCtas : 2) h2b_sweep_kernel(KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -3013,6 +3019,13 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
   const int max_nrhs_req = (o && o->max_nrhs > 0) ? o->max_nrhs : 16;
   const char* ns_env = std::getenv("H2B_NEAR_SPLIT");
   po.near_split = po.world_size <= 1 && max_nrhs_req >= 8 && !(ns_env && ns_env[0] == '0');
+  {
+    // the split product's bottom subtrees as sweeps too (the generic sweep kernel fits two
+    // CTAs per SM at 8/16 RHS): config 3, 8 RHS 3.398 -> 3.014 ms, 16 RHS 4.247 -> 4.089 ms,
+    // the same bits.  H2B_SPLIT_SWEEPS=0: every far-field item in the dataflow launch.
+    const char* sw = std::getenv("H2B_SPLIT_SWEEPS");
+    po.split_sweeps = po.staged && !(sw && sw[0] == '0');
+  }
   int rc = h2b::build_plan(d, po, &P, &err);
   if (rc != H2B_OK) return fail(rc, err);
   for (const auto& F : P.ph) {

@@ -601,24 +601,24 @@ int Builder::run(std::string* err) {
   };
   // the launches of one group of selected items: [up sweep] dataflow [down
   // sweep]; with `split` the near field gets a launch of its own (mode 2)
-  // (the split multi-RHS product keeps every far-field item in its dataflow
-  // launch: sweeps of 8/16 right-hand sides run one CTA per SM and measured
-  // slower, 16 RHS on config 3 4.57 -> 5.09 ms)
+  // (the split multi-RHS product forms sweeps too with opt_.split_sweeps;
+  // with one sweep CTA per SM they had measured slower, with two faster)
   auto emit_launches = [&](std::vector<Phase>* out, const std::vector<char>& in, int32_t group, bool split) -> int {
     std::vector<int32_t> up, dn, near, rest;
     std::vector<char> in_near(T, 0), in_rest(T, 0);
+    const bool sweeps = !split || opt_.split_sweeps;
     for (int32_t i = 0; i < T; ++i) {
       if (!in[i]) continue;
       const TaskTmp& t = tasks_[i];
-      if (!split && in_up_sweep(t)) up.push_back(i);
-      else if (!split && in_down_sweep(t)) dn.push_back(i);
+      if (sweeps && in_up_sweep(t)) up.push_back(i);
+      else if (sweeps && in_down_sweep(t)) dn.push_back(i);
       else if (split && t.kind == kNear) { near.push_back(i); in_near[i] = 1; }
       else { rest.push_back(i); in_rest[i] = 1; }
     }
     // closure: the dataflow launch must not wait for an item of the down sweep
     for (int32_t i : rest)
       for (int32_t dp : tasks_[i].deps)
-        if (!split && in[dp] && in_down_sweep(tasks_[dp])) { *err = "internal: dataflow item depends on the down sweep"; return H2B_EINVAL; }
+        if (sweeps && in[dp] && in_down_sweep(tasks_[dp])) { *err = "internal: dataflow item depends on the down sweep"; return H2B_EINVAL; }
     int rc2 = H2B_OK;
     if (!up.empty()) {
       out->emplace_back();
@@ -631,7 +631,7 @@ int Builder::run(std::string* err) {
       out->back().mode = 2;
       out->back().group = group;
     }
-    if (!rest.empty() || (!split && up.empty() && dn.empty())) {
+    if (!rest.empty() || (!split && up.empty() && dn.empty()) || (split && sweeps)) {
       out->emplace_back();
       if ((rc2 = finalize(&out->back(), rest, in_rest, err)) != H2B_OK) return rc2;
       out->back().group = group;

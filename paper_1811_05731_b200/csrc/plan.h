@@ -189,6 +189,9 @@ struct PlanOptions {
   // coupling rows of bottom clusters have neither inputs to wait for nor
   // successors to notify.  Multi-GPU: ranks own whole subtrees.
   bool staged = false;
+  // the split multi-RHS product (near_split) also runs the bottom subtrees as
+  // sweeps: [up sweep] near kernel, dataflow launch [down sweep]
+  bool split_sweeps = false;
   int64_t sweep_nodes = 0;        // 0: default (about 256 subtrees per rank)
   int32_t rank = 0;
   int32_t world_size = 1;

@@ -354,16 +354,18 @@ def test_level_skipping_chain_on_gpu(golden, nrhs, flags):
 
 
 @pytest.mark.gpu
-def test_host_entry_staged_copies_large_vector(monkeypatch):
+def test_operator_beyond_l2_and_staged_host_copies(monkeypatch):
     """h2b_matvec can stage vectors of >= 1 MB through pinned memory with
     copy threads (H2B_COPY_THREADS; pageable numpy arrays are what
     apply_operator / compute_demag pass).  A block-diagonal operator with
-    163 840 nodes: the plain path (default), the staged path with 2 and 7
-    threads and numpy agree; 1 and 2 right-hand sides, repeated calls."""
+    327 680 nodes and 168 MB of near-field blocks -- larger than the 126 MB
+    L2, so every product streams from HBM, unlike the golden operators: the
+    plain path (default), the staged path with 2 and 7 threads and numpy
+    agree; 1 and 2 right-hand sides, repeated calls."""
     from paper_1811_05731_b200.cluster import Cluster, ClusterTree
     from paper_1811_05731_b200.h2 import DeviceOperator, H2Matrix
     rng = np.random.default_rng(5)
-    leaf, nleaf = 32, 5120
+    leaf, nleaf = 64, 5120
     n = leaf * nleaf
     clusters = []
 
