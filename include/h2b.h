@@ -81,7 +81,7 @@ typedef struct h2b_desc {
    whose near-field and coupling bytes per rank are at least
    H2B_STREAM_DEFAULT_BYTES gets the streaming defaults for the fields left
    zero: every warp a ring warp with 4 KB stages, 6 near-priority warps,
-   leaf mix 4, 8 KB far-field and 128 KB near-field pieces, evict-first
+   leaf mix 4, 8 KB far-field and 256 KB near-field pieces, evict-first
    ring copies; smaller operators,
    whose time is the far-field chain's latency, keep plain scheduling. */
 #define H2B_SCHED_EXPLICIT 8

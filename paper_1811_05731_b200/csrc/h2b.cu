@@ -2512,11 +2512,15 @@ h2b::PlanOptions to_plan_options(const h2b_desc* d, const h2b_options* o) {
   po.skip_levels = desc_stream_bytes_per_rank(d, o) < H2B_SKIP_DEFAULT_BYTES;
   // streaming operators: 8 KB chain pieces (a ring warp stages both ring
   // stages at once), halving the latency-bound up-leaf items
-  // and 128 KB near-field pieces (a ring warp keeps streaming across the
-  // whole item: fewer per-item round trips; config 3 2.47 -> 2.40 ms)
+  // and 256 KB near-field pieces (a ring warp keeps streaming across the
+  // whole item: fewer per-item round trips, and fewer partial-sum slots for
+  // the finals to add -- at 16 RHS a slot is 8 KB; config 3 with 128 / 192 /
+  // 256 / 384 KB: 2.264 / 2.251 / 2.238 / 2.92 ms -- 384 KB exceeds the 512
+  // gathered columns of a ring item -- 8 RHS 3.017 / 2.952 / 2.916 / 2.877,
+  // 16 RHS 4.086 / 3.947 / 3.858 / 3.777 ms)
   if (streaming_defaults(d, o)) {
     po.far_task_bytes = 8192;
-    po.task_bytes = 131072;
+    po.task_bytes = 262144;
   }
   if (o) {
     if (o->task_bytes > 0) po.task_bytes = o->task_bytes;

@@ -142,7 +142,7 @@ def test_effective_sched_flags_reported():
         dev.close()
 
 
-STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20) | (1 << 25), far_task_bytes=8192, task_bytes=131072)
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20) | (1 << 25), far_task_bytes=8192, task_bytes=262144)
 
 
 @pytest.mark.parametrize("nrhs", [2, 4])

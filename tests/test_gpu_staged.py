@@ -29,7 +29,7 @@ def _h2():
     return h2
 
 
-STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20) | (1 << 25), task_bytes=131072)
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20) | (1 << 25), task_bytes=262144)
 
 
 @pytest.mark.parametrize("nodes", [0, 1, 2, 4])

@@ -132,7 +132,7 @@ def test_two_processes_gloo(tmp_path):
 
 
 # the streaming defaults a large rank operator gets, forced
-STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20), far_task_bytes=8192, task_bytes=131072)
+STREAMING = dict(sched_flags=8 | (8 << 4) | (2 << 18) | (6 << 26) | (4 << 20), far_task_bytes=8192, task_bytes=262144)
 
 
 @pytest.mark.gpu

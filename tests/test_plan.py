@@ -50,7 +50,7 @@ def test_plan_far_and_near_ablations(golden):
 
 
 @pytest.mark.parametrize("opts", [dict(far_task_bytes=8192), dict(sched_flags=2), dict(sched_flags=2, far_task_bytes=8192),
-                                  dict(far_task_bytes=8192, task_bytes=131072)])
+                                  dict(far_task_bytes=8192, task_bytes=131072), dict(far_task_bytes=8192, task_bytes=262144)])
 def test_plan_streaming_options(golden, opts):
     """The planning side of the streaming defaults (8 KB far-field pieces,
     finals in the slack queue) keeps the product exact."""
