@@ -14,3 +14,8 @@ timeout 900 python bench.py --config config3 --nrhs 16 --steps 20 --warmup 5 --n
 timeout 900 python bench.py --config config2 --steps 50 --warmup 5 > gpurun_out/bench_config2.json 2> gpurun_out/bench_config2.err; echo "config2 rc=$?"; cut -c1-300 gpurun_out/bench_config2.json
 timeout 900 python bench.py --config config1 --steps 100 --warmup 5 > gpurun_out/bench_config1.json 2> gpurun_out/bench_config1.err; echo "config1 rc=$?"; cut -c1-300 gpurun_out/bench_config1.json
 timeout 900 python bench.py --impl reference --steps 16 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "reference arm rc=$?"; cut -c1-400 gpurun_out/bench_reference.json
+# config 5 (only when its operator is cached on this box: the build takes 10 minutes)
+if ls /tmp/h2b_cache/h2b_config5_*/DONE >/dev/null 2>&1; then
+timeout 1500 python bench.py --config config5 --steps 10 --warmup 3 > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err; echo "config5 rc=$?"; cut -c1-300 gpurun_out/bench_config5.json
+timeout 900 python bench.py --config config3 --nrhs 8 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_nrhs8.json 2> gpurun_out/bench_nrhs8.err; echo "nrhs8 rc=$?"
+fi
