@@ -45,6 +45,7 @@ product) or, in the CPU tests only, ``oracle/rc_ops_ref.py::NumpyOps``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 
 import numpy as np
@@ -232,46 +233,54 @@ class CudaOps:
         self._call("h2b_rc_coupling", nb, bt, bs, rcol, ccol, kb, Qr, qoffr, kr, Qc, qoffc, kc, S, soff)
 
 
-def _pack_side(ops, T: _Tree, sp: _SidePlan, cid, factors, weights, say):
+def _pack_side(ops, T: _Tree, sp: _SidePlan, cid, factors, weights, say, workers: int = 8):
     """Upload the side's factors: per cluster its own blocks side by side
-    (row-major |c| x cown[c]), through a pinned staging buffer."""
+    (row-major |c| x cown[c]), through a pinned staging buffer filled by a
+    few host threads (numpy's copy loops release the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
     total = int(sp.foff[-1])
     fac = ops.empty(total)
     wts = np.ones(max(1, int(sp.woff[-1])))
-    stage_n = 1 << 26  # 512 MB of doubles
+    stage_n = int(os.environ.get("H2B_RC_STAGE_DOUBLES", 1 << 26))  # 512 MB of doubles
     stage = ops.staging(min(max(total, 1), stage_n))
-    pos = 0           # device offset of stage[0]
-    fill = 0
     size = T.end - T.start
-    for c in np.flatnonzero(sp.cown > 0):
+    owners = np.flatnonzero(sp.cown > 0)
+
+    def fill_one(c, base):
+        """Cluster c's packed block into stage[foff[c] - base ...], and its weights."""
         blocks = sp.order[sp.first[c]:sp.first[c + 1]]
-        need = int(size[c] * sp.cown[c])
-        if need > stage.size:  # a block larger than the staging buffer goes on its own
-            if fill:
-                ops.upload_into(fac, pos, stage[:fill])
-                pos += fill
-                fill = 0
-            big = np.concatenate([factors[b] for b in blocks], axis=1)
-            ops.upload_into(fac, pos, big.ravel())
-            pos += need
-        else:
-            if fill + need > stage.size:
-                ops.upload_into(fac, pos, stage[:fill])
-                pos += fill
-                fill = 0
-            np.concatenate([factors[b] for b in blocks], axis=1,
-                           out=stage[fill:fill + need].reshape(int(size[c]), int(sp.cown[c])))
-            fill += need
+        o = int(sp.foff[c]) - base
+        np.concatenate([factors[b] for b in blocks], axis=1,
+                       out=stage[o:o + int(size[c] * sp.cown[c])].reshape(int(size[c]), int(sp.cown[c])))
         if weights is not None:
             w0 = int(sp.woff[c])
             for b in blocks:
                 kb = factors[b].shape[1]
                 wts[w0:w0 + kb] = weights[b]
                 w0 += kb
-    if fill:
-        ops.upload_into(fac, pos, stage[:fill])
-        pos += fill
-    assert pos == total
+
+    with ThreadPoolExecutor(max_workers=max(1, workers)) as pool:
+        i = 0
+        while i < owners.size:
+            c0 = int(owners[i])
+            base = int(sp.foff[c0])
+            need0 = int(size[c0] * sp.cown[c0])
+            if need0 > stage.size:  # a block larger than the staging buffer goes on its own
+                blocks = sp.order[sp.first[c0]:sp.first[c0 + 1]]
+                big = np.concatenate([factors[b] for b in blocks], axis=1)
+                ops.upload_into(fac, base, big.ravel())
+                if weights is not None:
+                    wts[int(sp.woff[c0]):int(sp.woff[c0 + 1])] = np.concatenate([weights[b] for b in blocks])
+                i += 1
+                continue
+            # the clusters that fit the staging buffer together (foff is contiguous in cluster order)
+            j = int(np.searchsorted(sp.foff[owners + 1], base + stage.size, side="right"))
+            j = max(j, i + 1)
+            batch = owners[i:j]
+            list(pool.map(lambda c: fill_one(int(c), base), batch, chunksize=max(1, batch.size // (8 * max(1, workers)))))
+            fill = int(sp.foff[int(batch[-1]) + 1]) - base
+            ops.upload_into(fac, base, stage[:fill])
+            i = j
     return fac, ops.to_device(wts)
 
 

@@ -83,6 +83,19 @@ def test_level_algorithm_matches_host_recompression(seed, leaf, eps):
         assert rel(h2_matvec_ref(op, xv), h2_matvec_ref(ref, xv)) < 1e-10
 
 
+def test_packing_in_batches_and_oversized_blocks(monkeypatch):
+    """The factor upload goes through a staging buffer in batches of whole
+    clusters; a cluster's packed block larger than the buffer goes on its
+    own.  Same operator as with one batch."""
+    tree, n, lowrank, dense, weights = _blocks(1, n=600, leaf=24)
+    want = gr.recompress_gpu(tree, n, lowrank, dense, 2e-4, weights, ops=NumpyOps())
+    monkeypatch.setenv("H2B_RC_STAGE_DOUBLES", "2000")   # the largest packed block has 2590 doubles
+    got = gr.recompress_gpu(tree, n, lowrank, dense, 2e-4, weights, ops=NumpyOps())
+    assert all(np.array_equal(a[2], b[2]) for a, b in zip(got.coupling, want.coupling))
+    assert all(np.array_equal(got.row_basis[c], want.row_basis[c]) for c in want.row_basis)
+    assert all(np.array_equal(got.col_transfer[c], want.col_transfer[c]) for c in want.col_transfer)
+
+
 def test_normalise_block_keeps_the_product():
     rng = np.random.default_rng(0)
     a, b = rng.standard_normal((30, 5)), rng.standard_normal((20, 5))
