@@ -96,6 +96,21 @@ def test_packing_in_batches_and_oversized_blocks(monkeypatch):
     assert all(np.array_equal(got.col_transfer[c], want.col_transfer[c]) for c in want.col_transfer)
 
 
+def test_no_admissible_blocks_and_rank_zero_blocks():
+    """Edge cases: an operator without admissible blocks, and one whose
+    admissible blocks all have rank 0 -- every basis is empty and the product
+    is the near field's, as with the host recompression."""
+    tree, n, lowrank, dense, _ = _blocks(1, n=300, leaf=24)
+    x = np.random.default_rng(0).standard_normal(n)
+    for lr, w in (([], []),
+                  ([(t, s, a[:, :0], b[:, :0]) for t, s, a, b in lowrank],
+                   [(np.zeros((0, 0)), np.zeros((0, 0)))] * len(lowrank))):
+        op = gr.recompress_gpu(tree, n, lr, dense, 2e-4, w, ops=NumpyOps())
+        ref = recompress(tree, n, lr, dense, 2e-4, workers=1, weights=w)
+        assert op.storage_bytes() == ref.storage_bytes() and len(op.coupling) == len(ref.coupling)
+        assert np.array_equal(h2_matvec_ref(op, x), h2_matvec_ref(ref, x))
+
+
 def test_normalise_block_keeps_the_product():
     rng = np.random.default_rng(0)
     a, b = rng.standard_normal((30, 5)), rng.standard_normal((20, 5))
