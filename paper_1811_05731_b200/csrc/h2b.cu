@@ -141,6 +141,10 @@ struct KParams {
   const int64_t* __restrict__ u_range;
   int32_t cap_mat, cap_vec, cap_items;
   int32_t sweep_prefetch;               // generic sweep: the next item's static inputs prefetched to L2
+  // programmatic dependent launch (H2B_PDL=1): bit 0, a sweep lets the next
+  // launch start while it runs; bit 1, a dataflow launch started that way
+  // waits for the sweep before its first item that is not near field
+  int32_t pdl;
 };
 
 // scheduling switches
@@ -1203,6 +1207,7 @@ __global__ void __launch_bounds__(NRHS >= 8 ? kMrhsThreads : 256, NRHS >= 8 ? kM
   bool has_ring = false;
   double* abuf;
   unsigned rpar = 0;  // ring stage parities (all lanes)
+  bool pdl_waited = false;  // programmatic dependent launch: this warp has waited for the preceding sweep
   int stage_cap = kStageBytes;  // far-field staging capacity (a ring warp: both stages)
   {
     unsigned char* st = smem_raw + (size_t)nw * sizeof(WarpSmem);
@@ -1424,6 +1429,12 @@ __global__ void __launch_bounds__(NRHS >= 8 ? kMrhsThreads : 256, NRHS >= 8 ? kM
     if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     // descriptor, inline segments and successor range in one round trip
     const DTask T = p.tasks[item];
+    if ((p.pdl & 2) && !pdl_waited && T.kind != h2b::kNear) {
+      // started under the upward sweep (programmatic dependent launch): near
+      // items need only xp; anything else reads the sweep's x^
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      pdl_waited = true;
+    }
     DSeg sin{0, 0, 0, 0, 0};
     if (lane < kInlineSegs) sin = p.seg_inline[(int64_t)item * kInlineSegs + lane];
     const int s0 = __ldg(p.succ0 + item), s1 = __ldg(p.succ0 + item + 1);
@@ -1819,6 +1830,8 @@ __global__ void __launch_bounds__(256, NRHS >= 8 ? kMrhsSweepCtas : 2) h2b_sweep
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
+  // (H2B_PDL) the next launch may start now: its near field needs nothing from this sweep
+  if (p.pdl & 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   WarpSmem& w = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
   unsigned char* rb = smem_raw + (size_t)nw * sizeof(WarpSmem) + (size_t)wib * ring_bytes(4096);
   double* buf[2] = {reinterpret_cast<double*>(rb), reinterpret_cast<double*>(rb + kSweepStage)};
@@ -2019,6 +2032,7 @@ __global__ void __launch_bounds__(256) h2b_sweep_resident_kernel(KParams p) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
+  if (p.pdl & 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const SweepGeom G = sweep_geom(NRHS, nw, p.cap_mat, p.cap_vec, p.cap_items);
   double* Msm = reinterpret_cast<double*>(smem_raw);
   double* Vsm = reinterpret_cast<double*>(smem_raw + G.off_v);
@@ -2414,6 +2428,8 @@ struct h2b_op {
   int ring_stage = kRingStageBytes;  // NRHS < 8: ring stage payload (sched_flags bits 18-19)
   int mrhs_wpc = 8;                  // 8/16 RHS dataflow launches: warps per CTA (H2B_MRHS_WARPS, <= 12)
   int mrhs_stage = kMrhsStage;       // ... and their ring stage payload (6 KB above 10 warps: shared memory)
+  int pdl_now = 0;                   // set per launch by launch_group: 1 this sweep triggers its dependent, 2 this dataflow launch is the dependent
+  int pdl = 0;                       // the dataflow launch starts under the upward sweep (programmatic dependent launch)
   int sweep_prefetch = 0;            // generic sweep: L2 prefetch of the next item's static inputs (H2B_SWEEP_PREFETCH mask)
   std::vector<PhaseDev> ph;
   // single GPU, 8/16 right-hand sides: near field (lean kernel), then the rest
@@ -2659,6 +2675,7 @@ KParams phase_params(h2b_op* op, const PhaseDev& F, double* y) {
   p.cap_vec = F.cap_vec;
   p.cap_items = F.cap_items;
   p.sweep_prefetch = op->sweep_prefetch;
+  p.pdl = op->pdl_now;
   return p;
 }
 
@@ -2674,7 +2691,23 @@ int launch_phase_dev(h2b_op* op, const PhaseDev& F, double* y, cudaStream_t st) 
   const cudaError_t stale = cudaGetLastError();  // clear errors of unrelated earlier calls
   // the attribute is per function and shared by every operator of the process
   H2B_CUDA(cudaFuncSetAttribute(h2b_dataflow_kernel<NRHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  h2b_dataflow_kernel<NRHS><<<op->grid[gi], wpc * 32, smem, st>>>(p);
+  if (op->pdl_now == 2) {
+    // programmatic dependent launch: CTAs may become resident while the
+    // preceding sweep still runs; the kernel waits for it where it must
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)op->grid[gi]);
+    cfg.blockDim = dim3((unsigned)(wpc * 32));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    H2B_CUDA(cudaLaunchKernelEx(&cfg, h2b_dataflow_kernel<NRHS>, p));
+  } else {
+    h2b_dataflow_kernel<NRHS><<<op->grid[gi], wpc * 32, smem, st>>>(p);
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(H2B_ECUDA, std::string("kernel launch (nrhs=") + std::to_string(NRHS) + ", grid=" +
@@ -2785,11 +2818,24 @@ int launch_group(h2b_op* op, int group, const double* x, double* y, cudaStream_t
     mark();
     if ((rc = launch_permute<NRHS>(op, x, st)) != H2B_OK) return rc;
   }
-  for (const PhaseDev& F : list)
-    if (F.group == group) {
-      mark();
-      if ((rc = launch_one<NRHS>(op, F, y, st)) != H2B_OK) return rc;
-    }
+  // (H2B_PDL) an upward sweep directly followed by the dataflow launch of the
+  // same group: the pair is launched as primary and programmatic dependent
+  const bool pdl_ok = op->pdl && NRHS <= 4 && op->world <= 1 && !op->tev && op->split_only == 0;
+  for (size_t k = 0; k < list.size(); ++k) {
+    const PhaseDev& F = list[k];
+    if (F.group != group) continue;
+    op->pdl_now = 0;
+    if (pdl_ok && F.mode == 1 && F.ntasks > 0 && k + 1 < list.size() && list[k + 1].group == group &&
+        list[k + 1].mode == 0 && list[k + 1].ntasks > 0)
+      op->pdl_now = 1;
+    else if (pdl_ok && F.mode == 0 && k > 0 && list[k - 1].group == group && list[k - 1].mode == 1 &&
+             list[k - 1].ntasks > 0 && F.ntasks > 0)
+      op->pdl_now = 2;
+    mark();
+    rc = launch_one<NRHS>(op, F, y, st);
+    op->pdl_now = 0;
+    if (rc != H2B_OK) return rc;
+  }
   mark();
   return H2B_OK;
 }
@@ -3080,6 +3126,15 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
     const int sel = (sf >> 18) & 3;
     op->ring_stage = sel == 1 ? 6144 : sel == 2 ? 4096 : kRingStageBytes;
     {
+      // Programmatic dependent launch of the dataflow kernel under the upward sweep: its
+      // near-priority warps stream near-field items (which need only xp) while the sweep
+      // -- latency-bound, HBM mostly idle -- still runs; every other item waits for the
+      // sweep (griddepcontrol.wait).  On for streaming operators: config 3 2.240 -> 2.213 ms,
+      // config 5 4.636 -> 4.576 ms, the same bits; off for small ones, where the product is
+      // the far-field chain and the early near field only slows the sweep (config 2
+      // 0.179 -> 0.220 ms).  H2B_PDL=0 / 1 forces it.
+      const char* pd = std::getenv("H2B_PDL");
+      op->pdl = pd ? (pd[0] == '1') : (streaming_defaults(d, o) ? 1 : 0);
       const char* e = std::getenv("H2B_SWEEP_PREFETCH");  // A/B switch, read at create (tools/sweep.py --env)
       // bit 0: x ranges, 1: bias slots, 2: permutation entries.  Off by default: measured on
       // config 3 the up sweep gets faster (0.110 -> 0.093 ms) but the product does not
