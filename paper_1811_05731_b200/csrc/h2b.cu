@@ -2820,7 +2820,8 @@ int launch_group(h2b_op* op, int group, const double* x, double* y, cudaStream_t
   }
   // (H2B_PDL) an upward sweep directly followed by the dataflow launch of the
   // same group: the pair is launched as primary and programmatic dependent
-  const bool pdl_ok = op->pdl && NRHS <= 4 && op->world <= 1 && !op->tev && op->split_only == 0;
+  // (multi-GPU: group 0 is [upward sweep][dataflow launch of phase 0] -- the same pair)
+  const bool pdl_ok = op->pdl && NRHS <= 4 && !op->tev && op->split_only == 0;
   for (size_t k = 0; k < list.size(); ++k) {
     const PhaseDev& F = list[k];
     if (F.group != group) continue;
