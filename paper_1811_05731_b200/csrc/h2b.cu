@@ -3135,7 +3135,7 @@ int create_impl(const h2b_desc* d, const h2b_options* o, h2b_op** out) {
       // the far-field chain and the early near field only slows the sweep (config 2
       // 0.179 -> 0.220 ms).  H2B_PDL=0 / 1 forces it.
       const char* pd = std::getenv("H2B_PDL");
-      op->pdl = pd ? (pd[0] == '1') : (streaming_defaults(d, o) ? 1 : 0);
+      op->pdl = pd ? (pd[0] == '1') : (desc_stream_bytes_per_rank(d, o) >= H2B_STREAM_DEFAULT_BYTES ? 1 : 0);
       const char* e = std::getenv("H2B_SWEEP_PREFETCH");  // A/B switch, read at create (tools/sweep.py --env)
       // bit 0: x ranges, 1: bias slots, 2: permutation entries.  Off by default: measured on
       // config 3 the up sweep gets faster (0.110 -> 0.093 ms) but the product does not
