@@ -92,7 +92,9 @@ def main():
     T = plan["t_m"].size
     tr = np.zeros((T, 8), np.uint64)
     nat.check(lib.h2b_trace_read(dev._h, tr.ctypes.data, T))
-    if plan.get("mode", 0) == 1 and plan.get("resident") and os.environ.get("H2B_SWEEP_RESIDENT", "1") != "0":
+    # the resident sweep kernel ran only if the units fit shared memory at this nrhs (h2b_stats.resident_mask)
+    res_ran = bool(dev.stats().get("resident_mask", 0) & nrhs)
+    if plan.get("mode", 0) == 1 and plan.get("resident") and res_ran and os.environ.get("H2B_SWEEP_RESIDENT", "1") != "0":
         # resident sweep: one record per unit, in the slots of its first item:
         # start, end, waves | cta, copies issued, copies landed, end of wave 0, 1, last but one
         first = plan["wave0"][plan["unit0"][:-1]]
